@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""TSQR / CAQR benchmark on B200 (driver contract).
+
+Default workload (N=1): BASELINE config 3, TSQR fp64 of A 16777216 x 128
+iid N(0,1) (16 GiB, larger than L2), leaf blocks of 8192 x 128 + binary tree,
+R only.  One "step" = one full TSQR of A resident in HBM.
+
+  python bench.py                       # N=1, C3, R only
+  python bench.py --config c4           # other configs (c1..c5)
+  torchrun --nproc-per-node N bench.py --gpus N   # 1-D shards + cross-GPU tree
+  python bench.py --impl reference      # the reference's CPU path (oracle port)
+
+Metric: GFLOP/s with the standard Householder count F = 2mn^2 - 2n^3/3
+(whole job).  ``roofline`` reports the leaf kernel against the FP64 peak,
+``cpu_baseline`` the oracle port of the reference path on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
+METRIC = "TSQR fp64 GFLOP/s & % of roofline"
+
+CONFIGS = {
+    "c1": dict(m=65536, n=32, leaf=8192, q="explicit", dist="normal",
+               name="C1 TSQR 65536x32 N(0,1), 8 leaves of 8192, R + explicit Q"),
+    "c2": dict(m=1048576, n=64, leaf=4096, q="explicit", dist="cond",
+               name="C2 TSQR 1048576x64 kappa=1e12, leaves of 4096, R + explicit Q"),
+    "c3": dict(m=16777216, n=128, leaf=8192, q="none", dist="normal",
+               name="C3 TSQR 16777216x128 N(0,1), leaves of 8192x128, R only"),
+    "c4": dict(m=134217728, n=8, leaf=16384, q="none", dist="uniform",
+               name="C4 TSQR 134217728x8 U(-1,1), leaves of 16384x8, R only"),
+    "c5": dict(m=16384, n=16384, leaf=2048, q="implicit", dist="normal",
+               name="C5 CAQR 16384x16384 N(0,1), b=128, TSQR leaf 2048, R + implicit Q"),
+}
+
+
+def flops(m, n):
+    return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
+
+
+def env_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+def make_input(cfg, device, seed=0, rows=None):
+    import torch
+
+    m = rows if rows is not None else cfg["m"]
+    n = cfg["n"]
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if cfg["dist"] == "uniform":
+        A = torch.rand((m, n), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+    elif cfg["dist"] == "cond":
+        from paper_0809_2407_b200.core import CondSpec, gen_cond_matrix
+
+        A = torch.from_numpy(gen_cond_matrix(CondSpec(m, n, kappa=1e12, seed=seed))).to(device)
+    else:
+        A = torch.randn((m, n), generator=g, dtype=torch.float64, device=device)
+    return A
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference path (oracle port) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_baseline(cfg, budget_s=15.0, threads=None):
+    import oracle
+
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    n = cfg["n"]
+    leaf = min(cfg["leaf"], cfg["m"])
+    rng = np.random.Generator(np.random.Philox(1))
+    ctx = threadpool_limits(limits=threads) if (threadpool_limits and threads) else None
+    if ctx:
+        ctx.__enter__()
+    try:
+        if cfg is CONFIGS["c5"]:
+            N = 2048
+            A = rng.standard_normal((N, N))
+            t0 = time.perf_counter()
+            oracle.blocked_qr(A, 128)
+            dt = time.perf_counter() - t0
+            return {"value": flops(N, N) / dt / 1e9, "unit": "GFLOP/s",
+                    "sample": f"reference qr_blocked(A, nb=128) on {N}x{N} (C5 scaled 1/8)",
+                    "seconds": dt}
+        # one leaf first to size the sample
+        Aleaf = rng.standard_normal((leaf, n))
+        t0 = time.perf_counter()
+        Y, tau, R = oracle.geqr2(Aleaf)
+        t_leaf = time.perf_counter() - t0
+        Rs = [R]
+        t_comb = 0.0
+        nleaves = max(2, min(int(budget_s / max(t_leaf, 1e-3)), cfg["m"] // leaf))
+        t0 = time.perf_counter()
+        for _ in range(nleaves - 1):
+            Y, tau, R = oracle.geqr2(rng.standard_normal((leaf, n)))
+            Rs.append(R)
+        t_rest = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for (lvl, a, b) in oracle.binary_events(nleaves):
+            _, _, Rs[a] = oracle.stacked_qr(Rs[a], Rs[b])
+        t_comb = time.perf_counter() - t0
+        dt = t_leaf + t_rest + t_comb
+        m_s = nleaves * leaf
+        q = cfg["q"] != "none"
+        return {"value": flops(m_s, n) / dt / 1e9, "unit": "GFLOP/s",
+                "sample": (f"reference path (geqr2 leaves + stacked_qr binary tree), {nleaves} "
+                           f"leaves of {leaf}x{n} = {m_s} rows, R only"
+                           + ("; Q not formed in the sample" if q else "")),
+                "seconds": dt}
+    finally:
+        if ctx:
+            ctx.__exit__(None, None, None)
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = env_dist()
+    if rank != 0:
+        return
+    ncpu = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(cfg, budget_s=max(2.0, 60.0 / max(1, args.steps + args.warmup)),
+                          threads=ncpu)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = float(np.median([c["value"] for c in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.median([c["seconds"] for c in vals]) * 1e3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Philox N(0,1) per config)",
+        "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "leaf_rows": cfg["leaf"]},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncpu, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our path
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import _leaves_for, explicit_q_device, factor_device
+
+    ws, rank, local = env_dist()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _lib.load()
+    m, n = cfg["m"], cfg["n"]
+    is_caqr = cfg is CONFIGS["c5"]
+    if is_caqr and ws > 1:
+        raise SystemExit("c5 multi-GPU grid run is not part of this bench yet")
+    # shard rows (1-D block rows); A resident in HBM
+    from paper_0809_2407_b200.dist import shard_rows, tsqr_sharded
+
+    lo, hi = shard_rows(m, ws, rank)
+    A = make_input(cfg, dev, seed=rank, rows=hi - lo) if not is_caqr else make_input(cfg, dev)
+    P = _leaves_for(hi - lo, n, cfg["leaf"])
+    want_q = cfg["q"] != "none"
+    stream = torch.cuda.current_stream(dev)
+
+    leaf_ev = []
+
+    def step(record=False):
+        if is_caqr:
+            from paper_0809_2407_b200.caqr import caqr_factor
+
+            return caqr_factor(A, b=128, leaf_rows=cfg["leaf"])
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        f = factor_device(A, P, want_q=want_q)
+        if record:
+            e1.record(stream)
+            leaf_ev.append((e0, e1))
+        if ws > 1:
+            from paper_0809_2407_b200.dist import cross_tree, gpu_combine
+
+            cross_tree(f.R, gpu_combine)
+        if cfg["q"] == "explicit":
+            explicit_q_device(f)
+        return f
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    leaf_ev.clear()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=not is_caqr)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    F = flops(m, n)
+    value = F / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: the leaf factorization (factor_device's
+    # leaf + tree events bracket; the tree is < 2% of it, see profiles/)
+    roof = None
+    if leaf_ev:
+        t_leaf = float(np.mean([a.elapsed_time(b) for a, b in leaf_ev])) * 1e-3
+        F_leaf = flops(hi - lo, n)
+        ach = F_leaf / t_leaf / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "k_leaf_factor + k_tree_factor (one factor_device call)",
+                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
+                               "entry in MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": F_leaf}
+        if cfg["q"] == "none" and not is_caqr:
+            hbm = 6526.5
+            try:
+                hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+            except Exception:
+                pass
+            t_roof = max(F_leaf / (FP64_PEAK_TFLOPS * 1e12), 8.0 * (hi - lo) * n / (hbm * 1e9))
+            roof["t_roof_ms"] = t_roof * 1e3
+            roof["roofline_frac_time"] = t_roof / t_leaf
+
+    # e2e through the public API with host buffers (pinned), rank 0 view
+    e2e = None
+    if not args.no_e2e:
+        from paper_0809_2407_b200.tsqr import tsqr
+
+        Ah = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A)
+        e_steps = max(1, min(args.steps, 3))
+        if is_caqr:
+            from paper_0809_2407_b200.caqr import caqr_factor
+
+            def e2e_step():
+                res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"])
+                return res.R
+        else:
+            def e2e_step():
+                out = tsqr(Ah, leaf_rows=cfg["leaf"], q=cfg["q"])
+                return out
+        e2e_step()
+        barrier()
+        ts = time.perf_counter()
+        for _ in range(e_steps):
+            out = e2e_step()
+        barrier()
+        dt = (time.perf_counter() - ts) / e_steps
+        d2h = n * n * 8 + (m * n * 8 if cfg["q"] == "explicit" else 0)
+        if is_caqr:
+            d2h = n * n * 8
+        e2e_v = F / dt / 1e9
+        dt_t = torch.tensor([dt], device=dev)
+        if ws > 1:
+            dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+            e2e_v = F / float(dt_t.item()) / 1e9
+        e2e = {"value": e2e_v, "unit": "GFLOP/s", "h2d_bytes_per_step": int(A.numel() * 8) * ws,
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(dt_t.item()) * 1e3}
+        del Ah
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cb = cpu_baseline(cfg, budget_s=args.cpu_budget, threads=1)
+        cpu = {"value": cb["value"], "unit": "GFLOP/s", "cores": 1, "kind": "port",
+               "sample": cb["sample"]}
+    levels = max(0, int(np.ceil(np.log2(P)))) if P > 1 else 0
+    launches = (1 + levels) * args.steps
+    if cfg["q"] == "explicit":
+        launches += (levels + 1) * args.steps
+    if is_caqr:
+        launches = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic iid " + cfg["dist"] + " (torch Philox on device, seed = rank)",
+            "config": {"workload": cfg["name"], "m": m, "n": n, "leaf_rows": cfg["leaf"],
+                       "leaves_per_gpu": P, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
+                       "l2": "inputs larger than L2 (no flush needed)" if 8 * m * n > 256e6
+                       else "inputs smaller than L2"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "gflops_roofline_frac": value / (FP64_PEAK_TFLOPS * 1e3 * ws),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

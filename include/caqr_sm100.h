@@ -1,0 +1,107 @@
+/* caqr_sm100.h -- C-ABI of libcaqr_sm100.so, the B200 (sm_100a) FP64 TSQR/CAQR
+ * hot path of arXiv:0809.2407.
+ *
+ * All matrix pointers are DEVICE pointers to row-major (C-order) float64 data
+ * with an explicit leading dimension in elements (the reference's in-memory
+ * convention, pkg/src/caqr/core.py:3-5).  All calls are asynchronous on the
+ * given cudaStream_t (passed as void*), re-entrant across streams/devices,
+ * and allocate no device memory: the caller owns every buffer.
+ * Return value: 0 ok, 1 bad argument, 2 non-finite input, 3 CUDA error,
+ * 4 communication error; tsqr_last_error() describes the last failure of the
+ * calling thread.
+ *
+ * Reference interfaces replaced (the reference is numpy-only; these are the
+ * kernels its Python API would bind through ctypes):
+ *
+ *   tsqr_f64_leaf_factor       <- qr_unblocked per leaf block
+ *                                 (pkg/src/caqr/householder.py:128-145) composed
+ *                                 with qr_triangle_on_rect (:297-332) as the
+ *                                 flat in-leaf chain of Alg. 2;
+ *                                 leaf blocks follow BlockRowLayout (core.py:36-61)
+ *   tsqr_f64_tree_factor_level <- qr_stacked_triangles, q = 2 (householder.py:263-294)
+ *                                 for every CombineEvent of one level of
+ *                                 ReductionTree.schedule() (trees.py:146-152)
+ *   tsqr_f64_tree_apply_level  <- apply_q / apply_qt on a STACKED factor
+ *                                 (householder.py:377-396, row set :65-70), the
+ *                                 inner-product update of apply_qt_structured (:335-374)
+ *   tsqr_f64_leaf_apply        <- apply_q / apply_qt / explicit_q on a leaf
+ *                                 (householder.py:377-404) and the compact-WY
+ *                                 trailing update _apply_yt(transpose=True) (:175-186)
+ *   tsqr_f64_block_factor      <- qr_unblocked (mode 0) / qr_triangle_on_rect
+ *                                 (mode 2) on blocks of <= 128 rows
+ */
+#ifndef CAQR_SM100_H
+#define CAQR_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAQR_SM100_ABI_VERSION 1
+
+#define CAQR_OK 0
+#define CAQR_ERR_ARG 1
+#define CAQR_ERR_NONFINITE 2
+#define CAQR_ERR_CUDA 3
+#define CAQR_ERR_COMM 4
+
+int caqr_sm100_abi_version(void);
+const char* tsqr_last_error(void);
+
+/* Kernel geometry for n columns: padded width np (32/64/128), dense first-tile
+ * height h0 and chain tile height ht.  Leaf i's implicit Q is its dense tile
+ * (rows [0, min(b_i, h0)), LAPACK layout: R above, Y strictly below the
+ * diagonal, unit diagonal implicit) followed by ceil((b_i - h0)/ht) chain tiles
+ * (TRI_ON_RECT factors whose rectangle V is stored in the tile's rows). */
+int tsqr_f64_geometry(int64_t n, int64_t* np, int64_t* h0, int64_t* ht);
+
+/* Factor the P leaves of A (m x n, 1 <= n <= 128): leaf i = rows
+ * [i*floor(m/P), ...) with the last leaf absorbing the remainder.
+ * R: P x n x n (slot i = leaf i's upper-triangular R).
+ * Y (nullable, m x n, ldy) and tau (P x tau_stride, tile t of leaf i at
+ * tau[i*tau_stride + t*n]) receive the implicit Q; pass both or neither.
+ * flag (nullable, device int): OR-ed with 1 if A holds NaN/Inf. */
+int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                         double* Y, int64_t ldy, double* tau, int64_t tau_stride,
+                         double* R, int* flag, void* stream);
+
+/* One level of the binary reduce tree: for every event e (int32 triples
+ * {receiver, partner, node} in `events`, device memory), QR of
+ * [R[receiver]; R[partner]] -> R[receiver]; node factor -> Ynode[node] (n x n
+ * upper-triangular lower block of the STACKED Y) and taunode[node] (n). */
+int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,
+                               double* Ynode, double* taunode, void* stream);
+
+/* [C_a; C_b] <- Q_node^T [C_a; C_b] (transpose=1) or Q_node [C_a; C_b] for the
+ * events of one level; C_a = C + receiver*slot_rows*ldc, C_b likewise (n rows
+ * each, ncols columns).  zero_partner=1 treats C_b as zero on input. */
+int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_t n,
+                              const int32_t* events, int64_t nev, double* C, int64_t ldc,
+                              int64_t slot_rows, int64_t ncols, int transpose, int zero_partner,
+                              void* stream);
+
+/* C[leaf rows] <- Q_leaf^T C (transpose=1) or Q_leaf C for every leaf of the
+ * factor (Y, tau as written by tsqr_f64_leaf_factor).  For Q only: S (nullable)
+ * supplies the leaf's top n rows (leaf i at S + i*s_slot_rows*lds) instead of
+ * C's own; zero_init=1 treats the rest of C as zero (explicit-Q formation);
+ * tri_skip=1 skips columns known to stay zero (S upper triangular). */
+int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
+                        int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
+                        const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
+                        int zero_init, int tri_skip, void* stream);
+
+/* Single-CTA factorization of a block of rows <= 128: mode 0 = DENSE
+ * (qr_unblocked: R out, Y m x n LAPACK layout), mode 2 = TRIRECT
+ * (qr_triangle_on_rect: R in/out, Y = rectangle). */
+int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
+                          double* Y, int64_t ldy, double* tau, int mode, int* flag, void* stream);
+
+/* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */
+int caqr_f64_peak_probe(double* scratch, int mode, int iters, int blocks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAQR_SM100_H */

@@ -1,0 +1,108 @@
+"""ctypes binding of libcaqr_sm100.so (the C-ABI declared in include/caqr_sm100.h).
+
+The product path has no CPU fallback: if the library is missing or cannot be
+loaded, every compute entry point raises ``NativeLibraryError``.  The library
+is built in-tree by ``paper_0809_2407_b200.build`` / ``__graft_entry__.build()``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcaqr_sm100.so")
+ABI_VERSION = 1
+
+# exported symbols, in header order (tests check each one is present)
+SYMBOLS = (
+    "caqr_sm100_abi_version",
+    "tsqr_last_error",
+    "tsqr_f64_geometry",
+    "tsqr_f64_leaf_factor",
+    "tsqr_f64_tree_factor_level",
+    "tsqr_f64_tree_apply_level",
+    "tsqr_f64_leaf_apply",
+    "tsqr_f64_block_factor",
+    "caqr_f64_peak_probe",
+)
+
+OK, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_COMM = 0, 1, 2, 3, 4
+
+
+class NativeLibraryError(RuntimeError):
+    """The sm_100a library is missing or failed to load (no CPU fallback)."""
+
+
+_lib = None
+
+
+def _sig(lib):
+    i64, i32, vp, dp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p
+    ip = ctypes.c_void_p
+    lib.caqr_sm100_abi_version.restype = i32
+    lib.caqr_sm100_abi_version.argtypes = []
+    lib.tsqr_last_error.restype = ctypes.c_char_p
+    lib.tsqr_last_error.argtypes = []
+    lib.tsqr_f64_geometry.restype = i32
+    lib.tsqr_f64_geometry.argtypes = [i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                      ctypes.POINTER(i64)]
+    lib.tsqr_f64_leaf_factor.restype = i32
+    lib.tsqr_f64_leaf_factor.argtypes = [dp, i64, i64, i64, i64, dp, i64, dp, i64, dp, ip, vp]
+    lib.tsqr_f64_tree_factor_level.restype = i32
+    lib.tsqr_f64_tree_factor_level.argtypes = [dp, i64, ip, i64, dp, dp, vp]
+    lib.tsqr_f64_tree_apply_level.restype = i32
+    lib.tsqr_f64_tree_apply_level.argtypes = [dp, dp, i64, ip, i64, dp, i64, i64, i64, i32, i32, vp]
+    lib.tsqr_f64_leaf_apply.restype = i32
+    lib.tsqr_f64_leaf_apply.argtypes = [dp, i64, dp, i64, i64, i64, i64, dp, i64, i64, dp, i64,
+                                        i64, i32, i32, i32, vp]
+    lib.tsqr_f64_block_factor.restype = i32
+    lib.tsqr_f64_block_factor.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i32, ip, vp]
+    lib.caqr_f64_peak_probe.restype = i32
+    lib.caqr_f64_peak_probe.argtypes = [dp, i32, i32, i32, vp]
+
+
+def load():
+    """Load (once) and return the native library; raise if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryError(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover - environment specific
+        raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+    missing = [s for s in SYMBOLS if not hasattr(lib, s)]
+    if missing:
+        raise NativeLibraryError(f"{LIB_PATH} lacks symbols {missing}")
+    _sig(lib)
+    if lib.caqr_sm100_abi_version() != ABI_VERSION:
+        raise NativeLibraryError("ABI version mismatch; rebuild the library")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C-ABI status code to the reference's exception types."""
+    if rc == OK:
+        return
+    msg = (_lib.tsqr_last_error() or b"").decode(errors="replace")
+    from .core import DimensionError
+    from .executor import ExecutorError
+
+    if rc == ERR_ARG:
+        raise DimensionError(f"{what}: {msg}")
+    if rc == ERR_NONFINITE:
+        raise ValueError(f"{what}: matrix contains NaN or Inf entries")
+    raise ExecutorError(f"{what}: {msg} (status {rc})")
+
+
+def geometry(n: int):
+    lib = load()
+    np_, h0, ht = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    check(lib.tsqr_f64_geometry(n, ctypes.byref(np_), ctypes.byref(h0), ctypes.byref(ht)),
+          "tsqr_f64_geometry")
+    return np_.value, h0.value, ht.value

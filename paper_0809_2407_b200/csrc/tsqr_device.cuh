@@ -1,0 +1,431 @@
+// Device building blocks for the FP64 TSQR / CAQR kernels (sm_100a).
+//
+// Register layout shared by every kernel ("column-owned warp tiles"):
+//   a CTA has WARPS = 8 warps; warp w holds RW consecutive rows of a block,
+//   lane l holds the columns c = 32*s + l for the S = NP/32 column slots.
+//   Column dot products over a warp's rows are therefore lane-local FMA
+//   chains (no shuffles); only reductions ACROSS warps go through shared
+//   memory.  NP is n rounded up to 32/64/128; padded columns are zero and stay
+//   exactly zero through every reflector (their R row entries are zero).
+//
+// Two execution patterns:
+//   * cta_factor / cta_apply: CTA-cooperative sweep over a block held by all
+//     8 warps (dense first tile of a leaf, stacked-triangle tree combine,
+//     triangle-on-rectangle).  Two __syncthreads per reflector (factor) or one
+//     (apply, double-buffered partials).
+//   * ring_factor_tile / ring_apply_tile: the flat-tree chain of
+//     triangle-on-rectangle steps (Alg. 2 of the paper) as a systolic ring:
+//     each warp owns one HW-row tile, the n pivot rows (R, or the top block of
+//     C) live in shared memory and flow warp -> warp through per-row version
+//     counters, so no CTA barrier is ever taken inside the chain.
+//
+// Reflector conventions follow pkg/src/caqr/householder.py:9-11,89-114.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tsqr {
+
+constexpr int WARPS = 8;
+constexpr int THREADS = WARPS * 32;
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+enum Mode { DENSE = 0, STACKED = 1, TRIRECT = 2 };
+
+// Ring tile height per padded width: 64 doubles of tile per lane.
+template <int NP> struct Geo;
+template <> struct Geo<32>  { static constexpr int S = 1, HW = 32; };
+template <> struct Geo<64>  { static constexpr int S = 2, HW = 32; };
+template <> struct Geo<128> { static constexpr int S = 4, HW = 16; };
+
+// house_gen scalars (householder.py:97-113): given x0 and sigma = ||x[1:]||^2
+// return beta, tau and the scale 1/(x0 - beta) applied to x[1:].
+__device__ __forceinline__ void house_scalars(double x0, double sigma, double& beta,
+                                              double& tau, double& scale) {
+  if (sigma == 0.0) {
+    scale = 0.0;
+    if (x0 == 0.0) { tau = 0.0; beta = 0.0; }
+    else if (x0 >= 0.0) { tau = 0.0; beta = x0; }
+    else { tau = 2.0; beta = -x0; }
+    return;
+  }
+  const double nrm = sqrt(fma(x0, x0, sigma));
+  beta = (x0 >= 0.0) ? -nrm : nrm;
+  scale = 1.0 / (x0 - beta);
+  tau = (beta - x0) / beta;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;"
+               :: "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+// Warp waits until ver[j] == target (lane 0 polls, then the warp syncs).
+__device__ __forceinline__ void ring_wait(const int* ver, int target, int lane) {
+  if (lane == 0) {
+    while (ld_acquire(ver) != target) { }
+  }
+  __syncwarp();
+  __threadfence_block();
+}
+__device__ __forceinline__ void ring_signal(int* ver, int value, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    st_release(ver, value);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile load / store (row-major global, leading dimension ld, zero padding)
+// ---------------------------------------------------------------------------
+template <int RW, int S>
+__device__ __forceinline__ void load_rows(double (&X)[RW][S], const double* __restrict__ src,
+                                          int64_t ld, int rows_valid, int ncols, int col0,
+                                          bool& bad) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int c = col0 + 32 * s + lane;
+      double x = 0.0;
+      if (k < rows_valid && c < ncols) x = __ldg(src + (int64_t)k * ld + c);
+      bad |= !isfinite(x);
+      X[k][s] = x;
+    }
+  }
+}
+
+template <int RW, int S>
+__device__ __forceinline__ void store_rows(const double (&X)[RW][S], double* dst, int64_t ld,
+                                           int rows_valid, int ncols, int col0, int row_lo = 0) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+    if (k < row_lo || k >= rows_valid) continue;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int c = col0 + 32 * s + lane;
+      if (c < ncols) dst[(int64_t)k * ld + c] = X[k][s];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-cooperative factorization sweep.
+//   DENSE  : pivot row j is row j of the block (internal), support rows r >= j
+//            -> qr_unblocked on the block (householder.py:128-145).
+//   STACKED: pivot rows external (Ps, stride NP), support rows r <= j
+//            -> qr_stacked_triangles q=2 with X = lower triangle (:263-294).
+//   TRIRECT: pivot rows external, support all rows
+//            -> qr_triangle_on_rect with X = rectangle (:297-332).
+// Block row r = w*RW + k.  tau_out[j] written by thread 0 (nullable).
+// smem: red[WARPS], sx0[1], part[WARPS*NP], vbuf[WARPS*RW].
+// ---------------------------------------------------------------------------
+template <int NP, int RW, int MODE>
+__device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps, int n,
+                                           double* tau_out, double* red, double* sx0,
+                                           double* part, double* vbuf) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * s + jj;
+      if (j >= n) return;
+      const int pw = j / RW;
+      // -- 1. partial sigma of column j over this warp's support rows
+      double sg = 0.0;
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int r = w * RW + k;
+        const bool in = (MODE == DENSE) ? (r > j) : (MODE == STACKED ? (r <= j) : true);
+        const double x = X[k][s];
+        if (in) sg = fma(x, x, sg);
+      }
+      if (lane == jj) red[w] = sg;
+      if (MODE == DENSE && w == pw && lane == jj) {
+        double x0 = 0.0;
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (k == j - pw * RW) x0 = X[k][s];
+        *sx0 = x0;
+      }
+      __syncthreads();
+      double sigma = 0.0;
+#pragma unroll
+      for (int q = 0; q < WARPS; ++q) sigma += red[q];
+      const double x0 = (MODE == DENSE) ? *sx0 : Ps[j * NP + j];
+      double beta, tau, scale;
+      house_scalars(x0, sigma, beta, tau, scale);
+      const bool wact = (MODE == DENSE) ? (w >= pw) : (MODE == STACKED ? (w <= pw) : true);
+      double v[RW];
+      double pold[S];
+      if (wact) {
+        // -- 2. reflector entries for this warp's rows (lane jj owns column j)
+        if (lane == jj) {
+#pragma unroll
+          for (int k = 0; k < RW; ++k) {
+            const int r = w * RW + k;
+            const bool in = (MODE == DENSE) ? (r > j) : (MODE == STACKED ? (r <= j) : true);
+            double vk = 0.0;
+            if (in) vk = X[k][s] * scale;
+            else if (MODE == DENSE && r == j) vk = 1.0;
+            vbuf[w * RW + k] = vk;
+            if (in) X[k][s] = vk;
+            else if (MODE == DENSE && r == j) X[k][s] = beta;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < RW; ++k) v[k] = vbuf[w * RW + k];
+        // -- 3. partial dots with the trailing columns
+#pragma unroll
+        for (int s2 = s; s2 < S; ++s2) {
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < RW; k += 2) {
+            p0 = fma(v[k], X[k][s2], p0);
+            if (k + 1 < RW) p1 = fma(v[k + 1], X[k + 1][s2], p1);
+          }
+          double p = p0 + p1;
+          if (MODE != DENSE && w == 0) {
+            pold[s2] = Ps[j * NP + 32 * s2 + lane];
+            p += pold[s2];
+          }
+          part[w * NP + 32 * s2 + lane] = p;
+        }
+      }
+      __syncthreads();
+      if (wact) {
+        const int q0 = (MODE == DENSE) ? pw : 0;
+        const int q1 = (MODE == STACKED) ? pw : WARPS - 1;
+        // -- 4. rank-1 update of the trailing columns
+#pragma unroll
+        for (int s2 = s; s2 < S; ++s2) {
+          const int c = 32 * s2 + lane;
+          if (s2 > s || lane > jj) {
+            double tot = 0.0;
+            for (int q = q0; q <= q1; ++q) tot += part[q * NP + c];
+            const double wv = tau * tot;
+#pragma unroll
+            for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+            if (MODE != DENSE && w == 0) Ps[j * NP + c] = pold[s2] - wv;
+          }
+        }
+        if (MODE != DENSE && w == 0 && lane == jj) Ps[j * NP + j] = beta;
+      }
+      if (threadIdx.x == 0 && tau_out) tau_out[j] = tau;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ring step: one warp applies the n reflectors of its triangle-on-rectangle
+// tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
+// (stride NP) under the version protocol ver[j] == t.
+// On return X holds the tile's V (the stored rectangle of the factor).
+// ---------------------------------------------------------------------------
+template <int NP, int HW>
+__device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], double* Rs, int* ver,
+                                                 double* vb, int n, int t, double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * s + jj;
+      if (j >= n) return;
+      // norm of this lane's slot-s column (only lane jj's is used)
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int k = 0; k < HW; k += 2) {
+        sa = fma(X[k][s], X[k][s], sa);
+        sb = fma(X[k + 1][s], X[k + 1][s], sb);
+      }
+      const double sg = __shfl_sync(FULL, sa + sb, jj);
+      ring_wait(ver + j, t, lane);
+      double rr[S];
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) rr[s2] = Rs[j * NP + 32 * s2 + lane];
+      const double x0 = Rs[j * NP + j];
+      double beta, tau, scale;
+      house_scalars(x0, sg, beta, tau, scale);
+      if (lane == jj) {
+#pragma unroll
+        for (int k = 0; k < HW; ++k) {
+          const double vk = X[k][s] * scale;
+          vb[k] = vk;
+          X[k][s] = vk;
+        }
+      }
+      __syncwarp();
+      double v[HW];
+#pragma unroll
+      for (int k = 0; k < HW; k += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
+        v[k] = t2.x;
+        v[k + 1] = t2.y;
+      }
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) {
+        double p0 = rr[s2], p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < HW; k += 2) {
+          p0 = fma(v[k], X[k][s2], p0);
+          p1 = fma(v[k + 1], X[k + 1][s2], p1);
+        }
+        const double wv = tau * (p0 + p1);
+        if (s2 > s || lane > jj) {
+          rr[s2] -= wv;
+#pragma unroll
+          for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+        }
+      }
+      if (lane == jj) rr[s] = beta;
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2)
+        if (32 * s2 + lane >= j) Rs[j * NP + 32 * s2 + lane] = rr[s2];
+      if (lane == 0 && tau_tile) tau_tile[j] = tau;
+      ring_signal(ver + j, t + 1, lane);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-cooperative application of a DENSE (internal pivot, support r >= j) or
+// STACKED (external pivot rows Ps, support r <= j) factor to a block of C
+// columns held in registers.  Forward order (Q^T) or reverse (Q).
+// Ycol(r, j) gives the stored reflector entry for block row r.
+// Lane columns: col0 + 32*s + lane; tri_skip skips slots whose columns are
+// all < j (valid when C's columns < j are known to be zero, e.g. forming Q).
+// smem part: 2*WARPS*KB (double buffered -> one barrier per reflector).
+// ---------------------------------------------------------------------------
+template <int RW, int KBS, int MODE, bool TRANS, class YF>
+__device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int n, YF Ycol,
+                                          const double* __restrict__ tau, double* part,
+                                          int col0, bool tri_skip) {
+  constexpr int KB = 32 * KBS;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int jx = 0; jx < n; ++jx) {
+    const int j = TRANS ? jx : n - 1 - jx;
+    const int pw = j / RW;
+    const bool wact = (MODE == DENSE) ? (w >= pw) : (w <= pw);
+    double* pb = part + (jx & 1) * WARPS * KB;
+    const double tj = __ldg(tau + j);
+    double v[RW];
+    double pold[KBS];
+    if (wact) {
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int r = w * RW + k;
+        double vk = 0.0;
+        if (MODE == DENSE) {
+          if (r > j) vk = Ycol(r, j);
+          else if (r == j) vk = 1.0;
+        } else {
+          if (r <= j) vk = Ycol(r, j);
+        }
+        v[k] = vk;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < KBS; ++s2) {
+        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < RW; k += 2) {
+          p0 = fma(v[k], X[k][s2], p0);
+          if (k + 1 < RW) p1 = fma(v[k + 1], X[k + 1][s2], p1);
+        }
+        double p = p0 + p1;
+        if (MODE != DENSE && w == 0) {
+          pold[s2] = Ps[j * KB + 32 * s2 + lane];
+          p += pold[s2];
+        }
+        pb[w * KB + 32 * s2 + lane] = p;
+      }
+    }
+    __syncthreads();
+    if (wact && tj != 0.0) {
+      const int q0 = (MODE == DENSE) ? pw : 0;
+      const int q1 = (MODE == DENSE) ? WARPS - 1 : pw;
+#pragma unroll
+      for (int s2 = 0; s2 < KBS; ++s2) {
+        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+        const int c = 32 * s2 + lane;
+        double tot = 0.0;
+        for (int q = q0; q <= q1; ++q) tot += pb[q * KB + c];
+        const double wv = tj * tot;
+#pragma unroll
+        for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+        if (MODE != DENSE && w == 0) Ps[j * KB + c] = pold[s2] - wv;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ring application of one triangle-on-rectangle tile factor (V: HW x n rows
+// at Vt with stride ldv, rows >= vrows treated as zero) to [Cs; X]:
+// Cs = pivot rows (stride KB) in smem, X = this warp's tile of C.
+// ---------------------------------------------------------------------------
+template <int HW, int KBS, bool TRANS>
+__device__ __forceinline__ void ring_apply_tile(double (&X)[HW][KBS], double* Cs, int* ver,
+                                                const double* __restrict__ Vt, int64_t ldv,
+                                                int vrows, const double* __restrict__ tau,
+                                                int n, int order, int col0, bool tri_skip) {
+  constexpr int KB = 32 * KBS;
+  const int lane = threadIdx.x & 31;
+  double vn[HW];
+  double tn;
+  {
+    const int j = TRANS ? 0 : n - 1;
+#pragma unroll
+    for (int k = 0; k < HW; ++k) vn[k] = (k < vrows) ? __ldg(Vt + (int64_t)k * ldv + j) : 0.0;
+    tn = __ldg(tau + j);
+  }
+  for (int jx = 0; jx < n; ++jx) {
+    const int j = TRANS ? jx : n - 1 - jx;
+    double v[HW];
+#pragma unroll
+    for (int k = 0; k < HW; ++k) v[k] = vn[k];
+    const double tj = tn;
+    if (jx + 1 < n) {  // prefetch the next reflector
+      const int jn = TRANS ? j + 1 : j - 1;
+#pragma unroll
+      for (int k = 0; k < HW; ++k) vn[k] = (k < vrows) ? __ldg(Vt + (int64_t)k * ldv + jn) : 0.0;
+      tn = __ldg(tau + jn);
+    }
+    ring_wait(ver + j, order, lane);
+    if (tj != 0.0) {
+#pragma unroll
+      for (int s2 = 0; s2 < KBS; ++s2) {
+        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+        const double cold = Cs[j * KB + 32 * s2 + lane];
+        double p0 = cold, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < HW; k += 2) {
+          p0 = fma(v[k], X[k][s2], p0);
+          p1 = fma(v[k + 1], X[k + 1][s2], p1);
+        }
+        const double wv = tj * (p0 + p1);
+        Cs[j * KB + 32 * s2 + lane] = cold - wv;
+#pragma unroll
+        for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+      }
+    }
+    ring_signal(ver + j, order + 1, lane);
+  }
+}
+
+}  // namespace tsqr
