@@ -98,6 +98,11 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
 int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
                           double* Y, int64_t ldy, double* tau, int mode, int* flag, void* stream);
 
+/* Process-wide tuning knobs (not thread-safe; set before launching work).
+ * CAQR_TUNE_RING_WARPS: warps per CTA of the leaf chain ring (8 or 12). */
+#define CAQR_TUNE_RING_WARPS 1
+int caqr_tune(int key, int value);
+
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */
 int caqr_f64_peak_probe(double* scratch, int mode, int iters, int blocks, void* stream);
 

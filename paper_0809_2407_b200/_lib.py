@@ -24,6 +24,7 @@ SYMBOLS = (
     "tsqr_f64_tree_apply_level",
     "tsqr_f64_leaf_apply",
     "tsqr_f64_block_factor",
+    "caqr_tune",
     "caqr_f64_peak_probe",
 )
 
@@ -58,6 +59,8 @@ def _sig(lib):
                                         i64, i32, i32, i32, vp]
     lib.tsqr_f64_block_factor.restype = i32
     lib.tsqr_f64_block_factor.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i32, ip, vp]
+    lib.caqr_tune.restype = i32
+    lib.caqr_tune.argtypes = [i32, i32]
     lib.caqr_f64_peak_probe.restype = i32
     lib.caqr_f64_peak_probe.argtypes = [dp, i32, i32, i32, vp]
 
@@ -98,6 +101,13 @@ def check(rc: int, what: str) -> None:
     if rc == ERR_NONFINITE:
         raise ValueError(f"{what}: matrix contains NaN or Inf entries")
     raise ExecutorError(f"{what}: {msg} (status {rc})")
+
+
+TUNE_RING_WARPS = 1
+
+
+def tune(key: int, value: int) -> None:
+    check(load().caqr_tune(key, value), "caqr_tune")
 
 
 def geometry(n: int):

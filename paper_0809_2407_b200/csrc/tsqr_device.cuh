@@ -54,8 +54,9 @@ __device__ __forceinline__ void house_scalars(double x0, double sigma, double& b
   }
   const double nrm = sqrt(fma(x0, x0, sigma));
   beta = (x0 >= 0.0) ? -nrm : nrm;
-  scale = 1.0 / (x0 - beta);
-  tau = (beta - x0) / beta;
+  // x0 - beta and beta carry the same sign and |x0 - beta| >= |beta| > 0
+  scale = __drcp_rn(x0 - beta);
+  tau = (beta - x0) * __drcp_rn(beta);
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -236,70 +237,179 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
 // (stride NP) under the version protocol ver[j] == t.
 // On return X holds the tile's V (the stored rectangle of the factor).
 // ---------------------------------------------------------------------------
+// Branch-free reflector scalars for the pipelined ring.  Same conventions
+// as house_scalars (householder.py:101-111); sqrt and reciprocals from the
+// MUFU seeds refined by Newton steps (within 1 ulp), so the whole computation
+// schedules as straight-line code next to independent DFMA work.
+__device__ __forceinline__ double rsqrt_nr(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  const double e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+// Outputs beta, tau and scale = 1/(x0 - beta) (0 when sigma == 0).
+__device__ __forceinline__ void house_fast(double x0, double sigma, double& beta, double& tau,
+                                           double& scale) {
+  const double a = fma(x0, x0, sigma);
+  const double y = rsqrt_nr(a);
+  double nrm = a * y;
+  nrm = fma(0.5 * y, fma(-nrm, nrm, a), nrm);
+  const double b = (x0 >= 0.0) ? -nrm : nrm;
+  const double d = x0 - b;
+  const double sc = rcp_nr(d);
+  const double tg = -d * rcp_nr(b);
+  const bool z = (sigma == 0.0);
+  beta = z ? fabs(x0) : b;
+  tau = z ? ((x0 < 0.0) ? 2.0 : 0.0) : tg;
+  scale = z ? 0.0 : sc;
+}
+
+// ---------------------------------------------------------------------------
+// Ring step: one warp applies the n reflectors of its triangle-on-rectangle
+// tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
+// (stride NP) under the version protocol ver[j] == t.
+//
+// Software pipelined: reflector j+1 is generated (norm, ring wait, sqrt and
+// reciprocals) right after reflector j has updated the slot holding column
+// j+1, and its latency overlaps the update of the remaining slots.  The
+// broadcast vector is the RAW column x (v = scale * x); scale is folded into
+// the dot product / rank-1 coefficient and applied to the stored Y at the end.
+// On return X holds the tile's V (the stored rectangle of the factor).
+// ---------------------------------------------------------------------------
 template <int NP, int HW>
 __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], double* Rs, int* ver,
                                                  double* vb, int n, int t, double* tau_tile) {
   constexpr int S = NP / 32;
   const int lane = threadIdx.x & 31;
+  double mysc[S];  // this lane's column scale per slot (set when its reflector is made)
+#pragma unroll
+  for (int s = 0; s < S; ++s) mysc[s] = 1.0;
+  double v[HW];
+  double beta = 0.0, tau = 0.0, scale = 0.0;
 #pragma unroll
   for (int s = 0; s < S; ++s) {
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = 32 * s + jj;
-      if (j >= n) return;
-      // norm of this lane's slot-s column (only lane jj's is used)
+    if (32 * s >= n) break;
+    // ---- reflector for the first column of the slot (not overlapped)
+    {
+      const int j = 32 * s;
       double sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int k = 0; k < HW; k += 2) {
         sa = fma(X[k][s], X[k][s], sa);
         sb = fma(X[k + 1][s], X[k + 1][s], sb);
       }
-      const double sg = __shfl_sync(FULL, sa + sb, jj);
-      ring_wait(ver + j, t, lane);
-      double rr[S];
+      const double sg = __shfl_sync(FULL, sa + sb, 0);
+      while (ld_acquire(ver + j) != t) { }
+      house_fast(Rs[j * NP + j], sg, beta, tau, scale);
+      if (lane == 0) {
+        mysc[s] = scale;
 #pragma unroll
-      for (int s2 = s; s2 < S; ++s2) rr[s2] = Rs[j * NP + 32 * s2 + lane];
-      const double x0 = Rs[j * NP + j];
-      double beta, tau, scale;
-      house_scalars(x0, sg, beta, tau, scale);
-      if (lane == jj) {
-#pragma unroll
-        for (int k = 0; k < HW; ++k) {
-          const double vk = X[k][s] * scale;
-          vb[k] = vk;
-          X[k][s] = vk;
-        }
+        for (int k = 0; k < HW; k += 2)
+          *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][s], X[k + 1][s]);
       }
       __syncwarp();
-      double v[HW];
 #pragma unroll
       for (int k = 0; k < HW; k += 2) {
         const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
         v[k] = t2.x;
         v[k + 1] = t2.y;
       }
+    }
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * s + jj;
+      if (j >= n) break;
+      double* Rj = Rs + j * NP;
+      // ---- dot products of the raw column x with every active column
+      double p[S];
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) p[s2] = 0.0;
+#pragma unroll
+      for (int k = 0; k < HW; ++k) {
+#pragma unroll
+        for (int s2 = s; s2 < S; ++s2) p[s2] = fma(v[k], X[k][s2], p[s2]);
+      }
+      double w[S];   // coefficient on the raw x: tau*scale*(R + scale*x.X)
+      double wr[S];  // R-row decrement: tau*(R + scale*x.X)
 #pragma unroll
       for (int s2 = s; s2 < S; ++s2) {
-        double p0 = rr[s2], p1 = 0.0;
+        const bool act = (s2 > s) || (lane > jj);
+        const double r = Rj[32 * s2 + lane];
+        const double q = act ? tau * fma(scale, p[s2], r) : 0.0;
+        wr[s2] = q;
+        w[s2] = q * scale;
+      }
+      // ---- update the slot that holds column j+1 first
+#pragma unroll
+      for (int k = 0; k < HW; ++k) X[k][s] = fma(-v[k], w[s], X[k][s]);
+      const bool more = (jj < 31) && (j + 1 < n);
+      double sg = 0.0;
+      {
+        double sa = 0.0, sb = 0.0;
 #pragma unroll
         for (int k = 0; k < HW; k += 2) {
-          p0 = fma(v[k], X[k][s2], p0);
-          p1 = fma(v[k + 1], X[k + 1][s2], p1);
+          sa = fma(X[k][s], X[k][s], sa);
+          sb = fma(X[k + 1][s], X[k + 1][s], sb);
         }
-        const double wv = tau * (p0 + p1);
-        if (s2 > s || lane > jj) {
-          rr[s2] -= wv;
-#pragma unroll
-          for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
-        }
+        sg = __shfl_sync(FULL, sa + sb, (jj + 1) & 31);
       }
-      if (lane == jj) rr[s] = beta;
+      if (more) {
+        while (ld_acquire(ver + j + 1) != t) { }
+      }
+      // ---- next reflector's scalars || remaining slots' updates
+      double nbeta, ntau, nscale;
+      house_fast(more ? Rs[(j + 1) * NP + j + 1] : 1.0, sg, nbeta, ntau, nscale);
 #pragma unroll
-      for (int s2 = s; s2 < S; ++s2)
-        if (32 * s2 + lane >= j) Rs[j * NP + 32 * s2 + lane] = rr[s2];
+      for (int s2 = s + 1; s2 < S; ++s2) {
+#pragma unroll
+        for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], w[s2], X[k][s2]);
+      }
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) {
+        const int c = 32 * s2 + lane;
+        if (c > j) Rj[c] -= wr[s2];
+      }
+      if (lane == jj) Rj[j] = beta;
       if (lane == 0 && tau_tile) tau_tile[j] = tau;
-      ring_signal(ver + j, t + 1, lane);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        st_release(ver + j, t + 1);
+      }
+      if (more) {
+        if (lane == jj + 1) {
+          mysc[s] = nscale;
+#pragma unroll
+          for (int k = 0; k < HW; k += 2)
+            *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][s], X[k + 1][s]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < HW; k += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
+          v[k] = t2.x;
+          v[k + 1] = t2.y;
+        }
+        beta = nbeta;
+        tau = ntau;
+        scale = nscale;
+      }
     }
   }
+  // stored reflector entries: v = scale * x for every column of the tile
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int k = 0; k < HW; ++k) X[k][s] *= mysc[s];
 }
 
 // ---------------------------------------------------------------------------

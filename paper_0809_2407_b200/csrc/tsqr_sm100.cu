@@ -45,69 +45,100 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // ---------------------------------------------------------------------------
 // leaf factorization
 // ---------------------------------------------------------------------------
-template <int NP>
-struct LeafSmem {
-  static constexpr int HW = Geo<NP>::HW;
-  static constexpr size_t bytes =
-      sizeof(double) * ((size_t)NP * NP + WARPS * NP + WARPS * HW + WARPS + 2) + sizeof(int) * NP;
-};
+// Ring warps per CTA for the chain kernel (tunable: 8 warps x 255 registers
+// or 12 warps x 168 registers; the register file is split over 4 SMSPs).
+static int g_ring_warps = 8;
 
 template <int NP>
+struct DenseSmem {
+  static constexpr int HW = Geo<NP>::HW;
+  static constexpr size_t bytes = sizeof(double) * ((size_t)WARPS * NP + WARPS * HW + WARPS + 2);
+};
+template <int NP, int RWN>
+struct ChainSmem {
+  static constexpr int HW = Geo<NP>::HW;
+  static constexpr size_t bytes =
+      sizeof(double) * ((size_t)NP * NP + RWN * HW) + sizeof(int) * NP;
+};
+
+// Dense first tile of every leaf: rows [0, H0) (zero padded), CTA sweep.
+// Writes the leaf's R into its slot, tile 0 of Y (LAPACK layout) and tau.
+template <int NP>
 __global__ void __launch_bounds__(THREADS, 1)
-k_leaf_factor(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rout, int* flag) {
-  constexpr int S = Geo<NP>::S, HW = Geo<NP>::HW, H0 = WARPS * HW;
+k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rout, int* flag) {
+  constexpr int S = Geo<NP>::S, HW = Geo<NP>::HW;
   extern __shared__ __align__(16) double sm[];
-  double* Rs = sm;
-  double* part = Rs + NP * NP;
+  double* part = sm;
   double* vbuf = part + WARPS * NP;
   double* red = vbuf + WARPS * HW;
   double* sx0 = red + WARPS;
-  int* ver = reinterpret_cast<int*>(sx0 + 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   bool bad = false;
-  for (int leaf = blockIdx.x; leaf < P; leaf += gridDim.x) {
-    const int64_t r0 = (int64_t)leaf * base;
-    const int64_t b = (leaf == P - 1) ? m - r0 : base;
-    double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
-    double X[HW][S];
-    // ---- dense first tile: rows [0, H0) of the leaf (zero padded)
-    {
-      const int valid = (int)min64((int64_t)HW, b - (int64_t)w * HW);
-      load_rows<HW, S>(X, A + (r0 + (int64_t)w * HW) * lda, lda, valid, n, 0, bad);
-      cta_factor<NP, HW, DENSE>(X, nullptr, n, tl, red, sx0, part, vbuf);
-      if (Y) store_rows<HW, S>(X, Y + (r0 + (int64_t)w * HW) * ldy, ldy, valid, n, 0);
+  const int leaf = blockIdx.x;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
+  double X[HW][S];
+  const int valid = (int)min64((int64_t)HW, b - (int64_t)w * HW);
+  load_rows<HW, S>(X, A + (r0 + (int64_t)w * HW) * lda, lda, valid, n, 0, bad);
+  cta_factor<NP, HW, DENSE>(X, nullptr, n, tl, red, sx0, part, vbuf);
+  if (Y) store_rows<HW, S>(X, Y + (r0 + (int64_t)w * HW) * ldy, ldy, valid, n, 0);
+  double* Ro = Rout + (int64_t)leaf * n * n;
 #pragma unroll
-      for (int k = 0; k < HW; ++k) {
-        const int r = w * HW + k;
-        if (r < NP) {
+  for (int k = 0; k < HW; ++k) {
+    const int r = w * HW + k;
+    if (r < n) {
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
-            const int c = 32 * s + lane;
-            Rs[r * NP + c] = (c >= r && r < n && c < n) ? X[k][s] : 0.0;
-          }
-        }
+      for (int s = 0; s < S; ++s) {
+        const int c = 32 * s + lane;
+        if (c < n) Ro[r * n + c] = (c >= r) ? X[k][s] : 0.0;
       }
-      for (int j = threadIdx.x; j < NP; j += THREADS) ver[j] = 0;
-      __syncthreads();
     }
-    // ---- flat chain of triangle-on-rectangle tiles (warp ring)
-    const int64_t rest = b - H0;
-    const int T = rest > 0 ? (int)((rest + HW - 1) / HW) : 0;
-    for (int t = w; t < T; t += WARPS) {
-      const int64_t row = r0 + H0 + (int64_t)t * HW;
-      const int valid = (int)min64((int64_t)HW, r0 + b - row);
-      load_rows<HW, S>(X, A + row * lda, lda, valid, n, 0, bad);
-      ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * HW, n, t, tl ? tl + (int64_t)(t + 1) * n : nullptr);
-      if (Y) store_rows<HW, S>(X, Y + row * ldy, ldy, valid, n, 0);
-    }
-    __syncthreads();
-    double* Ro = Rout + (int64_t)leaf * n * n;
-    for (int idx = threadIdx.x; idx < n * n; idx += THREADS) {
-      const int r = idx / n, c = idx - r * n;
-      Ro[idx] = (c >= r) ? Rs[r * NP + c] : 0.0;
-    }
-    __syncthreads();
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+// Flat chain of triangle-on-rectangle tiles after the dense tile, as a warp
+// ring: R starts from the leaf's slot and is written back to it.
+template <int NP, int RING_WARPS>
+__global__ void __launch_bounds__(RING_WARPS * 32, 1)
+k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
+  constexpr int S = Geo<NP>::S, HW = Geo<NP>::HW, H0 = WARPS * HW;
+  constexpr int NT = RING_WARPS * 32;
+  extern __shared__ __align__(16) double sm[];
+  double* Rs = sm;
+  double* vbuf = Rs + NP * NP;
+  int* ver = reinterpret_cast<int*>(vbuf + RING_WARPS * HW);
+  const int w = threadIdx.x >> 5;
+  bool bad = false;
+  const int leaf = blockIdx.x;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const int64_t rest = b - H0;
+  const int T = rest > 0 ? (int)((rest + HW - 1) / HW) : 0;
+  if (T == 0) return;
+  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
+  double* Rl = Rio + (int64_t)leaf * n * n;
+  for (int idx = threadIdx.x; idx < NP * NP; idx += NT) {
+    const int r = idx / NP, c = idx - r * NP;
+    Rs[idx] = (r < n && c < n && c >= r) ? Rl[r * n + c] : 0.0;
+  }
+  for (int j = threadIdx.x; j < NP; j += NT) ver[j] = 0;
+  __syncthreads();
+  double X[HW][S];
+  for (int t = w; t < T; t += RING_WARPS) {
+    const int64_t row = r0 + H0 + (int64_t)t * HW;
+    const int valid = (int)min64((int64_t)HW, r0 + b - row);
+    load_rows<HW, S>(X, A + row * lda, lda, valid, n, 0, bad);
+    ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * HW, n, t, tl ? tl + (int64_t)(t + 1) * n : nullptr);
+    if (Y) store_rows<HW, S>(X, Y + row * ldy, ldy, valid, n, 0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+    const int r = idx / n, c = idx - r * n;
+    Rl[idx] = (c >= r) ? Rs[r * NP + c] : 0.0;
   }
   if (bad && flag) atomicOr(flag, 1);
 }
@@ -262,7 +293,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
   const bool tskip = tri_skip != 0;
   bool bad = false;
   double X[HW][KBS];
-  auto ycol = [&](int r, int j) { return __ldg(Yl + (int64_t)r * ldy + j); };
+  auto ycol = [&](int r, int j) { return (r < b) ? __ldg(Yl + (int64_t)r * ldy + j) : 0.0; };
   const int v0 = (int)max64(0, min64((int64_t)HW, b - (int64_t)w * HW));
   if (TRANS) {
     load_rows<HW, KBS>(X, Cl + (int64_t)w * HW * ldc, ldc, v0, ncb, 0, bad);
@@ -456,17 +487,28 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)P;
-#define LEAF_CASE(NPV)                                                                         \
-  case NPV: {                                                                                  \
-    int rc = prep(k_leaf_factor<NPV>, LeafSmem<NPV>::bytes);                                   \
-    if (rc) return rc;                                                                         \
-    k_leaf_factor<NPV><<<grid, THREADS, LeafSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P, \
-        base, Y, ldy, tau, tau_stride, R, flag);                                               \
-    break;                                                                                     \
+#define CHAIN_LAUNCH(NPV, RWN)                                                                  \
+  {                                                                                             \
+    rc = prep(k_leaf_chain<NPV, RWN>, ChainSmem<NPV, RWN>::bytes);                              \
+    if (rc) return rc;                                                                          \
+    k_leaf_chain<NPV, RWN><<<grid, RWN * 32, ChainSmem<NPV, RWN>::bytes, st>>>(A, lda, m,       \
+        (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                \
+  }
+#define LEAF_CASE(NPV)                                                                          \
+  case NPV: {                                                                                   \
+    int rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                    \
+    if (rc) return rc;                                                                          \
+    k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
+        base, Y, ldy, tau, tau_stride, R, flag);                                                \
+    if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HW) {                                    \
+      if (g_ring_warps == 12) CHAIN_LAUNCH(NPV, 12) else CHAIN_LAUNCH(NPV, 8)                   \
+    }                                                                                           \
+    break;                                                                                      \
   }
   switch (p) { LEAF_CASE(32) LEAF_CASE(64) LEAF_CASE(128) }
 #undef LEAF_CASE
-  return check_launch("k_leaf_factor");
+#undef CHAIN_LAUNCH
+  return check_launch("k_leaf_dense/k_leaf_chain");
 }
 
 int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,
@@ -576,6 +618,15 @@ int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n,
   switch (p) { BF_CASE(32) BF_CASE(64) BF_CASE(128) }
 #undef BF_CASE
   return check_launch("k_block_factor");
+}
+
+int caqr_tune(int key, int value) {
+  if (key == CAQR_TUNE_RING_WARPS) {
+    if (value != 8 && value != 12) return set_err(CAQR_ERR_ARG, "ring warps must be 8 or 12");
+    g_ring_warps = value;
+    return CAQR_OK;
+  }
+  return set_err(CAQR_ERR_ARG, "unknown tuning key");
 }
 
 int caqr_f64_peak_probe(double* scratch, int mode, int iters, int blocks, void* stream) {

@@ -104,6 +104,10 @@ def test_golden_composed_tsqr(golden):
         assert oracle.residual(A, Q, R) <= 10 * n * EPS, tag
         assert oracle.orthogonality(Q) <= 10 * n * EPS, tag
         # Q matches the reference Q column-by-column up to the R sign flips
+        # (well-conditioned cases only: for kappa = 1e12 the trailing columns of
+        # two backward-stable Q factors legitimately differ by O(eps kappa_j))
+        if "1024x64" in tag:
+            continue
         d = np.sign(np.diag(R)) * np.sign(np.diag(g[f"{tag}_R"]))
         assert np.max(np.abs(Q * d - g[f"{tag}_Q"])) <= 1e-6, tag
 
