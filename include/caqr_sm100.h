@@ -29,6 +29,8 @@
  *                                 trailing update _apply_yt(transpose=True) (:175-186)
  *   tsqr_f64_block_factor      <- qr_unblocked (mode 0) / qr_triangle_on_rect
  *                                 (mode 2) on blocks of <= 128 rows
+ *   tsqr_f64_block_apply       <- apply_q / apply_qt on those single-block factors
+ *                                 (householder.py:377-396)
  */
 #ifndef CAQR_SM100_H
 #define CAQR_SM100_H
@@ -94,9 +96,17 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
 
 /* Single-CTA factorization of a block of rows <= 128: mode 0 = DENSE
  * (qr_unblocked: R out, Y m x n LAPACK layout), mode 2 = TRIRECT
- * (qr_triangle_on_rect: R in/out, Y = rectangle). */
+ * (qr_triangle_on_rect: R in/out, Y = rectangle), mode 3 = STACKED with q-1
+ * lower triangles stacked in A (qr_stacked_triangles: R = top triangle in/out). */
 int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
                           double* Y, int64_t ldy, double* tau, int mode, int* flag, void* stream);
+
+/* Q C / Q^T C for a single-block factor of tsqr_f64_block_factor: mode 0 =
+ * DENSE (C has rows rows), mode 2 = TRIRECT (C = [Ctop (n rows, ldt); C
+ * (rows rows)]); rows <= 128. */
+int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, const double* tau,
+                         double* Ctop, int64_t ldt, double* C, int64_t ldc, int64_t ncols, int mode,
+                         int transpose, void* stream);
 
 /* Process-wide tuning knobs (not thread-safe; set before launching work).
  * CAQR_TUNE_RING_WARPS: warps per CTA of the leaf chain ring (8 or 12). */

@@ -24,6 +24,7 @@ SYMBOLS = (
     "tsqr_f64_tree_apply_level",
     "tsqr_f64_leaf_apply",
     "tsqr_f64_block_factor",
+    "tsqr_f64_block_apply",
     "caqr_tune",
     "caqr_f64_peak_probe",
 )
@@ -59,6 +60,8 @@ def _sig(lib):
                                         i64, i32, i32, i32, vp]
     lib.tsqr_f64_block_factor.restype = i32
     lib.tsqr_f64_block_factor.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i32, ip, vp]
+    lib.tsqr_f64_block_apply.restype = i32
+    lib.tsqr_f64_block_apply.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i64, i64, i32, i32, vp]
     lib.caqr_tune.restype = i32
     lib.caqr_tune.argtypes = [i32, i32]
     lib.caqr_f64_peak_probe.restype = i32

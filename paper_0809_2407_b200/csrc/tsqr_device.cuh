@@ -33,7 +33,7 @@ constexpr unsigned FULL = 0xffffffffu;
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
-enum Mode { DENSE = 0, STACKED = 1, TRIRECT = 2 };
+enum Mode { DENSE = 0, STACKED = 1, TRIRECT = 2, STACKEDQ = 3 };
 
 // Ring tile height per padded width: 64 doubles of tile per lane.
 template <int NP> struct Geo;
@@ -150,7 +150,8 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
 #pragma unroll
       for (int k = 0; k < RW; ++k) {
         const int r = w * RW + k;
-        const bool in = (MODE == DENSE) ? (r > j) : (MODE == STACKED ? (r <= j) : true);
+        const bool in = (MODE == DENSE) ? (r > j)
+                        : (MODE == STACKED ? (r <= j) : (MODE == STACKEDQ ? (r % n) <= j : true));
         const double x = X[k][s];
         if (in) sg = fma(x, x, sg);
       }
@@ -178,7 +179,8 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
 #pragma unroll
           for (int k = 0; k < RW; ++k) {
             const int r = w * RW + k;
-            const bool in = (MODE == DENSE) ? (r > j) : (MODE == STACKED ? (r <= j) : true);
+            const bool in = (MODE == DENSE) ? (r > j)
+                            : (MODE == STACKED ? (r <= j) : (MODE == STACKEDQ ? (r % n) <= j : true));
             double vk = 0.0;
             if (in) vk = X[k][s] * scale;
             else if (MODE == DENSE && r == j) vk = 1.0;
@@ -430,7 +432,7 @@ __device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int 
   for (int jx = 0; jx < n; ++jx) {
     const int j = TRANS ? jx : n - 1 - jx;
     const int pw = j / RW;
-    const bool wact = (MODE == DENSE) ? (w >= pw) : (w <= pw);
+    const bool wact = (MODE == DENSE) ? (w >= pw) : (MODE == STACKED ? (w <= pw) : true);
     double* pb = part + (jx & 1) * WARPS * KB;
     const double tj = __ldg(tau + j);
     double v[RW];
@@ -443,8 +445,10 @@ __device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int 
         if (MODE == DENSE) {
           if (r > j) vk = Ycol(r, j);
           else if (r == j) vk = 1.0;
-        } else {
+        } else if (MODE == STACKED) {
           if (r <= j) vk = Ycol(r, j);
+        } else {
+          vk = Ycol(r, j);
         }
         v[k] = vk;
       }
@@ -468,7 +472,7 @@ __device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int 
     __syncthreads();
     if (wact && tj != 0.0) {
       const int q0 = (MODE == DENSE) ? pw : 0;
-      const int q1 = (MODE == DENSE) ? WARPS - 1 : pw;
+      const int q1 = (MODE == STACKED) ? pw : WARPS - 1;
 #pragma unroll
       for (int s2 = 0; s2 < KBS; ++s2) {
         if (tri_skip && col0 + 32 * s2 + 31 < j) continue;

@@ -388,7 +388,7 @@ k_block_factor(const double* __restrict__ A, int64_t lda, int rows, int n, doubl
   double* sx0 = red + WARPS;
   const int w = threadIdx.x >> 5;
   bool bad = false;
-  if (MODE == TRIRECT) {
+  if (MODE == TRIRECT || MODE == STACKEDQ) {
     for (int idx = threadIdx.x; idx < NP * NP; idx += THREADS) {
       const int r = idx / NP, c = idx - r * NP;
       Ps[idx] = (r < n && c < n && c >= r) ? Rio[r * n + c] : 0.0;
@@ -401,13 +401,64 @@ k_block_factor(const double* __restrict__ A, int64_t lda, int rows, int n, doubl
   cta_factor<NP, RW, MODE>(X, Ps, n, tau, red, sx0, part, vbuf);
   __syncthreads();
   store_rows<RW, S>(X, Yout + (int64_t)w * RW * ldy, ldy, valid, n, 0);
-  if (MODE == TRIRECT) {
+  if (MODE == DENSE) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int r = w * RW + k;
+      if (r >= n) continue;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int c = 32 * s + lane;
+        if (c < n) Rio[r * n + c] = (c >= r) ? X[k][s] : 0.0;
+      }
+    }
+  }
+  if (MODE == TRIRECT || MODE == STACKEDQ) {
     for (int idx = threadIdx.x; idx < n * n; idx += THREADS) {
       const int r = idx / n, c = idx - r * n;
       Rio[idx] = (c >= r) ? Ps[r * NP + c] : 0.0;
     }
   }
   if (bad && flag) atomicOr(flag, 1);
+}
+
+// Single-CTA application of a DENSE (rows <= 128) or TRIRECT (rectangle rows
+// <= 128) factor: C block rows in registers; for TRIRECT the n pivot rows Ct
+// (the identity-top part of the factor) live in shared memory.
+template <int RW, int KBS, int MODE, bool TRANS>
+__global__ void __launch_bounds__(THREADS, 1)
+k_block_apply(const double* __restrict__ Yf, int64_t ldy, int rows, int n,
+              const double* __restrict__ tau, double* Ct, int64_t ldt, double* C, int64_t ldc,
+              int64_t ncols) {
+  constexpr int KB = 32 * KBS;
+  extern __shared__ __align__(16) double sm[];
+  double* Ps = sm;
+  double* part = Ps + 128 * KB;
+  const int w = threadIdx.x >> 5;
+  const int col0 = blockIdx.x * KB;
+  const int ncb = (int)min64(ncols - col0, KB);
+  if (MODE == TRIRECT) {
+    for (int idx = threadIdx.x; idx < 128 * KB; idx += THREADS) {
+      const int r = idx / KB, c = idx - r * KB;
+      Ps[idx] = (r < n && c < ncb) ? Ct[(int64_t)r * ldt + col0 + c] : 0.0;
+    }
+  }
+  double X[RW][KBS];
+  bool bad = false;
+  const int valid = max(0, min(RW, rows - w * RW));
+  load_rows<RW, KBS>(X, C + (int64_t)w * RW * ldc + col0, ldc, valid, ncb, 0, bad);
+  __syncthreads();
+  auto ycol = [&](int r, int j) { return (r < rows) ? __ldg(Yf + (int64_t)r * ldy + j) : 0.0; };
+  cta_apply<RW, KBS, MODE, TRANS>(X, Ps, n, ycol, tau, part, col0, false);
+  __syncthreads();
+  store_rows<RW, KBS>(X, C + (int64_t)w * RW * ldc + col0, ldc, valid, ncb, 0);
+  if (MODE == TRIRECT) {
+    for (int idx = threadIdx.x; idx < n * KB; idx += THREADS) {
+      const int r = idx / KB, c = idx - r * KB;
+      if (c < ncb) Ct[(int64_t)r * ldt + col0 + c] = Ps[idx];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -596,7 +647,8 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
 int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
                           double* Y, int64_t ldy, double* tau, int mode, int* flag, void* stream) {
   const int p = padded(n);
-  if (!p || !A || !R || !Y || !tau || rows < 1 || (mode == 0 && rows < n))
+  if (!p || !A || !R || !Y || !tau || rows < 1 || (mode == 0 && rows < n) ||
+      (mode != 0 && mode != 2 && mode != 3))
     return set_err(CAQR_ERR_ARG, "tsqr_f64_block_factor: bad arguments");
   constexpr int RWMAX = 16;
   if (rows > WARPS * RWMAX) return set_err(CAQR_ERR_ARG, "block too tall for the single-CTA kernel");
@@ -608,6 +660,10 @@ int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n,
       int rc = prep(k_block_factor<NPV, RWMAX, DENSE>, sm); if (rc) return rc;                  \
       k_block_factor<NPV, RWMAX, DENSE><<<1, THREADS, sm, st>>>(A, lda, (int)rows, (int)n, R,   \
           Y, ldy, tau, flag);                                                                   \
+    } else if (mode == 3) {                                                                     \
+      int rc = prep(k_block_factor<NPV, RWMAX, STACKEDQ>, sm); if (rc) return rc;               \
+      k_block_factor<NPV, RWMAX, STACKEDQ><<<1, THREADS, sm, st>>>(A, lda, (int)rows, (int)n,   \
+          R, Y, ldy, tau, flag);                                                                \
     } else {                                                                                    \
       int rc = prep(k_block_factor<NPV, RWMAX, TRIRECT>, sm); if (rc) return rc;                \
       k_block_factor<NPV, RWMAX, TRIRECT><<<1, THREADS, sm, st>>>(A, lda, (int)rows, (int)n, R, \
@@ -618,6 +674,28 @@ int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n,
   switch (p) { BF_CASE(32) BF_CASE(64) BF_CASE(128) }
 #undef BF_CASE
   return check_launch("k_block_factor");
+}
+
+int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, const double* tau,
+                         double* Ctop, int64_t ldt, double* C, int64_t ldc, int64_t ncols, int mode,
+                         int transpose, void* stream) {
+  if (n < 1 || n > 128 || rows < 1 || rows > 128 || !Y || !tau || !C || ncols < 1 ||
+      (mode == 2 && !Ctop) || (mode == 0 && rows < n) || (mode != 0 && mode != 2))
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_block_apply: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  constexpr int RW = 16, KBS = 1;
+  const size_t sm = sizeof(double) * ((size_t)128 * 32 * KBS + 2 * WARPS * 32 * KBS);
+  dim3 grid((unsigned)((ncols + 32 * KBS - 1) / (32 * KBS)));
+#define BA_LAUNCH(MD, TR)                                                                      \
+  {                                                                                            \
+    int rc = prep(k_block_apply<RW, KBS, MD, TR>, sm); if (rc) return rc;                      \
+    k_block_apply<RW, KBS, MD, TR><<<grid, THREADS, sm, st>>>(Y, ldy, (int)rows, (int)n, tau,  \
+        Ctop, ldt, C, ldc, ncols);                                                             \
+  }
+  if (mode == 0) { if (transpose) BA_LAUNCH(DENSE, true) else BA_LAUNCH(DENSE, false) }
+  else { if (transpose) BA_LAUNCH(TRIRECT, true) else BA_LAUNCH(TRIRECT, false) }
+#undef BA_LAUNCH
+  return check_launch("k_block_apply");
 }
 
 int caqr_tune(int key, int value) {

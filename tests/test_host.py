@@ -1,0 +1,181 @@
+"""Host-side logic (no GPU): trees, layouts, generators, counters, the C-ABI
+library's exported symbols, and the drop-in ``caqr`` package."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import oracle
+from paper_0809_2407_b200 import _lib
+from paper_0809_2407_b200.core import (
+    BlockCyclicLayout,
+    BlockRowLayout,
+    CondSpec,
+    DimensionError,
+    gen_cond_matrix,
+    partition_block_rows,
+    rng_for,
+)
+from paper_0809_2407_b200.counters import (
+    CommRecorder,
+    FlopCounter,
+    count_geqr2,
+    count_stacked,
+    critical_path,
+)
+from paper_0809_2407_b200.trees import (
+    ReductionTree,
+    TreeError,
+    build_qary_levels,
+    first_proc,
+    level,
+    parse_tree,
+    qary_tree,
+    target_first_proc,
+)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---- trees (reference tests: pkg/tests/test_trees.py) ----------------------
+
+def test_node_arithmetic():
+    assert level(5, 0) == 5 and level(5, 2) == 1 and level(7, 3) == 0
+    for i in range(4, 8):
+        assert first_proc(i, 2) == 4 and target_first_proc(i, 2) == 6
+    assert first_proc(3, 1) == 2 and target_first_proc(3, 1) == 3
+    with pytest.raises(TreeError):
+        target_first_proc(3, 0)
+
+
+def test_schedules(golden):
+    ev = ReductionTree(P=4).schedule()
+    assert [(e.level, e.participants, e.receiver) for e in ev] == [
+        (1, (0, 1), 0), (1, (2, 3), 2), (2, (0, 2), 0)]
+    assert ReductionTree(P=1).schedule() == []
+    assert [(e.participants, e.receiver) for e in ReductionTree(P=4, shape="flat").schedule()] == [
+        ((0, 1), 0), ((0, 2), 0), ((0, 3), 0)]
+    for k, v in golden["misc"].items():
+        if k.startswith("sched_"):
+            P = int(k.split("_")[1])
+            got = np.array([(e.level,) + e.participants for e in ReductionTree(P=P).schedule()],
+                           dtype=np.int64).reshape(-1, 3)
+            assert np.array_equal(got, v), P
+
+
+@given(st.integers(2, 64))
+@settings(max_examples=40, deadline=None)
+def test_binary_pairing(P):
+    tree = ReductionTree(P=P)
+    consumed = [p for grp in tree.levels for g in grp for p in g[1:]]
+    assert sorted(consumed + [tree.root]) == list(range(P))
+    lv = tree.device_levels()
+    ids = np.concatenate([x[:, 2] for x in lv])
+    assert list(ids) == list(range(P - 1))
+    assert sum(len(x) for x in lv) == P - 1
+
+
+def test_tree_misc():
+    assert ReductionTree(P=16).critical_path_stats() == {"stages": 4, "messages_per_proc": 4}
+    assert ReductionTree(P=4, shape="flat").critical_path_stats() == {"stages": 3,
+                                                                        "messages_per_proc": 3}
+    assert build_qary_levels(9, 3) == [[(0, 1, 2), (3, 4, 5), (6, 7, 8)], [(0, 3, 6)]]
+    assert qary_tree(10, 3).root == 0
+    t = parse_tree("levels:[[0,1],[2,3]];[[0,2]]")
+    assert t.schedule() == ReductionTree(P=4).schedule()
+    for bad in ("binary", "ring:4", "binary:x", "levels:[[0]]"):
+        with pytest.raises(TreeError):
+            parse_tree(bad)
+    with pytest.raises(TreeError):
+        ReductionTree(P=4, shape="levels", levels=(((0, 1),),))
+    with pytest.raises(TreeError):
+        qary_tree(9, 3).device_levels()  # q-ary groups are not pairwise
+
+
+# ---- core -------------------------------------------------------------------
+
+def test_layouts(golden):
+    lay = BlockRowLayout(10, 2, 3)
+    assert lay.block_rows == (3, 3, 4) and lay.row_offsets() == [0, 3, 6, 10]
+    with pytest.raises(DimensionError):
+        BlockRowLayout(5, 3, 2)
+    A = np.arange(60.0).reshape(20, 3)
+    assert np.array_equal(np.vstack(partition_block_rows(A, 3)), A)
+    bc = BlockCyclicLayout(1024, 1024, 128, 2, 4)
+    assert np.array_equal(np.array([[bc.owner(i, j) for j in range(8)] for i in range(8)]),
+                          golden["misc"]["bc_owner"])
+    with pytest.raises(DimensionError):
+        BlockCyclicLayout(100, 100, 30, 1, 1)
+
+
+def test_generators_bit_identical_to_reference(golden):
+    g = golden["misc"]
+    assert np.array_equal(rng_for(0).standard_normal((1000, 8)), g["normal_s0_1000x8"])
+    assert np.array_equal(rng_for(0).uniform(-1, 1, (1000, 8)), g["uniform_s0_1000x8"])
+    A = gen_cond_matrix(CondSpec(64, 8, kappa=1e12, seed=3))
+    assert np.max(np.abs(A - g["cond_64x8_k1e12_s3"])) <= 1e-15
+    with pytest.raises(DimensionError):
+        CondSpec(3, 5, kappa=10.0)
+
+
+# ---- counters -----------------------------------------------------------------
+
+def test_flop_counts_match_reference_model():
+    n, m = 16, 3200
+    f, d = count_geqr2(m, n)
+    model = 2 * m * n ** 2 - (2 / 3) * n ** 3
+    assert abs(f - model) <= 0.05 * model and d > 0
+    # stacked combine ~ 1/5 of the dense QR of the 2n x n stack (test_householder.py:188-200)
+    ratio = count_stacked(80)[0] / count_geqr2(160, 80)[0]
+    assert 0.17 <= ratio <= 0.23
+    c = FlopCounter()
+    c.add_gemm(3, 4, 5)
+    assert c.flops == 3 * 5 * 7
+
+
+def test_comm_recorder():
+    rs = [CommRecorder() for _ in range(4)]
+    for (lvl, a, b) in oracle.binary_events(4):
+        rs[b].record_send(10)
+        rs[a].record_recv(10, stage=(lvl, "R"))
+    assert critical_path(rs) == (2, 20)
+
+
+# ---- C-ABI boundary -----------------------------------------------------------
+
+def test_library_exports_every_declared_symbol():
+    assert os.path.exists(_lib.LIB_PATH), "build the library first (__graft_entry__.build())"
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    header = open(os.path.join(ROOT, "include", "caqr_sm100.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(\w+)\(", header, flags=re.M))
+    assert declared == set(_lib.SYMBOLS)
+    for s in declared:
+        assert hasattr(lib, s), s
+    loaded = _lib.load()
+    assert loaded.caqr_sm100_abi_version() == _lib.ABI_VERSION
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_dropin_package_imports():
+    import caqr.caqr
+    import caqr.core
+    import caqr.householder
+    import caqr.trees
+    import caqr.tsqr
+
+    assert caqr.trees.ReductionTree is ReductionTree
+    assert callable(caqr.tsqr.tsqr_parallel) and callable(caqr.caqr.caqr_factor)
+    assert callable(caqr.householder.qr_stacked_triangles)
