@@ -109,8 +109,14 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
                          int transpose, void* stream);
 
 /* Process-wide tuning knobs (not thread-safe; set before launching work).
- * CAQR_TUNE_RING_WARPS: warps per CTA of the leaf chain ring (8 or 12). */
-#define CAQR_TUNE_RING_WARPS 1
+ * CAQR_TUNE_CHAIN_HT_{32,64,128}: chain tile height for padded width 32/64
+ * (16 or 32) and 128 (8 or 16).  It fixes the implicit-Q format: factor and
+ * apply calls on the same factor must see the same value. */
+#define CAQR_TUNE_CHAIN_HT_32 1
+#define CAQR_TUNE_CHAIN_HT_64 2
+#define CAQR_TUNE_CHAIN_HT_128 3
+/* CAQR_TUNE_NARROW: 1 (default) = lane-private chains for n <= 8 when no Q is stored. */
+#define CAQR_TUNE_NARROW 4
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

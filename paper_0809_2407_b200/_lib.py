@@ -106,7 +106,8 @@ def check(rc: int, what: str) -> None:
     raise ExecutorError(f"{what}: {msg} (status {rc})")
 
 
-TUNE_RING_WARPS = 1
+TUNE_CHAIN_HT = {32: 1, 64: 2, 128: 3}
+TUNE_NARROW = 4
 
 
 def tune(key: int, value: int) -> None:

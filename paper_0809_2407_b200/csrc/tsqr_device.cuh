@@ -35,11 +35,18 @@ __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return
 
 enum Mode { DENSE = 0, STACKED = 1, TRIRECT = 2, STACKEDQ = 3 };
 
-// Ring tile height per padded width: 64 doubles of tile per lane.
+// Per padded width: S column slots per lane, HD rows per warp in the dense
+// first tile (H0 = 8*HD >= NP rows).  The chain tile height HT is a separate,
+// tunable template parameter of the chain / apply kernels.
 template <int NP> struct Geo;
-template <> struct Geo<32>  { static constexpr int S = 1, HW = 32; };
-template <> struct Geo<64>  { static constexpr int S = 2, HW = 32; };
-template <> struct Geo<128> { static constexpr int S = 4, HW = 16; };
+template <> struct Geo<32>  { static constexpr int S = 1, HD = 32; };
+template <> struct Geo<64>  { static constexpr int S = 2, HD = 32; };
+template <> struct Geo<128> { static constexpr int S = 4, HD = 16; };
+// Warps of the factorization ring for a chain tile height (register budget:
+// 16 warps -> 128 regs, 8 warps -> 255 regs per thread).
+template <int NP, int HT> struct RingCfg {
+  static constexpr int WARPS_R = (HT * (NP / 32) <= 32 && HT <= 16) ? 16 : 8;
+};
 
 // house_gen scalars (householder.py:97-113): given x0 and sigma = ||x[1:]||^2
 // return beta, tau and the scale 1/(x0 - beta) applied to x[1:].
@@ -288,10 +295,25 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
 // the dot product / rank-1 coefficient and applied to the stored Y at the end.
 // On return X holds the tile's V (the stored rectangle of the factor).
 // ---------------------------------------------------------------------------
+#ifdef TSQR_SPIN_PROBE
+__device__ unsigned long long g_spin_cycles[2];
+#define SPIN_WAIT(ptr, target)                                  \
+  {                                                             \
+    long long t0_ = clock64();                                  \
+    while (ld_acquire(ptr) != (target)) { }                     \
+    if (lane == 0) atomicAdd(&g_spin_cycles[0], clock64() - t0_); \
+  }
+#else
+#define SPIN_WAIT(ptr, target) { while (ld_acquire(ptr) != (target)) { } }
+#endif
+
 template <int NP, int HW>
 __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], double* Rs, int* ver,
                                                  double* vb, int n, int t, double* tau_tile) {
   constexpr int S = NP / 32;
+#ifdef TSQR_SPIN_PROBE
+  const long long tstart = clock64();
+#endif
   const int lane = threadIdx.x & 31;
   double mysc[S];  // this lane's column scale per slot (set when its reflector is made)
 #pragma unroll
@@ -311,7 +333,7 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
         sb = fma(X[k + 1][s], X[k + 1][s], sb);
       }
       const double sg = __shfl_sync(FULL, sa + sb, 0);
-      while (ld_acquire(ver + j) != t) { }
+      SPIN_WAIT(ver + j, t)
       house_fast(Rs[j * NP + j], sg, beta, tau, scale);
       if (lane == 0) {
         mysc[s] = scale;
@@ -332,14 +354,19 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
       if (j >= n) break;
       double* Rj = Rs + j * NP;
       // ---- dot products of the raw column x with every active column
-      double p[S];
+      double p[S], pq[S];
 #pragma unroll
-      for (int s2 = s; s2 < S; ++s2) p[s2] = 0.0;
+      for (int s2 = s; s2 < S; ++s2) { p[s2] = 0.0; pq[s2] = 0.0; }
 #pragma unroll
-      for (int k = 0; k < HW; ++k) {
+      for (int k = 0; k < HW; k += 2) {
 #pragma unroll
-        for (int s2 = s; s2 < S; ++s2) p[s2] = fma(v[k], X[k][s2], p[s2]);
+        for (int s2 = s; s2 < S; ++s2) {
+          p[s2] = fma(v[k], X[k][s2], p[s2]);
+          pq[s2] = fma(v[k + 1], X[k + 1][s2], pq[s2]);
+        }
       }
+#pragma unroll
+      for (int s2 = s; s2 < S; ++s2) p[s2] += pq[s2];
       double w[S];   // coefficient on the raw x: tau*scale*(R + scale*x.X)
       double wr[S];  // R-row decrement: tau*(R + scale*x.X)
 #pragma unroll
@@ -364,9 +391,7 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
         }
         sg = __shfl_sync(FULL, sa + sb, (jj + 1) & 31);
       }
-      if (more) {
-        while (ld_acquire(ver + j + 1) != t) { }
-      }
+      if (more) SPIN_WAIT(ver + j + 1, t)
       // ---- next reflector's scalars || remaining slots' updates
       double nbeta, ntau, nscale;
       house_fast(more ? Rs[(j + 1) * NP + j + 1] : 1.0, sg, nbeta, ntau, nscale);
@@ -412,6 +437,9 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
   for (int s = 0; s < S; ++s)
 #pragma unroll
     for (int k = 0; k < HW; ++k) X[k][s] *= mysc[s];
+#ifdef TSQR_SPIN_PROBE
+  if (lane == 0) atomicAdd(&g_spin_cycles[1], clock64() - tstart);
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -45,20 +45,22 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // ---------------------------------------------------------------------------
 // leaf factorization
 // ---------------------------------------------------------------------------
-// Ring warps per CTA for the chain kernel (tunable: 8 warps x 255 registers
-// or 12 warps x 168 registers; the register file is split over 4 SMSPs).
-static int g_ring_warps = 8;
+// Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
+// the implicit-Q storage format, so factor and apply calls must agree.
+static int g_ht[3] = {16, 16, 8};  // NP = 32, 64, 128
+static int g_narrow = 1;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
+static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
 struct DenseSmem {
-  static constexpr int HW = Geo<NP>::HW;
-  static constexpr size_t bytes = sizeof(double) * ((size_t)WARPS * NP + WARPS * HW + WARPS + 2);
+  static constexpr int HD = Geo<NP>::HD;
+  static constexpr size_t bytes = sizeof(double) * ((size_t)WARPS * NP + WARPS * HD + WARPS + 2);
 };
-template <int NP, int RWN>
+template <int NP, int HT>
 struct ChainSmem {
-  static constexpr int HW = Geo<NP>::HW;
+  static constexpr int RWN = RingCfg<NP, HT>::WARPS_R;
   static constexpr size_t bytes =
-      sizeof(double) * ((size_t)NP * NP + RWN * HW) + sizeof(int) * NP;
+      sizeof(double) * ((size_t)NP * NP + RWN * HT) + sizeof(int) * NP;
 };
 
 // Dense first tile of every leaf: rows [0, H0) (zero padded), CTA sweep.
@@ -67,11 +69,11 @@ template <int NP>
 __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rout, int* flag) {
-  constexpr int S = Geo<NP>::S, HW = Geo<NP>::HW;
+  constexpr int S = Geo<NP>::S, HD = Geo<NP>::HD;
   extern __shared__ __align__(16) double sm[];
   double* part = sm;
   double* vbuf = part + WARPS * NP;
-  double* red = vbuf + WARPS * HW;
+  double* red = vbuf + WARPS * HD;
   double* sx0 = red + WARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   bool bad = false;
@@ -79,15 +81,15 @@ k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   const int64_t r0 = (int64_t)leaf * base;
   const int64_t b = (leaf == P - 1) ? m - r0 : base;
   double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
-  double X[HW][S];
-  const int valid = (int)min64((int64_t)HW, b - (int64_t)w * HW);
-  load_rows<HW, S>(X, A + (r0 + (int64_t)w * HW) * lda, lda, valid, n, 0, bad);
-  cta_factor<NP, HW, DENSE>(X, nullptr, n, tl, red, sx0, part, vbuf);
-  if (Y) store_rows<HW, S>(X, Y + (r0 + (int64_t)w * HW) * ldy, ldy, valid, n, 0);
+  double X[HD][S];
+  const int valid = (int)min64((int64_t)HD, b - (int64_t)w * HD);
+  load_rows<HD, S>(X, A + (r0 + (int64_t)w * HD) * lda, lda, valid, n, 0, bad);
+  cta_factor<NP, HD, DENSE>(X, nullptr, n, tl, red, sx0, part, vbuf);
+  if (Y) store_rows<HD, S>(X, Y + (r0 + (int64_t)w * HD) * ldy, ldy, valid, n, 0);
   double* Ro = Rout + (int64_t)leaf * n * n;
 #pragma unroll
-  for (int k = 0; k < HW; ++k) {
-    const int r = w * HW + k;
+  for (int k = 0; k < HD; ++k) {
+    const int r = w * HD + k;
     if (r < n) {
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -101,11 +103,12 @@ k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
 
 // Flat chain of triangle-on-rectangle tiles after the dense tile, as a warp
 // ring: R starts from the leaf's slot and is written back to it.
-template <int NP, int RING_WARPS>
-__global__ void __launch_bounds__(RING_WARPS * 32, 1)
+template <int NP, int HT>
+__global__ void __launch_bounds__(RingCfg<NP, HT>::WARPS_R * 32, 1)
 k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
-  constexpr int S = Geo<NP>::S, HW = Geo<NP>::HW, H0 = WARPS * HW;
+  constexpr int S = Geo<NP>::S, H0 = WARPS * Geo<NP>::HD, HW = HT;
+  constexpr int RING_WARPS = RingCfg<NP, HT>::WARPS_R;
   constexpr int NT = RING_WARPS * 32;
   extern __shared__ __align__(16) double sm[];
   double* Rs = sm;
@@ -141,6 +144,119 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
     Rl[idx] = (c >= r) ? Rs[r * NP + c] : 0.0;
   }
   if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
+// Lane l owns an 8x8 upper-triangular R in registers and runs the flat chain
+// of triangle-on-rectangle steps (Alg. 2) over its own rows: K rows per step,
+// rows [q*32K + l*K, +K) of round q (256 contiguous bytes per lane per round,
+// the next round prefetched into registers).  The 32 lane R factors are then
+// combined in-warp by the same step applied to the partner lane's R (shuffled
+// in two 4-row halves), a binary tree over lanes.  R-only: the chains start
+// from R = 0, which gives the QR of [0; A] -- the same R, no stored Q.
+// ---------------------------------------------------------------------------
+constexpr int NARROW_K = 4;
+constexpr int NARROW_WARPS = 8;
+
+template <int K>
+__device__ __forceinline__ void narrow_step(double (&R)[8][8], double (&B)[K][8], int n) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= n) break;
+    double sg = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) sg = fma(B[k][j], B[k][j], sg);
+    double beta, tau, scale;
+    house_fast(R[j][j], sg, beta, tau, scale);
+#pragma unroll
+    for (int c = j + 1; c < 8; ++c) {
+      double d = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) d = fma(B[k][j], B[k][c], d);
+      const double q = tau * fma(scale, d, R[j][c]);
+      R[j][c] -= q;
+      const double qs = q * scale;
+#pragma unroll
+      for (int k = 0; k < K; ++k) B[k][c] = fma(-B[k][j], qs, B[k][c]);
+    }
+    R[j][j] = beta;
+  }
+}
+
+__global__ void __launch_bounds__(NARROW_WARPS * 32, 1)
+k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+              double* Rout, int* flag) {
+  constexpr int K = NARROW_K;
+  const int lane = threadIdx.x & 31;
+  const int leaf = blockIdx.x * NARROW_WARPS + (threadIdx.x >> 5);
+  if (leaf >= P) return;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  bool bad = false;
+  double R[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) R[i][c] = 0.0;
+  const int64_t rounds = (b + 32 * K - 1) / (32 * K);
+  double Bn[K][8];
+  auto load = [&](double (&Bt)[K][8], int64_t q) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t row = q * 32 * K + (int64_t)lane * K + k;
+      const bool ok = row < b;
+      const double* src = A + (r0 + row) * lda;
+      if (ok && n == 8 && lda == 8) {
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 t = __ldg(s2 + c);
+          Bt[k][2 * c] = t.x;
+          Bt[k][2 * c + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Bt[k][c] = (ok && c < n) ? __ldg(src + c) : 0.0;
+      }
+    }
+  };
+  if (rounds > 0) load(Bn, 0);
+  for (int64_t q = 0; q < rounds; ++q) {
+    double B[K][8];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        B[k][c] = Bn[k][c];
+        bad |= !isfinite(B[k][c]);
+      }
+    if (q + 1 < rounds) load(Bn, q + 1);
+    narrow_step<K>(R, B, n);
+  }
+  // in-warp binary tree over the lane R factors
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double B[4][8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) B[k][c] = __shfl_down_sync(FULL, R[4 * half + k][c], off);
+      if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, B, n);
+    }
+  }
+  if (lane == 0) {
+    double* Ro = Rout + (int64_t)leaf * n * n;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[i][c] : 0.0;
+  }
+  bad = __any_sync(FULL, bad);
+  if (bad && lane == 0 && flag) atomicOr(flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -268,13 +384,13 @@ struct LeafApplySmem {
       sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS) + sizeof(int) * NP;
 };
 
-template <int NP, int KBS, bool TRANS>
+template <int NP, int KBS, bool TRANS, int HT>
 __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
              int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
              int64_t ncols, const double* __restrict__ S, int64_t lds, int64_t s_slot_rows,
              int zero_init, int tri_skip) {
-  constexpr int HW = Geo<NP>::HW, H0 = WARPS * HW, KB = 32 * KBS;
+  constexpr int HD = Geo<NP>::HD, H0 = WARPS * HD, KB = 32 * KBS;
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
   double* part = Cs + NP * KB;
@@ -289,37 +405,40 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
   const double* Yl = Y + r0 * ldy;
   double* Cl = C + r0 * ldc + col0;
   const int64_t rest = b - H0;
-  const int T = rest > 0 ? (int)((rest + HW - 1) / HW) : 0;
+  const int T = rest > 0 ? (int)((rest + HT - 1) / HT) : 0;
   const bool tskip = tri_skip != 0;
   bool bad = false;
-  double X[HW][KBS];
   auto ycol = [&](int r, int j) { return (r < b) ? __ldg(Yl + (int64_t)r * ldy + j) : 0.0; };
-  const int v0 = (int)max64(0, min64((int64_t)HW, b - (int64_t)w * HW));
+  const int v0 = (int)max64(0, min64((int64_t)HD, b - (int64_t)w * HD));
   if (TRANS) {
-    load_rows<HW, KBS>(X, Cl + (int64_t)w * HW * ldc, ldc, v0, ncb, 0, bad);
-    cta_apply<HW, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false);
+    {
+    double X[HD][KBS];
+    load_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, bad);
+    cta_apply<HD, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false);
     // rows < n become the ring's pivot rows; rows >= n are final
 #pragma unroll
-    for (int k = 0; k < HW; ++k) {
-      const int r = w * HW + k;
+    for (int k = 0; k < HD; ++k) {
+      const int r = w * HD + k;
       if (r < NP) {
 #pragma unroll
         for (int s = 0; s < KBS; ++s) Cs[r * KB + 32 * s + lane] = (r < n) ? X[k][s] : 0.0;
       }
     }
     {
-      const int lo = max(0, n - w * HW);
-      store_rows<HW, KBS>(X, Cl + (int64_t)w * HW * ldc, ldc, v0, ncb, 0, lo);
+      const int lo = max(0, n - w * HD);
+      store_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, lo);
+    }
     }
     for (int j = threadIdx.x; j < NP; j += THREADS) ver[j] = 0;
     __syncthreads();
+    double X[HT][KBS];
     for (int t = w; t < T; t += WARPS) {
-      const int64_t row = H0 + (int64_t)t * HW;
-      const int valid = (int)min64((int64_t)HW, b - row);
-      load_rows<HW, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
-      ring_apply_tile<HW, KBS, true>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
+      const int64_t row = H0 + (int64_t)t * HT;
+      const int valid = (int)min64((int64_t)HT, b - row);
+      load_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
+      ring_apply_tile<HT, KBS, true>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
                                      n, t, col0, false);
-      store_rows<HW, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
+      store_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < n * KB; idx += THREADS) {
@@ -336,26 +455,30 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
     }
     for (int j = threadIdx.x; j < NP; j += THREADS) ver[j] = 0;
     __syncthreads();
+    {
+    double X[HT][KBS];
     for (int o = w; o < T; o += WARPS) {
       const int t = T - 1 - o;
-      const int64_t row = H0 + (int64_t)t * HW;
-      const int valid = (int)min64((int64_t)HW, b - row);
+      const int64_t row = H0 + (int64_t)t * HT;
+      const int valid = (int)min64((int64_t)HT, b - row);
       if (zero_init) {
 #pragma unroll
-        for (int k = 0; k < HW; ++k)
+        for (int k = 0; k < HT; ++k)
 #pragma unroll
           for (int s = 0; s < KBS; ++s) X[k][s] = 0.0;
       } else {
-        load_rows<HW, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
+        load_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
       }
-      ring_apply_tile<HW, KBS, false>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
+      ring_apply_tile<HT, KBS, false>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
                                       n, o, col0, tskip);
-      store_rows<HW, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
+      store_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
+    }
     }
     __syncthreads();
+    double X[HD][KBS];
 #pragma unroll
-    for (int k = 0; k < HW; ++k) {
-      const int r = w * HW + k;
+    for (int k = 0; k < HD; ++k) {
+      const int r = w * HD + k;
 #pragma unroll
       for (int s = 0; s < KBS; ++s) {
         double x = 0.0;
@@ -365,8 +488,8 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
       }
     }
     __syncthreads();
-    cta_apply<HW, KBS, DENSE, false>(X, nullptr, n, ycol, tl, part, col0, tskip);
-    store_rows<HW, KBS>(X, Cl + (int64_t)w * HW * ldc, ldc, v0, ncb, 0);
+    cta_apply<HD, KBS, DENSE, false>(X, nullptr, n, ycol, tl, part, col0, tskip);
+    store_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0);
   }
 }
 
@@ -520,10 +643,10 @@ const char* tsqr_last_error(void) { return g_err; }
 int tsqr_f64_geometry(int64_t n, int64_t* np, int64_t* h0, int64_t* ht) {
   const int p = padded(n);
   if (n < 1 || !p) return set_err(CAQR_ERR_ARG, "n must be in [1, 128]");
-  int hw = p == 32 ? Geo<32>::HW : (p == 64 ? Geo<64>::HW : Geo<128>::HW);
+  const int hd = p == 32 ? Geo<32>::HD : (p == 64 ? Geo<64>::HD : Geo<128>::HD);
   if (np) *np = p;
-  if (ht) *ht = hw;
-  if (h0) *h0 = (int64_t)WARPS * hw;
+  if (ht) *ht = g_ht[np_index(p)];
+  if (h0) *h0 = (int64_t)WARPS * hd;
   return CAQR_OK;
 }
 
@@ -538,25 +661,31 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)P;
-#define CHAIN_LAUNCH(NPV, RWN)                                                                  \
-  {                                                                                             \
-    rc = prep(k_leaf_chain<NPV, RWN>, ChainSmem<NPV, RWN>::bytes);                              \
-    if (rc) return rc;                                                                          \
-    k_leaf_chain<NPV, RWN><<<grid, RWN * 32, ChainSmem<NPV, RWN>::bytes, st>>>(A, lda, m,       \
-        (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                \
+  if (n <= 8 && !Y && g_narrow) {
+    k_leaf_narrow<<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
+        A, lda, m, (int)n, (int)P, base, R, flag);
+    return check_launch("k_leaf_narrow");
   }
-#define LEAF_CASE(NPV)                                                                          \
+#define CHAIN_LAUNCH(NPV, HTV)                                                                  \
+  {                                                                                             \
+    rc = prep(k_leaf_chain<NPV, HTV>, ChainSmem<NPV, HTV>::bytes);                              \
+    if (rc) return rc;                                                                          \
+    k_leaf_chain<NPV, HTV><<<grid, RingCfg<NPV, HTV>::WARPS_R * 32, ChainSmem<NPV, HTV>::bytes,  \
+                             st>>>(A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R,  \
+                                   flag);                                                        \
+  }
+#define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
     int rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                    \
     if (rc) return rc;                                                                          \
     k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
         base, Y, ldy, tau, tau_stride, R, flag);                                                \
-    if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HW) {                                    \
-      if (g_ring_warps == 12) CHAIN_LAUNCH(NPV, 12) else CHAIN_LAUNCH(NPV, 8)                   \
+    if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                                    \
+      if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)           \
     }                                                                                           \
     break;                                                                                      \
   }
-  switch (p) { LEAF_CASE(32) LEAF_CASE(64) LEAF_CASE(128) }
+  switch (p) { LEAF_CASE(32, 16, 32) LEAF_CASE(64, 16, 32) LEAF_CASE(128, 8, 16) }
 #undef LEAF_CASE
 #undef CHAIN_LAUNCH
   return check_launch("k_leaf_dense/k_leaf_chain");
@@ -625,22 +754,27 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
   cudaStream_t st = (cudaStream_t)stream;
   const int kbs = (p == 128) ? 4 : 1;
   dim3 grid((unsigned)P, (unsigned)((ncols + 32 * kbs - 1) / (32 * kbs)));
-#define LA_CASE(NPV, KB_)                                                                         \
-  case NPV: {                                                                                     \
+#define LA_LAUNCH(NPV, KB_, HTV)                                                                  \
+  {                                                                                               \
     const size_t sm = LeafApplySmem<NPV, KB_>::bytes;                                             \
     if (transpose) {                                                                              \
-      int rc = prep(k_leaf_apply<NPV, KB_, true>, sm); if (rc) return rc;                         \
-      k_leaf_apply<NPV, KB_, true><<<grid, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, \
-          (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init, tri_skip);                 \
+      int rc = prep(k_leaf_apply<NPV, KB_, true, HTV>, sm); if (rc) return rc;                    \
+      k_leaf_apply<NPV, KB_, true, HTV><<<grid, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,    \
+          (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init, tri_skip);         \
     } else {                                                                                      \
-      int rc = prep(k_leaf_apply<NPV, KB_, false>, sm); if (rc) return rc;                        \
-      k_leaf_apply<NPV, KB_, false><<<grid, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,        \
+      int rc = prep(k_leaf_apply<NPV, KB_, false, HTV>, sm); if (rc) return rc;                   \
+      k_leaf_apply<NPV, KB_, false, HTV><<<grid, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,   \
           (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init, tri_skip);         \
     }                                                                                             \
+  }
+#define LA_CASE(NPV, KB_, HA, HB)                                                                 \
+  case NPV: {                                                                                     \
+    if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
-  switch (p) { LA_CASE(32, 1) LA_CASE(64, 1) LA_CASE(128, 4) }
+  switch (p) { LA_CASE(32, 1, 16, 32) LA_CASE(64, 1, 16, 32) LA_CASE(128, 4, 8, 16) }
 #undef LA_CASE
+#undef LA_LAUNCH
   return check_launch("k_leaf_apply");
 }
 
@@ -699,9 +833,15 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 }
 
 int caqr_tune(int key, int value) {
-  if (key == CAQR_TUNE_RING_WARPS) {
-    if (value != 8 && value != 12) return set_err(CAQR_ERR_ARG, "ring warps must be 8 or 12");
-    g_ring_warps = value;
+  if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
+    const int i = key - CAQR_TUNE_CHAIN_HT_32;
+    const int a = i == 2 ? 8 : 16, b = i == 2 ? 16 : 32;
+    if (value != a && value != b) return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
+    g_ht[i] = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_NARROW) {
+    g_narrow = value ? 1 : 0;
     return CAQR_OK;
   }
   return set_err(CAQR_ERR_ARG, "unknown tuning key");

@@ -213,3 +213,32 @@ def test_c1_full_size():
     assert oracle.r_diff(R, ref["R"]) <= 1000 * EPS
     assert oracle.residual(A, Q, R) <= 10 * n * EPS
     assert oracle.orthogonality(Q) <= 10 * n * EPS
+
+
+@pytest.mark.parametrize("m,n,P", [(16384 * 3 + 77, 8, 3), (5000, 5, 2), (1 << 16, 8, 4), (999, 1, 3),
+                                   (40000, 7, 1)])
+def test_narrow_r_only_matches_oracle(m, n, P):
+    """n <= 8, R only: lane-private chains + in-warp tree (k_leaf_narrow)."""
+    from paper_0809_2407_b200.tsqr import tsqr
+    from paper_0809_2407_b200.trees import ReductionTree
+
+    A = philox(m + n).uniform(-1, 1, (m, n))
+    R = tsqr(A, tree=ReductionTree(P=P))
+    Rref = oracle.tsqr_reference(A, P)["R"]
+    assert oracle.r_diff(R, Rref) <= 1000 * EPS
+    # ill-conditioned, same path
+    from paper_0809_2407_b200.core import CondSpec, gen_cond_matrix
+
+    A = gen_cond_matrix(CondSpec(4096, n, kappa=1e12, seed=n))
+    R = tsqr(A, leaf_rows=1024)
+    Rref = np.linalg.qr(A, mode="r")
+    assert oracle.r_diff(R, Rref) <= 1000 * EPS
+
+
+def test_narrow_rejects_nonfinite():
+    from paper_0809_2407_b200.tsqr import tsqr
+
+    A = philox(5).standard_normal((20000, 8))
+    A[12345, 7] = np.inf
+    with pytest.raises(ValueError):
+        tsqr(A, leaf_rows=4096)

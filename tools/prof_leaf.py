@@ -14,10 +14,12 @@ ap.add_argument("--leaves", type=int, default=148)
 ap.add_argument("--leaf-rows", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--q", default="none")
-ap.add_argument("--ring-warps", type=int, default=8)
+ap.add_argument("--ht", type=int, default=0)
 a = ap.parse_args()
 from paper_0809_2407_b200 import _lib
-_lib.tune(_lib.TUNE_RING_WARPS, a.ring_warps)
+np_ = 32 if a.n <= 32 else (64 if a.n <= 64 else 128)
+if a.ht:
+    _lib.tune(_lib.TUNE_CHAIN_HT[np_], a.ht)
 A = torch.randn(a.leaves * a.leaf_rows, a.n, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
     f = factor_device(A, a.leaves, want_q=a.q != "none")
@@ -33,4 +35,4 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 m, n = A.shape
-print(f"n={n} leaves={a.leaves} rows={a.leaf_rows}: {ms:.3f} ms, {(2*m*n*n - 2*n**3/3)/ms/1e9:.2f} TFLOP/s ring_warps={a.ring_warps}")
+print(f"n={n} leaves={a.leaves} rows={a.leaf_rows}: {ms:.3f} ms, {(2*m*n*n - 2*n**3/3)/ms/1e9:.2f} TFLOP/s ht={_lib.geometry(a.n)[2]}")
