@@ -69,6 +69,14 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
                          double* Y, int64_t ldy, double* tau, int64_t tau_stride,
                          double* R, int* flag, void* stream);
 
+/* R-only TSQR with the binary reduce tree (trees.py:52-66), everything on
+ * device: the leaves of BlockRowLayout(m, n, P), then every tree level.  The
+ * root R ends in Rslots[0] (P x n x n workspace).  tickets: device workspace
+ * of P * ceil(log2 P) ints (zeroed by the call; used by the fused-tree narrow
+ * path for n <= 8, may be null otherwise). */
+int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
+                      int* tickets, int* flag, void* stream);
+
 /* One level of the binary reduce tree: for every event e (int32 triples
  * {receiver, partner, node} in `events`, device memory), QR of
  * [R[receiver]; R[partner]] -> R[receiver]; node factor -> Ynode[node] (n x n

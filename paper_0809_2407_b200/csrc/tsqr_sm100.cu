@@ -47,7 +47,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // ---------------------------------------------------------------------------
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
-static int g_ht[3] = {16, 16, 8};  // NP = 32, 64, 128
+static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 1;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -186,7 +186,7 @@ __device__ __forceinline__ void narrow_step(double (&R)[8][8], double (&B)[K][8]
 
 __global__ void __launch_bounds__(NARROW_WARPS * 32, 1)
 k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-              double* Rout, int* flag) {
+              double* Rout, int* flag, int* tickets) {
   constexpr int K = NARROW_K;
   const int lane = threadIdx.x & 31;
   const int leaf = blockIdx.x * NARROW_WARPS + (threadIdx.x >> 5);
@@ -247,16 +247,63 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
       if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, B, n);
     }
   }
-  if (lane == 0) {
-    double* Ro = Rout + (int64_t)leaf * n * n;
+  bad = __any_sync(FULL, bad);
+  if (bad && lane == 0 && flag) atomicOr(flag, 1);
+  if (lane != 0) return;
+  auto put = [&](int node) {
+    double* Ro = Rout + (int64_t)node * n * n;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[i][c] : 0.0;
+  };
+  if (!tickets) {
+    put(leaf);
+    return;
   }
-  bad = __any_sync(FULL, bad);
-  if (bad && lane == 0 && flag) atomicOr(flag, 1);
+  // Fused binary tree (trees.py:52-66): at level k the second child to arrive
+  // at parent p combines [R_p-side; R_sibling] with the lower index on top.
+  int node = leaf;
+  for (int k = 1; (1 << (k - 1)) < P; ++k) {
+    const int p = node & ~((1 << k) - 1);
+    const int sib_hi = p + (1 << (k - 1));
+    if (sib_hi >= P) continue;  // unpaired at this level: pass up unchanged
+    put(node);
+    __threadfence();
+    const int t = atomicAdd(tickets + (int64_t)(k - 1) * P + p, 1);
+    if (t == 0) return;  // first arrival: the sibling finishes this node
+    __threadfence();
+    const int other = (node == p) ? sib_hi : p;
+    const double* Ro = Rout + (int64_t)other * n * n;
+    double Ro8[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        Ro8[i][c] = (i < n && c < n && c >= i) ? __ldcg(Ro + i * n + c) : 0.0;
+    if (node != p) {  // receiver (lower index) goes on top
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double tmp = R[i][c];
+          R[i][c] = Ro8[i][c];
+          Ro8[i][c] = tmp;
+        }
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double B[4][8];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) B[kk][c] = Ro8[4 * half + kk][c];
+      narrow_step<4>(R, B, n);
+    }
+    node = p;
+  }
+  put(node);  // the root (node 0)
 }
 
 // ---------------------------------------------------------------------------
@@ -271,7 +318,8 @@ struct TreeSmem {
 
 template <int NP>
 __global__ void __launch_bounds__(THREADS, 1)
-k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, double* taunode) {
+k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, double* taunode,
+              int bin_level) {
   constexpr int S = NP / 32, RW = NP / WARPS;
   extern __shared__ __align__(16) double sm[];
   double* Ps = sm;
@@ -280,7 +328,12 @@ k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, 
   double* red = vbuf + WARPS * RW;
   double* sx0 = red + WARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int a = ev[3 * blockIdx.x], b = ev[3 * blockIdx.x + 1], id = ev[3 * blockIdx.x + 2];
+  int a, b, id;
+  if (ev) {
+    a = ev[3 * blockIdx.x]; b = ev[3 * blockIdx.x + 1]; id = ev[3 * blockIdx.x + 2];
+  } else {  // binary tree level bin_level: pair (e 2^k, e 2^k + 2^(k-1)) (trees.py:52-66)
+    a = blockIdx.x << bin_level; b = a + (1 << (bin_level - 1)); id = 0;
+  }
   const double* Ra = Rslots + (int64_t)a * n * n;
   const double* Rb = Rslots + (int64_t)b * n * n;
   for (int idx = threadIdx.x; idx < NP * NP; idx += THREADS) {
@@ -298,13 +351,15 @@ k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, 
     }
   }
   __syncthreads();
-  cta_factor<NP, RW, STACKED>(X, Ps, n, taunode + (int64_t)id * n, red, sx0, part, vbuf);
+  cta_factor<NP, RW, STACKED>(X, Ps, n, taunode ? taunode + (int64_t)id * n : nullptr, red, sx0,
+                               part, vbuf);
   __syncthreads();
   double* Ro = Rslots + (int64_t)a * n * n;
   for (int idx = threadIdx.x; idx < n * n; idx += THREADS) {
     const int r = idx / n, c = idx - r * n;
     Ro[idx] = (c >= r) ? Ps[r * NP + c] : 0.0;
   }
+  if (!Ynode) return;
   double* Yo = Ynode + (int64_t)id * n * n;
 #pragma unroll
   for (int k = 0; k < RW; ++k) {
@@ -663,7 +718,7 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
   const int grid = (int)P;
   if (n <= 8 && !Y && g_narrow) {
     k_leaf_narrow<<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
-        A, lda, m, (int)n, (int)P, base, R, flag);
+        A, lda, m, (int)n, (int)P, base, R, flag, nullptr);
     return check_launch("k_leaf_narrow");
   }
 #define CHAIN_LAUNCH(NPV, HTV)                                                                  \
@@ -691,6 +746,43 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
   return check_launch("k_leaf_dense/k_leaf_chain");
 }
 
+int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
+                      int* tickets, int* flag, void* stream) {
+  const int p = padded(n);
+  if (!p || !A || !Rslots || P < 1 || m < n * P || lda < n || (!tickets && n <= 8 && P > 1))
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_r_binary: bad arguments");
+  const int64_t base = m / P;
+  if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
+  cudaStream_t st = (cudaStream_t)stream;
+  int levels = 0;
+  while ((1LL << levels) < P) ++levels;
+  if (n <= 8 && g_narrow) {
+    if (P > 1 && cudaMemsetAsync(tickets, 0, sizeof(int) * (size_t)levels * P, st) != cudaSuccess)
+      return check_launch("cudaMemsetAsync");
+    k_leaf_narrow<<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
+        A, lda, m, (int)n, (int)P, base, Rslots, flag, P > 1 ? tickets : nullptr);
+    return check_launch("k_leaf_narrow");
+  }
+  int rc = tsqr_f64_leaf_factor(A, lda, m, n, P, nullptr, 0, nullptr, 0, Rslots, flag, stream);
+  if (rc) return rc;
+  for (int k = 1; k <= levels; ++k) {
+    const int64_t nev = (P - 1 - (1LL << (k - 1))) / (1LL << k) + 1;  // f + 2^(k-1) < P, f = e 2^k
+#define TB_CASE(NPV)                                                                     \
+  case NPV: {                                                                            \
+    rc = prep(k_tree_factor<NPV>, TreeSmem<NPV>::bytes);                                 \
+    if (rc) return rc;                                                                   \
+    k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
+        nullptr, nullptr, nullptr, k);                                                   \
+    break;                                                                               \
+  }
+    switch (p) { TB_CASE(32) TB_CASE(64) TB_CASE(128) }
+#undef TB_CASE
+    rc = check_launch("k_tree_factor");
+    if (rc) return rc;
+  }
+  return CAQR_OK;
+}
+
 int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,
                                double* Ynode, double* taunode, void* stream) {
   const int p = padded(n);
@@ -703,7 +795,7 @@ int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events,
     int rc = prep(k_tree_factor<NPV>, TreeSmem<NPV>::bytes);                             \
     if (rc) return rc;                                                                   \
     k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
-        events, Ynode, taunode);                                                         \
+        events, Ynode, taunode, 0);                                                      \
     break;                                                                               \
   }
   switch (p) { TREE_CASE(32) TREE_CASE(64) TREE_CASE(128) }

@@ -122,8 +122,38 @@ def _tiles_per_leaf(layout: BlockRowLayout, h0: int, ht: int) -> int:
     return 1 + max(0, -(-(b - h0) // ht))
 
 
+_LEVEL_CACHE: dict = {}
+
+
 def _levels_on(tree: ReductionTree, device):
-    return [torch.from_numpy(lv).to(device) for lv in tree.device_levels()]
+    """Per-level event arrays on the device, packed once per (tree, device)."""
+    key = (tree.P, tree.shape, tree.levels, str(device))
+    lv = _LEVEL_CACHE.get(key)
+    if lv is None:
+        packed = tree.device_levels()
+        if packed:
+            flat = torch.from_numpy(np.concatenate(packed)).to(device)
+            lv, o = [], 0
+            for a in packed:
+                lv.append(flat[o:o + len(a)])
+                o += len(a)
+        else:
+            lv = []
+        _LEVEL_CACHE[key] = lv
+    return lv
+
+
+def _count(counter, layout, n, h0, ht, P):
+    for b in layout.block_rows:
+        f, d = count_geqr2(min(b, h0), n)
+        counter.add(f, d)
+        rest = b - min(b, h0)
+        while rest > 0:
+            f, d = count_tri_rect(n, min(ht, rest))
+            counter.add(f, d)
+            rest -= ht
+    f, d = count_stacked(n)
+    counter.add(f * (P - 1), d * (P - 1))
 
 
 def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: ReductionTree | None = None,
@@ -148,6 +178,16 @@ def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: Reduction
     st = _stream(dev)
     Rs = torch.empty((P, n, n), dtype=torch.float64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    if not want_q and tree.shape == BINARY:
+        # R only on the binary tree: one C-ABI call, no node factors stored
+        nlev = max(1, (P - 1).bit_length())
+        tickets = torch.empty(nlev * P, dtype=torch.int32, device=dev)
+        _lib.check(lib.tsqr_f64_r_binary(_ptr(A), n, m, n, P, _ptr(Rs), _ptr(tickets), _ptr(flag),
+                                         st), "tsqr_f64_r_binary")
+        _check_flag(flag)
+        if counter is not None:
+            _count(counter, layout, n, h0, ht, P)
+        return TsqrFactor(tree=tree, layout=layout, R=Rs[0], n=n, h0=h0, ht=ht, host=host)
     Y = tau = None
     if want_q:
         Y = Y_out if Y_out is not None else torch.empty_like(A)
@@ -166,16 +206,7 @@ def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: Reduction
                        "tsqr_f64_tree_factor_level")
     _check_flag(flag)
     if counter is not None:
-        for b in layout.block_rows:
-            f, d = count_geqr2(min(b, h0), n)
-            counter.add(f, d)
-            rest = b - min(b, h0)
-            while rest > 0:
-                f, d = count_tri_rect(n, min(ht, rest))
-                counter.add(f, d)
-                rest -= ht
-        f, d = count_stacked(n)
-        counter.add(f * (P - 1), d * (P - 1))
+        _count(counter, layout, n, h0, ht, P)
     return TsqrFactor(tree=tree, layout=layout, R=Rs[tree.root], n=n, h0=h0, ht=ht, Y=Y, tau=tau,
                       node_Y=node_Y, node_tau=node_tau, host=host, levels=levels)
 
