@@ -240,12 +240,6 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
   }
 }
 
-// ---------------------------------------------------------------------------
-// Ring step: one warp applies the n reflectors of its triangle-on-rectangle
-// tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
-// (stride NP) under the version protocol ver[j] == t.
-// On return X holds the tile's V (the stored rectangle of the factor).
-// ---------------------------------------------------------------------------
 // Branch-free reflector scalars for the pipelined ring.  Same conventions
 // as house_scalars (householder.py:101-111); sqrt and reciprocals from the
 // MUFU seeds refined by Newton steps (within 1 ulp), so the whole computation
@@ -284,155 +278,222 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
 }
 
 // ---------------------------------------------------------------------------
-// Ring step: one warp applies the n reflectors of its triangle-on-rectangle
-// tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
-// (stride NP) under the version protocol ver[j] == t.
-//
-// Software pipelined: reflector j+1 is generated (norm, ring wait, sqrt and
-// reciprocals) right after reflector j has updated the slot holding column
-// j+1, and its latency overlaps the update of the remaining slots.  The
-// broadcast vector is the RAW column x (v = scale * x); scale is folded into
-// the dot product / rank-1 coefficient and applied to the stored Y at the end.
-// On return X holds the tile's V (the stored rectangle of the factor).
-// ---------------------------------------------------------------------------
 #ifdef TSQR_SPIN_PROBE
 __device__ unsigned long long g_spin_cycles[2];
-#define SPIN_WAIT(ptr, target)                                  \
-  {                                                             \
-    long long t0_ = clock64();                                  \
-    while (ld_acquire(ptr) != (target)) { }                     \
-    if (lane == 0) atomicAdd(&g_spin_cycles[0], clock64() - t0_); \
-  }
-#else
-#define SPIN_WAIT(ptr, target) { while (ld_acquire(ptr) != (target)) { } }
 #endif
 
+// Leaner reflector scalars for the pipelined ring: y = rsqrt(a) after two
+// Newton steps (MUFU seeds are ~2^-20) is accurate to a few ulp, so
+// nrm = a*y needs no correction and tau = 1 + |x0|/nrm = 1 + |x0|*y needs no
+// division; scale = 1/(x0 - beta) = sign(x0)/(|x0| + nrm).  Conventions of
+// house_gen (householder.py:101-111), branch-free.
+__device__ __forceinline__ void house_lean(double x0, double sigma, double& beta, double& tau,
+                                           double& scale) {
+  const double a = fma(x0, x0, sigma);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  const double nrm = a * y;
+  const double ax = fabs(x0);
+  const double d = ax + nrm;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  const bool pos = (x0 >= 0.0);
+  const bool z = (sigma == 0.0);
+  beta = z ? ax : (pos ? -nrm : nrm);
+  tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
+  scale = z ? 0.0 : (pos ? r : -r);
+}
+
+// Raw dot products of the broadcast column v with this lane's columns in
+// slots [s0, S) (the next reflector's p, before its scalars are known).
+template <int NP, int HT, int s0>
+__device__ __forceinline__ void raw_dots(const double (&X)[HT][NP / 32], const double (&v)[HT],
+                                         double (&p)[NP / 32]) {
+  constexpr int S = NP / 32;
+#pragma unroll
+  for (int s2 = s0; s2 < S; ++s2) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      a0 = fma(v[k], X[k][s2], a0);
+      a1 = fma(v[k + 1], X[k + 1][s2], a1);
+      a2 = fma(v[k + 2], X[k + 2][s2], a2);
+      a3 = fma(v[k + 3], X[k + 3][s2], a3);
+    }
+    p[s2] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+// One reflector step of the ring.  Entering step j: v = raw column x_j,
+// p[s2] = x_j . X[:, c] for this lane's columns (raw dots), and the scalars
+// (beta, tau, scale) of reflector j.  s = slot of column j (lane jj), SN =
+// slot of column j+1.  The critical path is only: coefficient and rank-1
+// update of column j+1 -> its norm -> sqrt / reciprocal of reflector j+1.
+// The other columns' updates, the R row write-back, the broadcast of x_{j+1}
+// and the next raw dots are issued while those scalars are in flight.
+template <int NP, int HT, int s, int SN>
+__device__ __forceinline__ void ring_step(double (&X)[HT][NP / 32], double (&v)[HT],
+                                          double (&p)[NP / 32], double (&mysc)[NP / 32],
+                                          double& beta, double& tau, double& scale, double* Rs,
+                                          int* ver, double* vb, int n, int t, int jj,
+                                          double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  const int j = 32 * s + jj;
+  const int jn = j + 1;
+  const bool more = (SN < S) && (jn < n);
+  constexpr int SNc = (SN < S) ? SN : S - 1;
+  double* Rj = Rs + j * NP;
+  // (1) ring: R row j+1 as left by the previous tile
+  double x0n = 1.0;
+  if (more) {
+#ifdef TSQR_SPIN_PROBE
+    const long long t0_ = clock64();
+#endif
+    while (ld_acquire(ver + jn) != t) { }
+#ifdef TSQR_SPIN_PROBE
+    if (lane == 0) atomicAdd(&g_spin_cycles[0], clock64() - t0_);
+#endif
+    x0n = Rs[jn * NP + jn];
+  }
+  // (2) slot SN: coefficient, rank-1 update fused with the next column's norm
+  double sg = 0.0;
+  if (SN < S) {
+    const double r = Rj[32 * SNc + lane];
+    const bool act = (SNc > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[SNc], r) : 0.0;
+    const double w = q * scale;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      X[k][SNc] = fma(-v[k], w, X[k][SNc]);
+      X[k + 1][SNc] = fma(-v[k + 1], w, X[k + 1][SNc]);
+      X[k + 2][SNc] = fma(-v[k + 2], w, X[k + 2][SNc]);
+      X[k + 3][SNc] = fma(-v[k + 3], w, X[k + 3][SNc]);
+      s0 = fma(X[k][SNc], X[k][SNc], s0);
+      s1 = fma(X[k + 1][SNc], X[k + 1][SNc], s1);
+      s2 = fma(X[k + 2][SNc], X[k + 2][SNc], s2);
+      s3 = fma(X[k + 3][SNc], X[k + 3][SNc], s3);
+    }
+    sg = (s0 + s1) + (s2 + s3);
+    if (32 * SNc + lane > j) Rj[32 * SNc + lane] = r - q;
+  }
+  sg = __shfl_sync(FULL, sg, jn & 31);
+  // (3) scalars of reflector j+1 (latency) || the remaining columns of reflector j
+  double nbeta, ntau, nscale;
+  house_lean(x0n, sg, nbeta, ntau, nscale);
+#pragma unroll
+  for (int s2 = s; s2 < S; ++s2) {
+    if (s2 == SN) continue;
+    if (s2 == s && SN != s) continue;  // jj == 31: nothing of slot s lies right of j
+    const double r = Rj[32 * s2 + lane];
+    const bool act = (s2 > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[s2], r) : 0.0;
+    const double w = q * scale;
+#pragma unroll
+    for (int k = 0; k < HT; ++k) X[k][s2] = fma(-v[k], w, X[k][s2]);
+    if (32 * s2 + lane > j) Rj[32 * s2 + lane] = r - q;
+  }
+  if (lane == jj) Rj[j] = beta;
+  if (lane == 0 && tau_tile) tau_tile[j] = tau;
+  // (4) hand R row j to the next tile
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    st_release(ver + j, t + 1);
+  }
+  if (!more) return;
+  // (5) broadcast x_{j+1} (raw) and form its dot products with the updated tile
+  if (lane == (jn & 31)) {
+    mysc[SNc] = nscale;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2)
+      *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][SNc], X[k + 1][SNc]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < HT; k += 2) {
+    const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
+    v[k] = t2.x;
+    v[k + 1] = t2.y;
+  }
+  __syncwarp();  // vb may be overwritten in the next step
+  raw_dots<NP, HT, SNc>(X, v, p);
+  beta = nbeta;
+  tau = ntau;
+  scale = nscale;
+}
+
+template <int NP, int HT, int s>
+__device__ __forceinline__ void ring_slot(double (&X)[HT][NP / 32], double (&v)[HT],
+                                          double (&p)[NP / 32], double (&mysc)[NP / 32],
+                                          double& beta, double& tau, double& scale, double* Rs,
+                                          int* ver, double* vb, int n, int t, double* tau_tile) {
+  for (int jj = 0; jj < 31; ++jj) {
+    if (32 * s + jj >= n) return;
+    ring_step<NP, HT, s, s>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, jj, tau_tile);
+  }
+  if (32 * s + 31 >= n) return;
+  ring_step<NP, HT, s, s + 1>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, 31, tau_tile);
+}
+
+// ---------------------------------------------------------------------------
+// Ring tile: one warp applies the n reflectors of its triangle-on-rectangle
+// tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
+// (stride NP) under the version protocol ver[j] == t.  The broadcast vector
+// is the RAW column x (v = scale * x); scale is folded into the coefficients
+// and applied to the stored Y at the end, so on return X holds the tile's V
+// (the stored rectangle of the factor).
+// ---------------------------------------------------------------------------
 template <int NP, int HW>
 __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], double* Rs, int* ver,
                                                  double* vb, int n, int t, double* tau_tile) {
   constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
 #ifdef TSQR_SPIN_PROBE
   const long long tstart = clock64();
 #endif
-  const int lane = threadIdx.x & 31;
-  double mysc[S];  // this lane's column scale per slot (set when its reflector is made)
+  double mysc[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) mysc[s] = 1.0;
   double v[HW];
-  double beta = 0.0, tau = 0.0, scale = 0.0;
+  double p[S];
+  double beta, tau, scale;
+  {  // prologue: reflector 0
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    if (32 * s >= n) break;
-    // ---- reflector for the first column of the slot (not overlapped)
-    {
-      const int j = 32 * s;
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int k = 0; k < HW; k += 2) {
-        sa = fma(X[k][s], X[k][s], sa);
-        sb = fma(X[k + 1][s], X[k + 1][s], sb);
-      }
-      const double sg = __shfl_sync(FULL, sa + sb, 0);
-      SPIN_WAIT(ver + j, t)
-      house_fast(Rs[j * NP + j], sg, beta, tau, scale);
-      if (lane == 0) {
-        mysc[s] = scale;
-#pragma unroll
-        for (int k = 0; k < HW; k += 2)
-          *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][s], X[k + 1][s]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < HW; k += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
-        v[k] = t2.x;
-        v[k + 1] = t2.y;
-      }
+    for (int k = 0; k < HW; k += 2) {
+      s0 = fma(X[k][0], X[k][0], s0);
+      s1 = fma(X[k + 1][0], X[k + 1][0], s1);
     }
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = 32 * s + jj;
-      if (j >= n) break;
-      double* Rj = Rs + j * NP;
-      // ---- dot products of the raw column x with every active column
-      double p[S], pq[S];
+    const double sg = __shfl_sync(FULL, s0 + s1, 0);
+    while (ld_acquire(ver) != t) { }
+    house_lean(Rs[0], sg, beta, tau, scale);
+    if (lane == 0) {
+      mysc[0] = scale;
 #pragma unroll
-      for (int s2 = s; s2 < S; ++s2) { p[s2] = 0.0; pq[s2] = 0.0; }
-#pragma unroll
-      for (int k = 0; k < HW; k += 2) {
-#pragma unroll
-        for (int s2 = s; s2 < S; ++s2) {
-          p[s2] = fma(v[k], X[k][s2], p[s2]);
-          pq[s2] = fma(v[k + 1], X[k + 1][s2], pq[s2]);
-        }
-      }
-#pragma unroll
-      for (int s2 = s; s2 < S; ++s2) p[s2] += pq[s2];
-      double w[S];   // coefficient on the raw x: tau*scale*(R + scale*x.X)
-      double wr[S];  // R-row decrement: tau*(R + scale*x.X)
-#pragma unroll
-      for (int s2 = s; s2 < S; ++s2) {
-        const bool act = (s2 > s) || (lane > jj);
-        const double r = Rj[32 * s2 + lane];
-        const double q = act ? tau * fma(scale, p[s2], r) : 0.0;
-        wr[s2] = q;
-        w[s2] = q * scale;
-      }
-      // ---- update the slot that holds column j+1 first
-#pragma unroll
-      for (int k = 0; k < HW; ++k) X[k][s] = fma(-v[k], w[s], X[k][s]);
-      const bool more = (jj < 31) && (j + 1 < n);
-      double sg = 0.0;
-      {
-        double sa = 0.0, sb = 0.0;
-#pragma unroll
-        for (int k = 0; k < HW; k += 2) {
-          sa = fma(X[k][s], X[k][s], sa);
-          sb = fma(X[k + 1][s], X[k + 1][s], sb);
-        }
-        sg = __shfl_sync(FULL, sa + sb, (jj + 1) & 31);
-      }
-      if (more) SPIN_WAIT(ver + j + 1, t)
-      // ---- next reflector's scalars || remaining slots' updates
-      double nbeta, ntau, nscale;
-      house_fast(more ? Rs[(j + 1) * NP + j + 1] : 1.0, sg, nbeta, ntau, nscale);
-#pragma unroll
-      for (int s2 = s + 1; s2 < S; ++s2) {
-#pragma unroll
-        for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], w[s2], X[k][s2]);
-      }
-#pragma unroll
-      for (int s2 = s; s2 < S; ++s2) {
-        const int c = 32 * s2 + lane;
-        if (c > j) Rj[c] -= wr[s2];
-      }
-      if (lane == jj) Rj[j] = beta;
-      if (lane == 0 && tau_tile) tau_tile[j] = tau;
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        st_release(ver + j, t + 1);
-      }
-      if (more) {
-        if (lane == jj + 1) {
-          mysc[s] = nscale;
-#pragma unroll
-          for (int k = 0; k < HW; k += 2)
-            *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][s], X[k + 1][s]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < HW; k += 2) {
-          const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
-          v[k] = t2.x;
-          v[k + 1] = t2.y;
-        }
-        beta = nbeta;
-        tau = ntau;
-        scale = nscale;
-      }
+      for (int k = 0; k < HW; k += 2)
+        *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][0], X[k + 1][0]);
     }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < HW; k += 2) {
+      const double2 t2 = *reinterpret_cast<const double2*>(vb + k);
+      v[k] = t2.x;
+      v[k + 1] = t2.y;
+    }
+    __syncwarp();
+    raw_dots<NP, HW, 0>(X, v, p);
   }
-  // stored reflector entries: v = scale * x for every column of the tile
+  ring_slot<NP, HW, 0>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 1) ring_slot<NP, HW, 1>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 2) ring_slot<NP, HW, 2>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 3) ring_slot<NP, HW, 3>(X, v, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
 #pragma unroll
   for (int s = 0; s < S; ++s)
 #pragma unroll
