@@ -504,6 +504,198 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
 }
 
 // ---------------------------------------------------------------------------
+// Dual-chain ring (two leaves per CTA): every warp carries tile t of leaf 0
+// AND tile t of leaf 1 and runs both reflector chains in one instruction
+// stream, so the latency of one chain's norm / sqrt / reciprocal overlaps the
+// other chain's rank-1 updates.  Each leaf keeps its own ring (R rows stored
+// packed upper-triangular in shared memory, version counters, broadcast
+// buffer).  Packed row j starts at pk(j) = j*NP - j(j-1)/2; element (j, c),
+// c >= j, at pk(j) + c - j.
+// ---------------------------------------------------------------------------
+template <int NP>
+__host__ __device__ __forceinline__ int pk(int j) { return j * NP - (j * (j - 1)) / 2; }
+
+template <int NP, int HT, int C>
+struct Chains {
+  double X[C][HT][NP / 32];
+  double v[C][HT];
+  double p[C][NP / 32];
+  double mysc[C][NP / 32];
+  double beta[C], tau[C], scale[C];
+};
+
+// Per-chain buffers: chain c uses Rs0 + c*RSTR (packed R), ver0 + c*NP,
+// vb0 + c*VSTR and tau0 + c*tstr (tau0 may be null).
+#define CH_RS(c) (Rs0 + (c) * RSTR)
+#define CH_VER(c) (ver0 + (c) * NP)
+#define CH_VB(c) (vb0 + (c) * VSTR)
+template <int NP, int HT, int C, int RSTR, int VSTR, int s, int SN>
+__device__ __forceinline__ void ring_step_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
+                                            double* vb0, int n, int t, int jj, double* tau0,
+                                            int64_t tstr) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  const int j = 32 * s + jj;
+  const int jn = j + 1;
+  const bool more = (SN < S) && (jn < n);
+  constexpr int SNc = (SN < S) ? SN : S - 1;
+  const int rj = pk<NP>(j) - j;  // element (j, c) at rj + c
+  double x0n[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    x0n[c] = 1.0;
+    if (more) {
+      while (ld_acquire(CH_VER(c) + jn) != t) { }
+      x0n[c] = CH_RS(c)[pk<NP>(jn)];
+    }
+  }
+  double sg[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    sg[c] = 0.0;
+    if (SN < S) {
+      const int col = 32 * SNc + lane;
+      const double r = (col >= j) ? CH_RS(c)[rj + col] : 0.0;
+      const bool act = (SNc > s) || (lane > jj);
+      const double qq = act ? q.tau[c] * fma(q.scale[c], q.p[c][SNc], r) : 0.0;
+      const double w = qq * q.scale[c];
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < HT; k += 2) {
+        q.X[c][k][SNc] = fma(-q.v[c][k], w, q.X[c][k][SNc]);
+        q.X[c][k + 1][SNc] = fma(-q.v[c][k + 1], w, q.X[c][k + 1][SNc]);
+        s0 = fma(q.X[c][k][SNc], q.X[c][k][SNc], s0);
+        s1 = fma(q.X[c][k + 1][SNc], q.X[c][k + 1][SNc], s1);
+      }
+      sg[c] = s0 + s1;
+      if (col > j) CH_RS(c)[rj + col] = r - qq;
+    }
+  }
+  double nbeta[C], ntau[C], nscale[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    sg[c] = __shfl_sync(FULL, sg[c], jn & 31);
+    house_lean(x0n[c], sg[c], nbeta[c], ntau[c], nscale[c]);
+  }
+#pragma unroll
+  for (int s2 = s; s2 < S; ++s2) {
+    if (s2 == SN) continue;
+    if (s2 == s && SN != s) continue;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int col = 32 * s2 + lane;
+      const double r = (col >= j) ? CH_RS(c)[rj + col] : 0.0;
+      const bool act = (s2 > s) || (lane > jj);
+      const double qq = act ? q.tau[c] * fma(q.scale[c], q.p[c][s2], r) : 0.0;
+      const double w = qq * q.scale[c];
+#pragma unroll
+      for (int k = 0; k < HT; ++k) q.X[c][k][s2] = fma(-q.v[c][k], w, q.X[c][k][s2]);
+      if (col > j) CH_RS(c)[rj + col] = r - qq;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (lane == jj) CH_RS(c)[rj + j] = q.beta[c];
+    if (lane == 0 && tau0) tau0[c * tstr + j] = q.tau[c];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+#pragma unroll
+    for (int c = 0; c < C; ++c) st_release(CH_VER(c) + j, t + 1);
+  }
+  if (!more) return;
+  if (lane == (jn & 31)) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      q.mysc[c][SNc] = nscale[c];
+#pragma unroll
+      for (int k = 0; k < HT; k += 2)
+        *reinterpret_cast<double2*>(CH_VB(c) + k) = make_double2(q.X[c][k][SNc], q.X[c][k + 1][SNc]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      const double2 t2 = *reinterpret_cast<const double2*>(CH_VB(c) + k);
+      q.v[c][k] = t2.x;
+      q.v[c][k + 1] = t2.y;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    raw_dots<NP, HT, SNc>(q.X[c], q.v[c], q.p[c]);
+    q.beta[c] = nbeta[c];
+    q.tau[c] = ntau[c];
+    q.scale[c] = nscale[c];
+  }
+}
+
+template <int NP, int HT, int C, int RSTR, int VSTR, int s>
+__device__ __forceinline__ void ring_slot_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
+                                            double* vb0, int n, int t, double* tau0, int64_t tstr) {
+  for (int jj = 0; jj < 31; ++jj) {
+    if (32 * s + jj >= n) return;
+    ring_step_c<NP, HT, C, RSTR, VSTR, s, s>(q, Rs0, ver0, vb0, n, t, jj, tau0, tstr);
+  }
+  if (32 * s + 31 >= n) return;
+  ring_step_c<NP, HT, C, RSTR, VSTR, s, s + 1>(q, Rs0, ver0, vb0, n, t, 31, tau0, tstr);
+}
+
+template <int NP, int HT, int C, int RSTR, int VSTR>
+__device__ __forceinline__ void ring_tile_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
+                                            double* vb0, int n, int t, double* tau0, int64_t tstr) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) q.mysc[c][s] = 1.0;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      s0 = fma(q.X[c][k][0], q.X[c][k][0], s0);
+      s1 = fma(q.X[c][k + 1][0], q.X[c][k + 1][0], s1);
+    }
+    const double sg = __shfl_sync(FULL, s0 + s1, 0);
+    while (ld_acquire(CH_VER(c)) != t) { }
+    house_lean(CH_RS(c)[0], sg, q.beta[c], q.tau[c], q.scale[c]);
+    if (lane == 0) {
+      q.mysc[c][0] = q.scale[c];
+#pragma unroll
+      for (int k = 0; k < HT; k += 2)
+        *reinterpret_cast<double2*>(CH_VB(c) + k) = make_double2(q.X[c][k][0], q.X[c][k + 1][0]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      const double2 t2 = *reinterpret_cast<const double2*>(CH_VB(c) + k);
+      q.v[c][k] = t2.x;
+      q.v[c][k + 1] = t2.y;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < C; ++c) raw_dots<NP, HT, 0>(q.X[c], q.v[c], q.p[c]);
+  ring_slot_c<NP, HT, C, RSTR, VSTR, 0>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
+  if constexpr (S > 1) ring_slot_c<NP, HT, C, RSTR, VSTR, 1>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
+  if constexpr (S > 2) ring_slot_c<NP, HT, C, RSTR, VSTR, 2>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
+  if constexpr (S > 3) ring_slot_c<NP, HT, C, RSTR, VSTR, 3>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int k = 0; k < HT; ++k) q.X[c][k][s] *= q.mysc[c][s];
+}
+
+// ---------------------------------------------------------------------------
 // CTA-cooperative application of a DENSE (internal pivot, support r >= j) or
 // STACKED (external pivot rows Ps, support r <= j) factor to a block of C
 // columns held in registers.  Forward order (Q^T) or reverse (Q).

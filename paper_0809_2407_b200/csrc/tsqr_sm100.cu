@@ -48,7 +48,8 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
 static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
-static int g_narrow = 1;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
+static int g_narrow = 1;
+static int g_dual = 1;  // CAQR_TUNE_DUAL: two-leaf chain kernel for NP = 128, HT = 8  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -142,6 +143,99 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   for (int idx = threadIdx.x; idx < n * n; idx += NT) {
     const int r = idx / n, c = idx - r * n;
     Rl[idx] = (c >= r) ? Rs[r * NP + c] : 0.0;
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Dual-leaf chain kernel: CTA b runs the chains of leaves 2b and 2b+1 with
+// every warp carrying one tile of each (ring_tile_c, C = 2).  A CTA whose two
+// leaves have different tile counts (the ragged last leaf) or only one leaf
+// falls back to one chain per warp.
+// ---------------------------------------------------------------------------
+constexpr int DUAL_WARPS = 8;
+template <int NP, int HT>
+struct DualSmem {
+  static constexpr size_t bytes =
+      sizeof(double) * (2 * (size_t)(NP * (NP + 1) / 2) + 2 * DUAL_WARPS * HT) + sizeof(int) * 2 * NP;
+};
+
+template <int NP, int HT>
+__global__ void __launch_bounds__(DUAL_WARPS * 32, 1)
+k_leaf_chain2(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
+  constexpr int S = NP / 32, H0 = WARPS * Geo<NP>::HD, NT = DUAL_WARPS * 32;
+  constexpr int PKN = NP * (NP + 1) / 2;
+  constexpr int VSTR = DUAL_WARPS * HT;
+  extern __shared__ __align__(16) double sm[];
+  const int w = threadIdx.x >> 5;
+  bool bad = false;
+  const int L0 = 2 * (int)blockIdx.x;
+  const bool two = (L0 + 1 < P);
+  const int64_t r00 = (int64_t)L0 * base;
+  const int64_t b0 = (L0 == P - 1) ? m - r00 : base;
+  const int64_t r01 = r00 + base;
+  const int64_t b1 = two ? ((L0 + 1 == P - 1) ? m - r01 : base) : 0;
+  const int T0 = b0 > H0 ? (int)((b0 - H0 + HT - 1) / HT) : 0;
+  const int T1 = b1 > H0 ? (int)((b1 - H0 + HT - 1) / HT) : 0;
+  double* Rs0 = sm;
+  double* vball = sm + 2 * PKN;
+  int* ver0 = reinterpret_cast<int*>(vball + 2 * VSTR);
+  double* vb0 = vball + w * HT;
+  for (int c = 0; c < 2; ++c) {
+    if ((c == 0 ? T0 : T1) == 0) continue;
+    const double* Rl = Rio + (int64_t)(L0 + c) * n * n;
+    double* Rc = Rs0 + c * PKN;
+    for (int idx = threadIdx.x; idx < NP * NP; idx += NT) {
+      const int r = idx / NP, col = idx - r * NP;
+      if (col >= r) Rc[pk<NP>(r) + col - r] = (r < n && col < n) ? Rl[r * n + col] : 0.0;
+    }
+  }
+  for (int j = threadIdx.x; j < 2 * NP; j += NT) ver0[j] = 0;
+  __syncthreads();
+  double* tl0 = tau ? tau + (int64_t)L0 * tau_stride : nullptr;
+  if (T0 > 0 && T0 == T1) {
+    Chains<NP, HT, 2> q;
+    for (int t = w; t < T0; t += DUAL_WARPS) {
+      const int64_t row0 = r00 + H0 + (int64_t)t * HT, row1 = r01 + H0 + (int64_t)t * HT;
+      const int v0 = (int)min64((int64_t)HT, r00 + b0 - row0);
+      const int v1 = (int)min64((int64_t)HT, r01 + b1 - row1);
+      load_rows<HT, S>(q.X[0], A + row0 * lda, lda, v0, n, 0, bad);
+      load_rows<HT, S>(q.X[1], A + row1 * lda, lda, v1, n, 0, bad);
+      ring_tile_c<NP, HT, 2, PKN, VSTR>(q, Rs0, ver0, vb0, n, t,
+                                        tl0 ? tl0 + (int64_t)(t + 1) * n : nullptr, tau_stride);
+      if (Y) {
+        store_rows<HT, S>(q.X[0], Y + row0 * ldy, ldy, v0, n, 0);
+        store_rows<HT, S>(q.X[1], Y + row1 * ldy, ldy, v1, n, 0);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const int Tc = c == 0 ? T0 : T1;
+      if (Tc == 0) continue;
+      const int64_t rc0 = c == 0 ? r00 : r01, bc = c == 0 ? b0 : b1;
+      Chains<NP, HT, 1> q;
+      double* tlc = tau ? tau + (int64_t)(L0 + c) * tau_stride : nullptr;
+      for (int t = w; t < Tc; t += DUAL_WARPS) {
+        const int64_t row = rc0 + H0 + (int64_t)t * HT;
+        const int valid = (int)min64((int64_t)HT, rc0 + bc - row);
+        load_rows<HT, S>(q.X[0], A + row * lda, lda, valid, n, 0, bad);
+        ring_tile_c<NP, HT, 1, PKN, VSTR>(q, Rs0 + c * PKN, ver0 + c * NP, vb0 + c * VSTR, n, t,
+                                          tlc ? tlc + (int64_t)(t + 1) * n : nullptr, 0);
+        if (Y) store_rows<HT, S>(q.X[0], Y + row * ldy, ldy, valid, n, 0);
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < 2; ++c) {
+    if ((c == 0 ? T0 : T1) == 0) continue;
+    double* Rl = Rio + (int64_t)(L0 + c) * n * n;
+    const double* Rc = Rs0 + c * PKN;
+    for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+      const int r = idx / n, col = idx - r * n;
+      Rl[idx] = (col >= r) ? Rc[pk<NP>(r) + col - r] : 0.0;
+    }
   }
   if (bad && flag) atomicOr(flag, 1);
 }
@@ -705,6 +799,16 @@ int tsqr_f64_geometry(int64_t n, int64_t* np, int64_t* h0, int64_t* ht) {
   return CAQR_OK;
 }
 
+static int launch_dual(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, int64_t base,
+                       double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* R,
+                       int* flag, cudaStream_t st) {
+  int rc = prep(k_leaf_chain2<128, 8>, DualSmem<128, 8>::bytes);
+  if (rc) return rc;
+  k_leaf_chain2<128, 8><<<(int)((P + 1) / 2), DUAL_WARPS * 32, DualSmem<128, 8>::bytes, st>>>(
+      A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag);
+  return CAQR_OK;
+}
+
 int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Y,
                          int64_t ldy, double* tau, int64_t tau_stride, double* R, int* flag,
                          void* stream) {
@@ -736,7 +840,10 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
     k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
         base, Y, ldy, tau, tau_stride, R, flag);                                                \
     if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                                    \
-      if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)           \
+      if (NPV == 128 && g_dual && g_ht[np_index(NPV)] == 8) {                                    \
+        rc = launch_dual(A, lda, m, n, P, base, Y, ldy, tau, tau_stride, R, flag, st);           \
+        if (rc) return rc;                                                                      \
+      } else if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)     \
     }                                                                                           \
     break;                                                                                      \
   }
@@ -930,6 +1037,10 @@ int caqr_tune(int key, int value) {
     const int a = i == 2 ? 8 : 16, b = i == 2 ? 16 : 32;
     if (value != a && value != b) return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DUAL) {
+    g_dual = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_NARROW) {
