@@ -774,52 +774,79 @@ __device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int 
 // at Vt with stride ldv, rows >= vrows treated as zero) to [Cs; X]:
 // Cs = pivot rows (stride KB) in smem, X = this warp's tile of C.
 // ---------------------------------------------------------------------------
+// Shared-memory staging per warp for ring_apply_tile: the tile's V columns of
+// one block of 32 reflectors, transposed (row stride HW + 2 doubles: 16-byte
+// aligned rows, 2-way conflicts on the transposing stores), plus their tau.
+template <int HW>
+struct ApplyStage {
+  static constexpr int LD = HW + 2;
+  static constexpr int DOUBLES = 32 * LD + 32;
+};
+
 template <int HW, int KBS, bool TRANS>
 __device__ __forceinline__ void ring_apply_tile(double (&X)[HW][KBS], double* Cs, int* ver,
                                                 const double* __restrict__ Vt, int64_t ldv,
                                                 int vrows, const double* __restrict__ tau,
-                                                int n, int order, int col0, bool tri_skip) {
+                                                int n, int order, int col0, bool tri_skip,
+                                                double* vs) {
   constexpr int KB = 32 * KBS;
+  constexpr int LD = ApplyStage<HW>::LD;
   const int lane = threadIdx.x & 31;
-  double vn[HW];
-  double tn;
-  {
-    const int j = TRANS ? 0 : n - 1;
+  double* vt = vs + 32 * LD;
+  const int nb = (n + 31) / 32;
+  for (int bx = 0; bx < nb; ++bx) {
+    const int jb = TRANS ? bx : nb - 1 - bx;
+    // stage V[:, 32 jb + lane] (coalesced rows) and tau, transposed
+    {
+      const int c = 32 * jb + lane;
+      __syncwarp();
 #pragma unroll
-    for (int k = 0; k < HW; ++k) vn[k] = (k < vrows) ? __ldg(Vt + (int64_t)k * ldv + j) : 0.0;
-    tn = __ldg(tau + j);
-  }
-  for (int jx = 0; jx < n; ++jx) {
-    const int j = TRANS ? jx : n - 1 - jx;
-    double v[HW];
-#pragma unroll
-    for (int k = 0; k < HW; ++k) v[k] = vn[k];
-    const double tj = tn;
-    if (jx + 1 < n) {  // prefetch the next reflector
-      const int jn = TRANS ? j + 1 : j - 1;
-#pragma unroll
-      for (int k = 0; k < HW; ++k) vn[k] = (k < vrows) ? __ldg(Vt + (int64_t)k * ldv + jn) : 0.0;
-      tn = __ldg(tau + jn);
+      for (int k = 0; k < HW; k += 2) {
+        const double a0 = (k < vrows && c < n) ? __ldg(Vt + (int64_t)k * ldv + c) : 0.0;
+        const double a1 = (k + 1 < vrows && c < n) ? __ldg(Vt + (int64_t)(k + 1) * ldv + c) : 0.0;
+        *reinterpret_cast<double2*>(vs + lane * LD + k) = make_double2(a0, a1);
+      }
+      vt[lane] = (c < n) ? __ldg(tau + c) : 0.0;
+      __syncwarp();
     }
-    ring_wait(ver + j, order, lane);
-    if (tj != 0.0) {
+    const int jlim = min(32, n - 32 * jb);
+    for (int jx = 0; jx < jlim; ++jx) {
+      const int jj = TRANS ? jx : jlim - 1 - jx;
+      const int j = 32 * jb + jj;
+      const double tj = vt[jj];
+      double v[HW];
 #pragma unroll
-      for (int s2 = 0; s2 < KBS; ++s2) {
-        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
-        const double cold = Cs[j * KB + 32 * s2 + lane];
-        double p0 = cold, p1 = 0.0;
+      for (int k = 0; k < HW; k += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(vs + jj * LD + k);
+        v[k] = t2.x;
+        v[k + 1] = t2.y;
+      }
+      while (ld_acquire(ver + j) != order) { }
+      if (tj != 0.0) {
 #pragma unroll
-        for (int k = 0; k < HW; k += 2) {
-          p0 = fma(v[k], X[k][s2], p0);
-          p1 = fma(v[k + 1], X[k + 1][s2], p1);
+        for (int s2 = 0; s2 < KBS; ++s2) {
+          if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+          const double cold = Cs[j * KB + 32 * s2 + lane];
+          double p0 = cold, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < HW; k += 4) {
+            p0 = fma(v[k], X[k][s2], p0);
+            p1 = fma(v[k + 1], X[k + 1][s2], p1);
+            p2 = fma(v[k + 2], X[k + 2][s2], p2);
+            p3 = fma(v[k + 3], X[k + 3][s2], p3);
+          }
+          const double wv = tj * ((p0 + p1) + (p2 + p3));
+          Cs[j * KB + 32 * s2 + lane] = cold - wv;
+#pragma unroll
+          for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
         }
-        const double wv = tj * (p0 + p1);
-        Cs[j * KB + 32 * s2 + lane] = cold - wv;
-#pragma unroll
-        for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        st_release(ver + j, order + 1);
       }
     }
-    ring_signal(ver + j, order + 1, lane);
   }
 }
 

@@ -530,7 +530,8 @@ k_tree_apply(const double* __restrict__ Ynode, const double* __restrict__ taunod
 template <int NP, int KBS>
 struct LeafApplySmem {
   static constexpr size_t bytes =
-      sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS) + sizeof(int) * NP;
+      sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS +
+                        (size_t)WARPS * ApplyStage<32>::DOUBLES) + sizeof(int) * NP;
 };
 
 template <int NP, int KBS, bool TRANS, int HT>
@@ -543,7 +544,8 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
   double* part = Cs + NP * KB;
-  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * KB);
+  double* vstage = part + 2 * WARPS * KB + (threadIdx.x >> 5) * ApplyStage<HT>::DOUBLES;
+  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * KB + WARPS * ApplyStage<32>::DOUBLES);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int leaf = blockIdx.x;
   const int col0 = blockIdx.y * KB;
@@ -586,7 +588,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
       const int valid = (int)min64((int64_t)HT, b - row);
       load_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
       ring_apply_tile<HT, KBS, true>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
-                                     n, t, col0, false);
+                                     n, t, col0, false, vstage);
       store_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
     }
     __syncthreads();
@@ -619,7 +621,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
         load_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0, bad);
       }
       ring_apply_tile<HT, KBS, false>(X, Cs, ver, Yl + row * ldy, ldy, valid, tl + (int64_t)(t + 1) * n,
-                                      n, o, col0, tskip);
+                                      n, o, col0, tskip, vstage);
       store_rows<HT, KBS>(X, Cl + row * ldc, ldc, valid, ncb, 0);
     }
     }
