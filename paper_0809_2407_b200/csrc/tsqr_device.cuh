@@ -707,63 +707,86 @@ __device__ __forceinline__ void ring_tile_c(Chains<NP, HT, C>& q, double* Rs0, i
 template <int RW, int KBS, int MODE, bool TRANS, class YF>
 __device__ __forceinline__ void cta_apply(double (&X)[RW][KBS], double* Ps, int n, YF Ycol,
                                           const double* __restrict__ tau, double* part,
-                                          int col0, bool tri_skip) {
+                                          int col0, bool tri_skip, double* vs) {
   constexpr int KB = 32 * KBS;
+  constexpr int LD = RW + 2;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int jx = 0; jx < n; ++jx) {
-    const int j = TRANS ? jx : n - 1 - jx;
-    const int pw = j / RW;
-    const bool wact = (MODE == DENSE) ? (w >= pw) : (MODE == STACKED ? (w <= pw) : true);
-    double* pb = part + (jx & 1) * WARPS * KB;
-    const double tj = __ldg(tau + j);
-    double v[RW];
-    double pold[KBS];
-    if (wact) {
+  double* vt = vs + 32 * LD;
+  const int nb = (n + 31) / 32;
+  for (int bx = 0; bx < nb; ++bx) {
+    const int jb = TRANS ? bx : nb - 1 - bx;
+    {  // stage this warp's rows of the block's 32 reflector columns, transposed
+      const int c = 32 * jb + lane;
+      __syncwarp();
 #pragma unroll
-      for (int k = 0; k < RW; ++k) {
-        const int r = w * RW + k;
-        double vk = 0.0;
-        if (MODE == DENSE) {
-          if (r > j) vk = Ycol(r, j);
-          else if (r == j) vk = 1.0;
-        } else if (MODE == STACKED) {
-          if (r <= j) vk = Ycol(r, j);
-        } else {
-          vk = Ycol(r, j);
-        }
-        v[k] = vk;
+      for (int k = 0; k < RW; k += 2) {
+        const double a0 = (c < n) ? Ycol(w * RW + k, c) : 0.0;
+        const double a1 = (c < n) ? Ycol(w * RW + k + 1, c) : 0.0;
+        *reinterpret_cast<double2*>(vs + lane * LD + k) = make_double2(a0, a1);
       }
-#pragma unroll
-      for (int s2 = 0; s2 < KBS; ++s2) {
-        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
-        double p0 = 0.0, p1 = 0.0;
+      vt[lane] = (c < n) ? __ldg(tau + c) : 0.0;
+      __syncwarp();
+    }
+    const int jlim = min(32, n - 32 * jb);
+    for (int jx = 0; jx < jlim; ++jx) {
+      const int jj = TRANS ? jx : jlim - 1 - jx;
+      const int j = 32 * jb + jj;
+      const int pw = j / RW;
+      const bool wact = (MODE == DENSE) ? (w >= pw) : (MODE == STACKED ? (w <= pw) : true);
+      double* pb = part + (j & 1) * WARPS * KB;
+      const double tj = vt[jj];
+      double v[RW];
+      double pold[KBS];
+      if (wact) {
 #pragma unroll
         for (int k = 0; k < RW; k += 2) {
-          p0 = fma(v[k], X[k][s2], p0);
-          if (k + 1 < RW) p1 = fma(v[k + 1], X[k + 1][s2], p1);
+          const double2 t2 = *reinterpret_cast<const double2*>(vs + jj * LD + k);
+          v[k] = t2.x;
+          v[k + 1] = t2.y;
         }
-        double p = p0 + p1;
-        if (MODE != DENSE && w == 0) {
-          pold[s2] = Ps[j * KB + 32 * s2 + lane];
-          p += pold[s2];
+#pragma unroll
+        for (int k = 0; k < RW; ++k) {
+          const int r = w * RW + k;
+          if (MODE == DENSE) v[k] = (r > j) ? v[k] : (r == j ? 1.0 : 0.0);
+          else if (MODE == STACKED) v[k] = (r <= j) ? v[k] : 0.0;
         }
-        pb[w * KB + 32 * s2 + lane] = p;
+#pragma unroll
+        for (int s2 = 0; s2 < KBS; ++s2) {
+          if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < RW; k += 2) {
+            p0 = fma(v[k], X[k][s2], p0);
+            p1 = fma(v[k + 1], X[k + 1][s2], p1);
+          }
+          double p = p0 + p1;
+          if (MODE != DENSE && w == 0) {
+            pold[s2] = Ps[j * KB + 32 * s2 + lane];
+            p += pold[s2];
+          }
+          pb[w * KB + 32 * s2 + lane] = p;
+        }
       }
-    }
-    __syncthreads();
-    if (wact && tj != 0.0) {
-      const int q0 = (MODE == DENSE) ? pw : 0;
-      const int q1 = (MODE == STACKED) ? pw : WARPS - 1;
+      __syncthreads();
+      if (wact && tj != 0.0) {
+        const int q0 = (MODE == DENSE) ? pw : 0;
+        const int q1 = (MODE == STACKED) ? pw : WARPS - 1;
 #pragma unroll
-      for (int s2 = 0; s2 < KBS; ++s2) {
-        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
-        const int c = 32 * s2 + lane;
-        double tot = 0.0;
-        for (int q = q0; q <= q1; ++q) tot += pb[q * KB + c];
-        const double wv = tj * tot;
+        for (int s2 = 0; s2 < KBS; ++s2) {
+          if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+          const int c = 32 * s2 + lane;
+          double t0 = 0.0, t1 = 0.0;
+          int q = q0;
+          for (; q + 1 <= q1; q += 2) {
+            t0 += pb[q * KB + c];
+            t1 += pb[(q + 1) * KB + c];
+          }
+          if (q <= q1) t0 += pb[q * KB + c];
+          const double wv = tj * (t0 + t1);
 #pragma unroll
-        for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
-        if (MODE != DENSE && w == 0) Ps[j * KB + c] = pold[s2] - wv;
+          for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+          if (MODE != DENSE && w == 0) Ps[j * KB + c] = pold[s2] - wv;
+        }
       }
     }
   }

@@ -473,7 +473,8 @@ k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, 
 // ---------------------------------------------------------------------------
 template <int NP, int KBS>
 struct TreeApplySmem {
-  static constexpr size_t bytes = sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS);
+  static constexpr size_t bytes = sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS +
+                                                    (size_t)WARPS * (32 * (NP / WARPS + 2) + 32));
 };
 
 template <int NP, int KBS, bool TRANS>
@@ -486,6 +487,7 @@ k_tree_apply(const double* __restrict__ Ynode, const double* __restrict__ taunod
   double* Ps = sm;
   double* part = Ps + NP * KB;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* vstage = part + 2 * WARPS * KB + w * (32 * (RW + 2) + 32);
   const int a = ev[3 * blockIdx.x], b = ev[3 * blockIdx.x + 1], id = ev[3 * blockIdx.x + 2];
   const int col0 = blockIdx.y * KB;
   double* Ca = C + (int64_t)a * slot_rows * ldc;
@@ -508,8 +510,9 @@ k_tree_apply(const double* __restrict__ Ynode, const double* __restrict__ taunod
   }
   __syncthreads();
   const double* Yn = Ynode + (int64_t)id * n * n;
-  auto ycol = [&](int r, int j) { return __ldg(Yn + (int64_t)r * n + j); };
-  cta_apply<RW, KBS, STACKED, TRANS>(X, Ps, n, ycol, taunode + (int64_t)id * n, part, col0, false);
+  auto ycol = [&](int r, int j) { return (r < n) ? __ldg(Yn + (int64_t)r * n + j) : 0.0; };
+  cta_apply<RW, KBS, STACKED, TRANS>(X, Ps, n, ycol, taunode + (int64_t)id * n, part, col0, false,
+                                     vstage);
   __syncthreads();
   for (int idx = threadIdx.x; idx < n * KB; idx += THREADS) {
     const int r = idx / KB, c = idx - r * KB;
@@ -544,7 +547,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
   double* part = Cs + NP * KB;
-  double* vstage = part + 2 * WARPS * KB + (threadIdx.x >> 5) * ApplyStage<HT>::DOUBLES;
+  double* vstage = part + 2 * WARPS * KB + (threadIdx.x >> 5) * ApplyStage<32>::DOUBLES;
   int* ver = reinterpret_cast<int*>(part + 2 * WARPS * KB + WARPS * ApplyStage<32>::DOUBLES);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int leaf = blockIdx.x;
@@ -565,7 +568,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
     {
     double X[HD][KBS];
     load_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, bad);
-    cta_apply<HD, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false);
+    cta_apply<HD, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false, vstage);
     // rows < n become the ring's pivot rows; rows >= n are final
 #pragma unroll
     for (int k = 0; k < HD; ++k) {
@@ -639,7 +642,7 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
       }
     }
     __syncthreads();
-    cta_apply<HD, KBS, DENSE, false>(X, nullptr, n, ycol, tl, part, col0, tskip);
+    cta_apply<HD, KBS, DENSE, false>(X, nullptr, n, ycol, tl, part, col0, tskip, vstage);
     store_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0);
   }
 }
@@ -710,6 +713,7 @@ k_block_apply(const double* __restrict__ Yf, int64_t ldy, int rows, int n,
   double* Ps = sm;
   double* part = Ps + 128 * KB;
   const int w = threadIdx.x >> 5;
+  double* vstage = part + 2 * WARPS * KB + w * (32 * (RW + 2) + 32);
   const int col0 = blockIdx.x * KB;
   const int ncb = (int)min64(ncols - col0, KB);
   if (MODE == TRIRECT) {
@@ -724,7 +728,7 @@ k_block_apply(const double* __restrict__ Yf, int64_t ldy, int rows, int n,
   load_rows<RW, KBS>(X, C + (int64_t)w * RW * ldc + col0, ldc, valid, ncb, 0, bad);
   __syncthreads();
   auto ycol = [&](int r, int j) { return (r < rows) ? __ldg(Yf + (int64_t)r * ldy + j) : 0.0; };
-  cta_apply<RW, KBS, MODE, TRANS>(X, Ps, n, ycol, tau, part, col0, false);
+  cta_apply<RW, KBS, MODE, TRANS>(X, Ps, n, ycol, tau, part, col0, false, vstage);
   __syncthreads();
   store_rows<RW, KBS>(X, C + (int64_t)w * RW * ldc + col0, ldc, valid, ncb, 0);
   if (MODE == TRIRECT) {
@@ -1019,7 +1023,8 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
     return set_err(CAQR_ERR_ARG, "tsqr_f64_block_apply: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   constexpr int RW = 16, KBS = 1;
-  const size_t sm = sizeof(double) * ((size_t)128 * 32 * KBS + 2 * WARPS * 32 * KBS);
+  const size_t sm = sizeof(double) * ((size_t)128 * 32 * KBS + 2 * WARPS * 32 * KBS +
+                                      (size_t)WARPS * (32 * (RW + 2) + 32));
   dim3 grid((unsigned)((ncols + 32 * KBS - 1) / (32 * KBS)));
 #define BA_LAUNCH(MD, TR)                                                                      \
   {                                                                                            \
