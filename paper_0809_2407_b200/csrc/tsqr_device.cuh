@@ -129,6 +129,33 @@ __device__ __forceinline__ void store_rows(const double (&X)[RW][S], double* dst
   }
 }
 
+// Leaner reflector scalars for the pipelined ring: y = rsqrt(a) after two
+// Newton steps (MUFU seeds are ~2^-20) is accurate to a few ulp, so
+// nrm = a*y needs no correction and tau = 1 + |x0|/nrm = 1 + |x0|*y needs no
+// division; scale = 1/(x0 - beta) = sign(x0)/(|x0| + nrm).  Conventions of
+// house_gen (householder.py:101-111), branch-free.
+__device__ __forceinline__ void house_lean(double x0, double sigma, double& beta, double& tau,
+                                           double& scale) {
+  const double a = fma(x0, x0, sigma);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  const double nrm = a * y;
+  const double ax = fabs(x0);
+  const double d = ax + nrm;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  const bool pos = (x0 >= 0.0);
+  const bool z = (sigma == 0.0);
+  beta = z ? ax : (pos ? -nrm : nrm);
+  tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
+  scale = z ? 0.0 : (pos ? r : -r);
+}
+
 // ---------------------------------------------------------------------------
 // CTA-cooperative factorization sweep.
 //   DENSE  : pivot row j is row j of the block (internal), support rows r >= j
@@ -153,15 +180,16 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
       if (j >= n) return;
       const int pw = j / RW;
       // -- 1. partial sigma of column j over this warp's support rows
-      double sg = 0.0;
+      double sga[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int k = 0; k < RW; ++k) {
         const int r = w * RW + k;
         const bool in = (MODE == DENSE) ? (r > j)
                         : (MODE == STACKED ? (r <= j) : (MODE == STACKEDQ ? (r % n) <= j : true));
-        const double x = X[k][s];
-        if (in) sg = fma(x, x, sg);
+        const double x = in ? X[k][s] : 0.0;
+        sga[k & 3] = fma(x, x, sga[k & 3]);
       }
+      const double sg = (sga[0] + sga[1]) + (sga[2] + sga[3]);
       if (lane == jj) red[w] = sg;
       if (MODE == DENSE && w == pw && lane == jj) {
         double x0 = 0.0;
@@ -171,12 +199,17 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
         *sx0 = x0;
       }
       __syncthreads();
-      double sigma = 0.0;
+      double rq[WARPS];
 #pragma unroll
-      for (int q = 0; q < WARPS; ++q) sigma += red[q];
+      for (int q = 0; q < WARPS; ++q) rq[q] = red[q];
+#pragma unroll
+      for (int h = WARPS / 2; h >= 1; h /= 2)
+#pragma unroll
+        for (int q = 0; q < h; ++q) rq[q] += rq[q + h];
+      const double sigma = rq[0];
       const double x0 = (MODE == DENSE) ? *sx0 : Ps[j * NP + j];
       double beta, tau, scale;
-      house_scalars(x0, sigma, beta, tau, scale);
+      house_lean(x0, sigma, beta, tau, scale);
       const bool wact = (MODE == DENSE) ? (w >= pw) : (MODE == STACKED ? (w <= pw) : true);
       double v[RW];
       double pold[S];
@@ -202,13 +235,10 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
         // -- 3. partial dots with the trailing columns
 #pragma unroll
         for (int s2 = s; s2 < S; ++s2) {
-          double p0 = 0.0, p1 = 0.0;
+          double pa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int k = 0; k < RW; k += 2) {
-            p0 = fma(v[k], X[k][s2], p0);
-            if (k + 1 < RW) p1 = fma(v[k + 1], X[k + 1][s2], p1);
-          }
-          double p = p0 + p1;
+          for (int k = 0; k < RW; ++k) pa[k & 3] = fma(v[k], X[k][s2], pa[k & 3]);
+          double p = (pa[0] + pa[1]) + (pa[2] + pa[3]);
           if (MODE != DENSE && w == 0) {
             pold[s2] = Ps[j * NP + 32 * s2 + lane];
             p += pold[s2];
@@ -225,9 +255,14 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
         for (int s2 = s; s2 < S; ++s2) {
           const int c = 32 * s2 + lane;
           if (s2 > s || lane > jj) {
-            double tot = 0.0;
-            for (int q = q0; q <= q1; ++q) tot += part[q * NP + c];
-            const double wv = tau * tot;
+            double t0 = 0.0, t1 = 0.0;
+            int q = q0;
+            for (; q + 1 <= q1; q += 2) {
+              t0 += part[q * NP + c];
+              t1 += part[(q + 1) * NP + c];
+            }
+            if (q <= q1) t0 += part[q * NP + c];
+            const double wv = tau * (t0 + t1);
 #pragma unroll
             for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
             if (MODE != DENSE && w == 0) Ps[j * NP + c] = pold[s2] - wv;
@@ -282,32 +317,6 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
 __device__ unsigned long long g_spin_cycles[2];
 #endif
 
-// Leaner reflector scalars for the pipelined ring: y = rsqrt(a) after two
-// Newton steps (MUFU seeds are ~2^-20) is accurate to a few ulp, so
-// nrm = a*y needs no correction and tau = 1 + |x0|/nrm = 1 + |x0|*y needs no
-// division; scale = 1/(x0 - beta) = sign(x0)/(|x0| + nrm).  Conventions of
-// house_gen (householder.py:101-111), branch-free.
-__device__ __forceinline__ void house_lean(double x0, double sigma, double& beta, double& tau,
-                                           double& scale) {
-  const double a = fma(x0, x0, sigma);
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-  const double h = 0.5 * a;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  const double nrm = a * y;
-  const double ax = fabs(x0);
-  const double d = ax + nrm;
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  r = r * fma(-d, r, 2.0);
-  r = r * fma(-d, r, 2.0);
-  const bool pos = (x0 >= 0.0);
-  const bool z = (sigma == 0.0);
-  beta = z ? ax : (pos ? -nrm : nrm);
-  tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
-  scale = z ? 0.0 : (pos ? r : -r);
-}
 
 // Raw dot products of the broadcast column v with this lane's columns in
 // slots [s0, S) (the next reflector's p, before its scalars are known).
