@@ -75,8 +75,15 @@ def _panel_leaves(mj: int, w: int, leaf_rows: int) -> int:
 
 
 def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_rows: int = 2048,
-                device=None, counter=None) -> CaqrResult:
-    """CAQR of A (m x n, m >= n) with panel width b <= 128."""
+                device=None, counter=None, lookahead: bool = False) -> CaqrResult:
+    """CAQR of A (m x n, m >= n) with panel width b <= 128.
+
+    With ``lookahead`` the panels run on a high-priority stream:
+    panel j+1's columns are updated by Q_j and factored there while the
+    low-priority stream applies Q_j to the rest of the trailing matrix
+    (depth-1 lookahead; the data dependencies are the same as the
+    sequential right-looking order, so results are identical).
+    """
     lib = _lib.load()
     if layout is not None:
         b = layout.b
@@ -90,10 +97,13 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         raise DimensionError("layout does not match A")
     W = At.clone() if not host else At
     dev = W.device
-    st = _stream(dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    panels = []
-    for c0 in range(0, n, b):
+    starts = list(range(0, n, b))
+    nb = len(starts)
+    panels = [None] * nb
+
+    def factor(jp, st):
+        c0 = starts[jp]
         c1 = min(c0 + b, n)
         w = c1 - c0
         mj = m - c0
@@ -103,8 +113,9 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         tau = torch.zeros((P, _tiles_per_leaf(lay, h0, ht), w), dtype=torch.float64, device=dev)
         Rs = torch.empty((P, w, w), dtype=torch.float64, device=dev)
         base_ptr = _ptr(W) + 8 * (c0 * n + c0)
+        sh = int(st.cuda_stream)
         _lib.check(lib.tsqr_f64_leaf_factor(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
-                                            tau.shape[1] * w, _ptr(Rs), _ptr(flag), st),
+                                            tau.shape[1] * w, _ptr(Rs), _ptr(flag), sh),
                    "tsqr_f64_leaf_factor")
         tree = ReductionTree(P=P, shape=BINARY)
         levels = _levels_on(tree, dev)
@@ -114,22 +125,72 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
             node_tau = torch.zeros((P - 1, w), dtype=torch.float64, device=dev)
             for ev in levels:
                 _lib.check(lib.tsqr_f64_tree_factor_level(_ptr(Rs), w, _ptr(ev), ev.shape[0],
-                                                          _ptr(node_Y), _ptr(node_tau), st),
+                                                          _ptr(node_Y), _ptr(node_tau), sh),
                            "tsqr_f64_tree_factor_level")
         # root R onto the diagonal block (its strict lower part keeps leaf 0's Y)
         blk = W[c0:c1, c0:c1]
         blk.copy_(torch.tril(blk, -1) + Rs[tree.root])
-        if c1 < n:
-            cptr = _ptr(W) + 8 * (c0 * n + c1)
-            _lib.check(lib.tsqr_f64_leaf_apply(base_ptr, n, _ptr(tau), tau.shape[1] * w, mj, w, P,
-                                               cptr, n, n - c1, 0, 0, 0, 1, 0, 0, st),
-                       "tsqr_f64_leaf_apply")
-            for ev in levels:
-                _lib.check(lib.tsqr_f64_tree_apply_level(_ptr(node_Y), _ptr(node_tau), w, _ptr(ev),
-                                                         ev.shape[0], cptr, n, lay.base, n - c1,
-                                                         1, 0, st),
-                           "tsqr_f64_tree_apply_level")
-        panels.append(CaqrPanel(c0, c1, lay, tree, tau, node_Y, node_tau, levels))
+        panels[jp] = CaqrPanel(c0, c1, lay, tree, tau, node_Y, node_tau, levels)
+
+    def apply(jp, lo, hi, st):
+        """Q_jp^T applied to W[c0:, lo:hi] (leaf level, then the tree levels)."""
+        if lo >= hi:
+            return
+        pnl = panels[jp]
+        c0, w, P = pnl.c0, pnl.width, pnl.layout.P
+        mj = m - c0
+        base_ptr = _ptr(W) + 8 * (c0 * n + c0)
+        cptr = _ptr(W) + 8 * (c0 * n + lo)
+        sh = int(st.cuda_stream)
+        _lib.check(lib.tsqr_f64_leaf_apply(base_ptr, n, _ptr(pnl.tau), pnl.tau.shape[1] * w, mj, w,
+                                           P, cptr, n, hi - lo, 0, 0, 0, 1, 0, 0, sh),
+                   "tsqr_f64_leaf_apply")
+        for ev in pnl.levels:
+            _lib.check(lib.tsqr_f64_tree_apply_level(_ptr(pnl.node_Y), _ptr(pnl.node_tau), w,
+                                                     _ptr(ev), ev.shape[0], cptr, n,
+                                                     pnl.layout.base, hi - lo, 1, 0, sh),
+                       "tsqr_f64_tree_apply_level")
+
+    cur = torch.cuda.current_stream(dev)
+    if not lookahead or nb == 1:
+        for jp in range(nb):
+            factor(jp, cur)
+            if jp + 1 < nb:
+                apply(jp, starts[jp + 1], n, cur)
+    else:
+        sA = torch.cuda.Stream(device=dev, priority=-1)
+        sB = torch.cuda.Stream(device=dev, priority=0)
+        sA.wait_stream(cur)
+        sB.wait_stream(cur)
+        evF = [None] * nb
+        evB = [None] * nb
+        with torch.cuda.stream(sA):
+            factor(0, sA)
+            evF[0] = torch.cuda.Event()
+            evF[0].record(sA)
+        for jp in range(nb):
+            if jp + 1 < nb:
+                # near: block jp+1 already carries Q_0..Q_{jp-1} (far updates on sB)
+                if jp >= 1:
+                    sA.wait_event(evB[jp - 1])
+                with torch.cuda.stream(sA):
+                    nxt = starts[jp + 1]
+                    apply(jp, nxt, min(nxt + b, n), sA)
+                    factor(jp + 1, sA)
+                    evF[jp + 1] = torch.cuda.Event()
+                    evF[jp + 1].record(sA)
+            sB.wait_event(evF[jp])
+            with torch.cuda.stream(sB):
+                if jp + 2 < nb:
+                    apply(jp, starts[jp + 2], n, sB)
+                evB[jp] = torch.cuda.Event()
+                evB[jp].record(sB)
+        cur.wait_stream(sA)
+        cur.wait_stream(sB)
+        for pnl in panels:  # device buffers created on sA are read on sB
+            for t in (pnl.tau, pnl.node_Y, pnl.node_tau):
+                if t is not None:
+                    t.record_stream(sB)
     _check_flag(flag)
     if counter is not None:
         counter.add(2 * m * n * n - (2 * n ** 3) // 3)
