@@ -240,6 +240,10 @@ def run_ours(args, cfg):
     lo, hi = shard_rows(m, ws, rank)
     A = make_input(cfg, dev, seed=rank, rows=hi - lo) if not is_caqr else make_input(cfg, dev)
     P = _leaves_for(hi - lo, n, cfg["leaf"])
+    from paper_0809_2407_b200.tsqr import split_leaves
+
+    chains = 1 if is_caqr else split_leaves(hi - lo, n, P)
+    P *= chains
     want_q = cfg["q"] != "none"
     stream = torch.cuda.current_stream(dev)
 
@@ -249,7 +253,7 @@ def run_ours(args, cfg):
         if is_caqr:
             from paper_0809_2407_b200.caqr import caqr_factor
 
-            return caqr_factor(A, b=128, leaf_rows=cfg["leaf"])
+            return caqr_factor(A, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -327,7 +331,7 @@ def run_ours(args, cfg):
             from paper_0809_2407_b200.caqr import caqr_factor
 
             def e2e_step():
-                res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"])
+                res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
                 return res.R
         else:
             def e2e_step():
@@ -370,7 +374,7 @@ def run_ours(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic iid " + cfg["dist"] + " (torch Philox on device, seed = rank)",
             "config": {"workload": cfg["name"], "m": m, "n": n, "leaf_rows": cfg["leaf"],
-                       "leaves_per_gpu": P, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
+                       "leaves_per_gpu": P // chains, "gpu_chains_per_leaf": chains, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
                        "l2": "inputs larger than L2 (no flush needed)" if 8 * m * n > 256e6
                        else "inputs smaller than L2"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -392,6 +396,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--panel-chains", type=int, default=1,
+                    help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -75,7 +75,8 @@ def _panel_leaves(mj: int, w: int, leaf_rows: int) -> int:
 
 
 def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_rows: int = 2048,
-                device=None, counter=None, lookahead: bool = False) -> CaqrResult:
+                device=None, counter=None, lookahead: bool = False,
+                panel_chains: int = 1) -> CaqrResult:
     """CAQR of A (m x n, m >= n) with panel width b <= 128.
 
     With ``lookahead`` the panels run on a high-priority stream:
@@ -108,6 +109,8 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         w = c1 - c0
         mj = m - c0
         P = _panel_leaves(mj, w, leaf_rows)
+        while panel_chains > 1 and P < panel_chains and mj // (2 * P) >= max(256, 2 * w):
+            P *= 2  # split leaves into GPU chains (hybrid tree, see tsqr.split_leaves)
         lay = BlockRowLayout(mj, w, P)
         _, h0, ht = _lib.geometry(w)
         tau = torch.zeros((P, _tiles_per_leaf(lay, h0, ht), w), dtype=torch.float64, device=dev)

@@ -293,13 +293,33 @@ def _leaves_for(m: int, n: int, leaf_rows: int) -> int:
     return P
 
 
+def split_leaves(m: int, n: int, P: int, min_chains: int | None = None,
+                 min_rows: int = 512) -> int:
+    """GPU chains per leaf (a power of two) for a leaf count P.
+
+    A leaf processed as 2^k equal chains whose R factors are combined by a
+    binary tree is the paper's hybrid tree: the
+    binary tree over P*2^k chains combines every leaf's chains in its first
+    k levels.  Leaves are split until there is at least one chain per SM
+    (``min_chains``), keeping chains >= max(min_rows, 4n) rows.
+    """
+    if min_chains is None:
+        min_chains = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    k = 1
+    while P * k < min_chains and m // (P * 2 * k) >= max(min_rows, 4 * n):
+        k *= 2
+    return k
+
+
 def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None = None,
-         device=None, counter=None):
+         device=None, counter=None, split: bool = True):
     """Convenience TSQR: returns R, (R, factor) or (R, Q).
 
     q = "none" (R only), "implicit" (R + TsqrFactor) or "explicit" (R + thin Q).
-    Leaves follow BlockRowLayout(m, n, floor(m / leaf_rows)).  R follows the
-    reference's sign convention (beta = -sign(x0)||x||: mixed-sign diagonal).
+    Leaves follow BlockRowLayout(m, n, floor(m / leaf_rows)); with ``split``
+    (default, binary tree only) each leaf runs as 2^k GPU chains when there
+    are fewer leaves than SMs (``split_leaves``).  R follows the reference's
+    sign convention (beta = -sign(x0)||x||: mixed-sign diagonal).
     """
     if q not in ("none", "implicit", "explicit"):
         raise ValueError(f"q must be none / implicit / explicit, got {q!r}")
@@ -307,7 +327,12 @@ def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None =
     m, n = At.shape
     if m < n:
         raise DimensionError(f"need m >= n, got {m} x {n}")
-    P = tree.P if tree is not None else _leaves_for(m, n, leaf_rows)
+    if tree is not None:
+        P = tree.P
+    else:
+        P = _leaves_for(m, n, leaf_rows)
+        if split:
+            P *= split_leaves(m, n, P)
     f = factor_device(At, P, want_q=(q != "none"), tree=tree, counter=counter, host=host)
     if q == "none":
         return f.R_out()
