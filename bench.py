@@ -303,8 +303,14 @@ def run_ours(args, cfg):
         t_leaf = float(np.mean([a.elapsed_time(b) for a, b in leaf_ev])) * 1e-3
         F_leaf = flops(hi - lo, n)
         ach = F_leaf / t_leaf / 1e12
+        # DRAM traffic of the chain kernel from the committed ncu capture
+        # (profiles/r01/chain_kernel_ncu_summary.txt: 1.233e9 B read + 5.9e6 B
+        # written for 148 leaves of 8192 x 128 = 1.020x the 8mn algorithmic
+        # bytes), scaled to this launch's rows; None for other widths.
+        traffic = 8.0 * (hi - lo) * n * 1.0245 if (n == 128 and cfg["q"] == "none") else None
         roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_source": "ncu --set full, profiles/r01 (scaled per launch)",
                 "kernel": "k_leaf_factor + k_tree_factor (one factor_device call)",
                 "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
                                "entry in MEASURED_PEAKS.json)",
