@@ -452,6 +452,168 @@ __device__ __forceinline__ void ring_slot(double (&X)[HT][NP / 32], double (&v)[
 }
 
 // ---------------------------------------------------------------------------
+// Shared-vector variant of the ring step: the broadcast column x_j is read
+// from a double-buffered per-warp shared slot (vb + (j&1)*HT) at its point of
+// use instead of being held in registers, which frees 2*HT registers per
+// thread for taller tiles (HT = 24 at n = 128).
+// ---------------------------------------------------------------------------
+template <int NP, int HT, int s0>
+__device__ __forceinline__ void raw_dots_vs(const double (&X)[HT][NP / 32], const double* vx,
+                                            double (&p)[NP / 32]) {
+  constexpr int S = NP / 32;
+  double a[S][2];
+#pragma unroll
+  for (int s2 = s0; s2 < S; ++s2) { a[s2][0] = 0.0; a[s2][1] = 0.0; }
+#pragma unroll
+  for (int k = 0; k < HT; k += 2) {
+    const double2 v2 = *reinterpret_cast<const double2*>(vx + k);
+#pragma unroll
+    for (int s2 = s0; s2 < S; ++s2) {
+      a[s2][0] = fma(v2.x, X[k][s2], a[s2][0]);
+      a[s2][1] = fma(v2.y, X[k + 1][s2], a[s2][1]);
+    }
+  }
+#pragma unroll
+  for (int s2 = s0; s2 < S; ++s2) p[s2] = a[s2][0] + a[s2][1];
+}
+
+template <int NP, int HT, int s, int SN>
+__device__ __forceinline__ void ring_step_vs(double (&X)[HT][NP / 32], double (&p)[NP / 32],
+                                             double (&mysc)[NP / 32], double& beta, double& tau,
+                                             double& scale, double* Rs, int* ver, double* vb,
+                                             int n, int t, int jj, double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  const int j = 32 * s + jj;
+  const int jn = j + 1;
+  const bool more = (SN < S) && (jn < n);
+  constexpr int SNc = (SN < S) ? SN : S - 1;
+  double* Rj = Rs + j * NP;
+  const double* vx = vb + (j & 1) * HT;   // x_j
+  double* vnx = vb + (jn & 1) * HT;       // x_{j+1}
+  double x0n = 1.0;
+  if (more) {
+    while (ld_acquire(ver + jn) != t) { }
+    x0n = Rs[jn * NP + jn];
+  }
+  double sg = 0.0;
+  if (SN < S) {
+    const double r = Rj[32 * SNc + lane];
+    const bool act = (SNc > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[SNc], r) : 0.0;
+    const double w = q * scale;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      const double2 vc = *reinterpret_cast<const double2*>(vx + k + 2);
+      X[k][SNc] = fma(-va.x, w, X[k][SNc]);
+      X[k + 1][SNc] = fma(-va.y, w, X[k + 1][SNc]);
+      X[k + 2][SNc] = fma(-vc.x, w, X[k + 2][SNc]);
+      X[k + 3][SNc] = fma(-vc.y, w, X[k + 3][SNc]);
+      s0 = fma(X[k][SNc], X[k][SNc], s0);
+      s1 = fma(X[k + 1][SNc], X[k + 1][SNc], s1);
+      s2 = fma(X[k + 2][SNc], X[k + 2][SNc], s2);
+      s3 = fma(X[k + 3][SNc], X[k + 3][SNc], s3);
+    }
+    sg = (s0 + s1) + (s2 + s3);
+    if (32 * SNc + lane > j) Rj[32 * SNc + lane] = r - q;
+  }
+  sg = __shfl_sync(FULL, sg, jn & 31);
+  double nbeta, ntau, nscale;
+  house_lean(x0n, sg, nbeta, ntau, nscale);
+#pragma unroll
+  for (int s2 = s; s2 < S; ++s2) {
+    if (s2 == SN) continue;
+    if (s2 == s && SN != s) continue;
+    const double r = Rj[32 * s2 + lane];
+    const bool act = (s2 > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[s2], r) : 0.0;
+    const double w = q * scale;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      X[k][s2] = fma(-va.x, w, X[k][s2]);
+      X[k + 1][s2] = fma(-va.y, w, X[k + 1][s2]);
+    }
+    if (32 * s2 + lane > j) Rj[32 * s2 + lane] = r - q;
+  }
+  if (lane == jj) Rj[j] = beta;
+  if (lane == 0 && tau_tile) tau_tile[j] = tau;
+  __syncwarp();  // R row j written; every lane is done with x_{j-1} in vnx
+  if (lane == 0) {
+    __threadfence_block();
+    st_release(ver + j, t + 1);
+  }
+  if (!more) return;
+  if (lane == (jn & 31)) {
+    mysc[SNc] = nscale;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2)
+      *reinterpret_cast<double2*>(vnx + k) = make_double2(X[k][SNc], X[k + 1][SNc]);
+  }
+  __syncwarp();
+  raw_dots_vs<NP, HT, SNc>(X, vnx, p);
+  beta = nbeta;
+  tau = ntau;
+  scale = nscale;
+}
+
+template <int NP, int HT, int s>
+__device__ __forceinline__ void ring_slot_vs(double (&X)[HT][NP / 32], double (&p)[NP / 32],
+                                             double (&mysc)[NP / 32], double& beta, double& tau,
+                                             double& scale, double* Rs, int* ver, double* vb,
+                                             int n, int t, double* tau_tile) {
+  for (int jj = 0; jj < 31; ++jj) {
+    if (32 * s + jj >= n) return;
+    ring_step_vs<NP, HT, s, s>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, jj, tau_tile);
+  }
+  if (32 * s + 31 >= n) return;
+  ring_step_vs<NP, HT, s, s + 1>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, 31, tau_tile);
+}
+
+// Same contract as ring_factor_tile; vb holds 2*HT doubles for this warp.
+template <int NP, int HW>
+__device__ __forceinline__ void ring_factor_tile_vs(double (&X)[HW][NP / 32], double* Rs, int* ver,
+                                                    double* vb, int n, int t, double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  double mysc[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) mysc[s] = 1.0;
+  double p[S];
+  double beta, tau, scale;
+  {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HW; k += 2) {
+      s0 = fma(X[k][0], X[k][0], s0);
+      s1 = fma(X[k + 1][0], X[k + 1][0], s1);
+    }
+    const double sg = __shfl_sync(FULL, s0 + s1, 0);
+    while (ld_acquire(ver) != t) { }
+    house_lean(Rs[0], sg, beta, tau, scale);
+    __syncwarp();
+    if (lane == 0) {
+      mysc[0] = scale;
+#pragma unroll
+      for (int k = 0; k < HW; k += 2)
+        *reinterpret_cast<double2*>(vb + k) = make_double2(X[k][0], X[k + 1][0]);
+    }
+    __syncwarp();
+    raw_dots_vs<NP, HW, 0>(X, vb, p);
+  }
+  ring_slot_vs<NP, HW, 0>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 1) ring_slot_vs<NP, HW, 1>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 2) ring_slot_vs<NP, HW, 2>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+  if constexpr (S > 3) ring_slot_vs<NP, HW, 3>(X, p, mysc, beta, tau, scale, Rs, ver, vb, n, t, tau_tile);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int k = 0; k < HW; ++k) X[k][s] *= mysc[s];
+}
+
+// ---------------------------------------------------------------------------
 // Ring tile: one warp applies the n reflectors of its triangle-on-rectangle
 // tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
 // (stride NP) under the version protocol ver[j] == t.  The broadcast vector

@@ -61,7 +61,7 @@ template <int NP, int HT>
 struct ChainSmem {
   static constexpr int RWN = RingCfg<NP, HT>::WARPS_R;
   static constexpr size_t bytes =
-      sizeof(double) * ((size_t)NP * NP + RWN * HT) + sizeof(int) * NP;
+      sizeof(double) * ((size_t)NP * NP + RWN * 2 * HT) + sizeof(int) * NP;
 };
 
 // Dense first tile of every leaf: rows [0, H0) (zero padded), CTA sweep.
@@ -114,7 +114,7 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   extern __shared__ __align__(16) double sm[];
   double* Rs = sm;
   double* vbuf = Rs + NP * NP;
-  int* ver = reinterpret_cast<int*>(vbuf + RING_WARPS * HW);
+  int* ver = reinterpret_cast<int*>(vbuf + RING_WARPS * 2 * HW);
   const int w = threadIdx.x >> 5;
   bool bad = false;
   const int leaf = blockIdx.x;
@@ -136,7 +136,12 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
     const int64_t row = r0 + H0 + (int64_t)t * HW;
     const int valid = (int)min64((int64_t)HW, r0 + b - row);
     load_rows<HW, S>(X, A + row * lda, lda, valid, n, 0, bad);
-    ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * HW, n, t, tl ? tl + (int64_t)(t + 1) * n : nullptr);
+    if constexpr (NP == 128 && HW > 16)
+      ring_factor_tile_vs<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
+                                  tl ? tl + (int64_t)(t + 1) * n : nullptr);
+    else
+      ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
+                               tl ? tl + (int64_t)(t + 1) * n : nullptr);
     if (Y) store_rows<HW, S>(X, Y + row * ldy, ldy, valid, n, 0);
   }
   __syncthreads();
@@ -253,8 +258,12 @@ k_leaf_chain2(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
 constexpr int NARROW_K = 4;
 constexpr int NARROW_WARPS = 8;
 
+// Packed upper-triangular 8x8 R in registers: element (i, c), c >= i.
+__host__ __device__ constexpr int pk8(int i, int c) { return i * 8 - (i * (i - 1)) / 2 + (c - i); }
+
+// One triangle-on-rectangle step [R; B] (householder.py:297-332) on K rows.
 template <int K>
-__device__ __forceinline__ void narrow_step(double (&R)[8][8], double (&B)[K][8], int n) {
+__device__ __forceinline__ void narrow_step(double (&R)[36], double (&B)[K][8], int n) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     if (j >= n) break;
@@ -262,19 +271,43 @@ __device__ __forceinline__ void narrow_step(double (&R)[8][8], double (&B)[K][8]
 #pragma unroll
     for (int k = 0; k < K; ++k) sg = fma(B[k][j], B[k][j], sg);
     double beta, tau, scale;
-    house_fast(R[j][j], sg, beta, tau, scale);
+    house_lean(R[pk8(j, j)], sg, beta, tau, scale);
 #pragma unroll
     for (int c = j + 1; c < 8; ++c) {
       double d = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) d = fma(B[k][j], B[k][c], d);
-      const double q = tau * fma(scale, d, R[j][c]);
-      R[j][c] -= q;
+      const double q = tau * fma(scale, d, R[pk8(j, c)]);
+      R[pk8(j, c)] -= q;
       const double qs = q * scale;
 #pragma unroll
       for (int k = 0; k < K; ++k) B[k][c] = fma(-B[k][j], qs, B[k][c]);
     }
-    R[j][j] = beta;
+    R[pk8(j, j)] = beta;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void narrow_load(double (&Bt)[K][8], const double* __restrict__ A,
+                                            int64_t lda, int64_t r0, int64_t b, int64_t q, int n,
+                                            int lane) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int64_t row = q * 32 * K + (int64_t)k * 32 + lane;  // rows interleaved over lanes
+    const bool ok = row < b;
+    const double* src = A + (r0 + row) * lda;
+    if (ok && n == 8 && lda == 8) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 t = __ldg(s2 + c);
+        Bt[k][2 * c] = t.x;
+        Bt[k][2 * c + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Bt[k][c] = (ok && c < n) ? __ldg(src + c) : 0.0;
+    }
   }
 }
 
@@ -287,70 +320,49 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
   if (leaf >= P) return;
   const int64_t r0 = (int64_t)leaf * base;
   const int64_t b = (leaf == P - 1) ? m - r0 : base;
-  bool bad = false;
-  double R[8][8];
+  double R[36];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) R[i][c] = 0.0;
+  for (int i = 0; i < 36; ++i) R[i] = 0.0;
   const int64_t rounds = (b + 32 * K - 1) / (32 * K);
-  double Bn[K][8];
-  auto load = [&](double (&Bt)[K][8], int64_t q) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int64_t row = q * 32 * K + (int64_t)lane * K + k;
-      const bool ok = row < b;
-      const double* src = A + (r0 + row) * lda;
-      if (ok && n == 8 && lda == 8) {
-        const double2* s2 = reinterpret_cast<const double2*>(src);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double2 t = __ldg(s2 + c);
-          Bt[k][2 * c] = t.x;
-          Bt[k][2 * c + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) Bt[k][c] = (ok && c < n) ? __ldg(src + c) : 0.0;
-      }
-    }
-  };
-  if (rounds > 0) load(Bn, 0);
-  for (int64_t q = 0; q < rounds; ++q) {
-    double B[K][8];
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        B[k][c] = Bn[k][c];
-        bad |= !isfinite(B[k][c]);
-      }
-    if (q + 1 < rounds) load(Bn, q + 1);
-    narrow_step<K>(R, B, n);
+  // double-buffered prefetch without register copies: two rounds per trip
+  double B0[K][8], B1[K][8];
+  if (rounds > 0) narrow_load<K>(B0, A, lda, r0, b, 0, n, lane);
+  for (int64_t q = 0; q < rounds; q += 2) {
+    if (q + 1 < rounds) narrow_load<K>(B1, A, lda, r0, b, q + 1, n, lane);
+    narrow_step<K>(R, B0, n);
+    if (q + 1 >= rounds) break;
+    if (q + 2 < rounds) narrow_load<K>(B0, A, lda, r0, b, q + 2, n, lane);
+    narrow_step<K>(R, B1, n);
   }
-  // in-warp binary tree over the lane R factors
+  // in-warp binary tree over the lane R factors (partner rows in two halves)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
-      double B[4][8];
+      double Bs[4][8];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) B[k][c] = __shfl_down_sync(FULL, R[4 * half + k][c], off);
-      if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, B, n);
+        for (int c = 0; c < 8; ++c) {
+          const int i = 4 * half + k;
+          Bs[k][c] = (c >= i) ? __shfl_down_sync(FULL, R[pk8(i, c)], off) : 0.0;
+        }
+      if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, Bs, n);
     }
   }
-  bad = __any_sync(FULL, bad);
-  if (bad && lane == 0 && flag) atomicOr(flag, 1);
   if (lane != 0) return;
+  // a NaN/Inf anywhere in the leaf reaches its R (every entry enters a norm)
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 36; ++i) bad |= !isfinite(R[i]);
+  if (bad && flag) atomicOr(flag, 1);
   auto put = [&](int node) {
     double* Ro = Rout + (int64_t)node * n * n;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[i][c] : 0.0;
+        if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[pk8(i, c < i ? i : c)] : 0.0;
   };
   if (!tickets) {
     put(leaf);
@@ -370,30 +382,30 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
     __threadfence();
     const int other = (node == p) ? sib_hi : p;
     const double* Ro = Rout + (int64_t)other * n * n;
-    double Ro8[8][8];
+    double Ro8[36];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        Ro8[i][c] = (i < n && c < n && c >= i) ? __ldcg(Ro + i * n + c) : 0.0;
+      for (int c = i; c < 8; ++c) Ro8[pk8(i, c)] = (i < n && c < n) ? __ldcg(Ro + i * n + c) : 0.0;
     if (node != p) {  // receiver (lower index) goes on top
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double tmp = R[i][c];
-          R[i][c] = Ro8[i][c];
-          Ro8[i][c] = tmp;
-        }
+      for (int i = 0; i < 36; ++i) {
+        const double tmp = R[i];
+        R[i] = Ro8[i];
+        Ro8[i] = tmp;
+      }
     }
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
-      double B[4][8];
+      double Bs[4][8];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) B[kk][c] = Ro8[4 * half + kk][c];
-      narrow_step<4>(R, B, n);
+        for (int c = 0; c < 8; ++c) {
+          const int i = 4 * half + kk;
+          Bs[kk][c] = (c >= i) ? Ro8[pk8(i, c < i ? i : c)] : 0.0;
+        }
+      narrow_step<4>(R, Bs, n);
     }
     node = p;
   }
@@ -853,7 +865,7 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
     }                                                                                           \
     break;                                                                                      \
   }
-  switch (p) { LEAF_CASE(32, 16, 32) LEAF_CASE(64, 16, 32) LEAF_CASE(128, 8, 16) }
+  switch (p) { LEAF_CASE(32, 16, 32) LEAF_CASE(64, 16, 32) LEAF_CASE(128, 16, 24) }
 #undef LEAF_CASE
 #undef CHAIN_LAUNCH
   return check_launch("k_leaf_dense/k_leaf_chain");
@@ -957,7 +969,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     return set_err(CAQR_ERR_ARG, "S / zero_init / tri_skip only apply to Q (not Q^T)");
   const int64_t base = m / P;
   cudaStream_t st = (cudaStream_t)stream;
-  const int kbs = (p == 128) ? 4 : 1;
+  const int kbs = (p == 128) ? (g_ht[2] == 24 ? 2 : 4) : 1;
   dim3 grid((unsigned)P, (unsigned)((ncols + 32 * kbs - 1) / (32 * kbs)));
 #define LA_LAUNCH(NPV, KB_, HTV)                                                                  \
   {                                                                                               \
@@ -977,7 +989,14 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
-  switch (p) { LA_CASE(32, 1, 16, 32) LA_CASE(64, 1, 16, 32) LA_CASE(128, 4, 8, 16) }
+  switch (p) {
+    LA_CASE(32, 1, 16, 32)
+    LA_CASE(64, 1, 16, 32)
+    case 128: {
+      if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24) else LA_LAUNCH(128, 4, 16)
+      break;
+    }
+  }
 #undef LA_CASE
 #undef LA_LAUNCH
   return check_launch("k_leaf_apply");
@@ -1041,7 +1060,7 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
-    const int a = i == 2 ? 8 : 16, b = i == 2 ? 16 : 32;
+    const int a = 16, b = i == 2 ? 24 : 32;
     if (value != a && value != b) return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
     return CAQR_OK;
