@@ -614,6 +614,234 @@ __device__ __forceinline__ void ring_factor_tile_vs(double (&X)[HW][NP / 32], do
 }
 
 // ---------------------------------------------------------------------------
+// Pair ring (n in (64, 128]): two warps share one 32-row chain tile and split
+// its 128 columns into global slots {0, 3} (role A) and {1, 2} (role B), which
+// balances their update work.  Reflector j is generated by the role that owns
+// column j (A: j < 32 or j >= 96, B: 32 <= j < 96) and its raw column, tau and
+// scale are broadcast to the partner through a double-buffered per-pair
+// shared slot (pub / ack sequence counters).  R rows are split the same way:
+// each role keeps its own column part of the ring (verA / verB).
+// ---------------------------------------------------------------------------
+constexpr int PAIR_HT = 32;
+constexpr int PBUF = 36;  // 32 raw values, tau, scale, pad
+
+__host__ __device__ constexpr int pr_owner(int g) { return (g == 1 || g == 2) ? 1 : 0; }
+__host__ __device__ constexpr int pr_gslot(int role, int l) {
+  return role == 0 ? (l == 0 ? 0 : 3) : (l == 0 ? 1 : 2);
+}
+__host__ __device__ constexpr int pr_lslot(int role, int g) {
+  return role == 0 ? (g == 0 ? 0 : (g == 3 ? 1 : -1)) : (g == 1 ? 0 : (g == 2 ? 1 : -1));
+}
+
+struct PairState {
+  double mysc[2];
+  double beta;  // beta of the reflector this warp generated last (written into R[j][j])
+};
+
+template <int ROLE, int G, bool LAST>
+__device__ __forceinline__ void pair_step(PairState& st, double (&X)[PAIR_HT][2], double* Rs,
+                                          int* verMine, int* pub, int* ackMine, int* ackOther,
+                                          double* buf, int n, int t, int seq0, int jj,
+                                          double* tau_tile) {
+  constexpr int HT = PAIR_HT;
+  constexpr bool OWN = (pr_owner(G) == ROLE);
+  constexpr int GN = LAST ? G + 1 : G;
+  constexpr bool OWNN = (GN < 4) && (pr_owner(GN) == ROLE);
+  constexpr int LSN = OWNN ? pr_lslot(ROLE, GN) : -1;
+  const int lane = threadIdx.x & 31;
+  const int j = 32 * G + jj;
+  const int jn = j + 1;
+  const int sq = seq0 + j;
+  const bool more = OWNN && (jn < n);
+  if (!OWN) {
+    while (ld_acquire(pub) < sq + 1) { }
+  }
+  const double* vx = buf + (sq & 1) * PBUF;
+  const double tau = vx[32], scale = vx[33];
+  const double bcur = st.beta;
+  while (ld_acquire(verMine + j) != t) { }
+  double* Rj = Rs + j * 128;
+  double qv[2] = {0.0, 0.0}, rv[2] = {0.0, 0.0};
+  // (1) the slot holding column j+1 (if this warp generates reflector j+1)
+  if constexpr (OWNN) {
+    constexpr int L = LSN;
+    constexpr int GS = pr_gslot(ROLE, L);
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      const double2 vc = *reinterpret_cast<const double2*>(vx + k + 2);
+      p0 = fma(va.x, X[k][L], p0);
+      p1 = fma(va.y, X[k + 1][L], p1);
+      p2 = fma(vc.x, X[k + 2][L], p2);
+      p3 = fma(vc.y, X[k + 3][L], p3);
+    }
+    const double r = Rj[32 * GS + lane];
+    const bool act = (GS > G) || (lane > jj);
+    const double q = act ? tau * fma(scale, (p0 + p1) + (p2 + p3), r) : 0.0;
+    const double w = q * scale;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      const double2 vc = *reinterpret_cast<const double2*>(vx + k + 2);
+      X[k][L] = fma(-va.x, w, X[k][L]);
+      X[k + 1][L] = fma(-va.y, w, X[k + 1][L]);
+      X[k + 2][L] = fma(-vc.x, w, X[k + 2][L]);
+      X[k + 3][L] = fma(-vc.y, w, X[k + 3][L]);
+      s0 = fma(X[k][L], X[k][L], s0);
+      s1 = fma(X[k + 1][L], X[k + 1][L], s1);
+      s2 = fma(X[k + 2][L], X[k + 2][L], s2);
+      s3 = fma(X[k + 3][L], X[k + 3][L], s3);
+    }
+    rv[L] = r;
+    qv[L] = q;
+    const double sg = __shfl_sync(FULL, (s0 + s1) + (s2 + s3), jn & 31);
+    double x0n = 1.0;
+    if (more) {
+      while (ld_acquire(verMine + jn) != t) { }
+      x0n = Rs[jn * 128 + jn];
+    }
+    double nbeta, ntau, nscale;
+    house_lean(x0n, sg, nbeta, ntau, nscale);
+    if (more) {
+      while (ld_acquire(ackOther) < sq) { }  // partner done with reflector j-1's slot
+      double* vn = buf + ((sq + 1) & 1) * PBUF;
+      if (lane == (jn & 31)) {
+        st.mysc[L] = nscale;
+#pragma unroll
+        for (int k = 0; k < HT; k += 2)
+          *reinterpret_cast<double2*>(vn + k) = make_double2(X[k][L], X[k + 1][L]);
+        vn[32] = ntau;
+        vn[33] = nscale;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        st_release(pub, sq + 2);
+      }
+      st.beta = nbeta;
+    }
+  }
+  // (2) the other active slots of this warp
+#pragma unroll
+  for (int L2 = 0; L2 < 2; ++L2) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    if (L2 == LSN) continue;
+    const int GS = pr_gslot(ROLE, L2);
+    if (GS < G) continue;  // finished columns
+    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      p0 = fma(va.x, X[k][L2], p0);
+      p1 = fma(va.y, X[k + 1][L2], p1);
+    }
+    const double r = Rj[32 * GS + lane];
+    const bool act = (GS > G) || (lane > jj);
+    const double q = act ? tau * fma(scale, p0 + p1, r) : 0.0;
+    const double w = q * scale;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      const double2 va = *reinterpret_cast<const double2*>(vx + k);
+      X[k][L2] = fma(-va.x, w, X[k][L2]);
+      X[k + 1][L2] = fma(-va.y, w, X[k + 1][L2]);
+    }
+    rv[L2] = r;
+    qv[L2] = q;
+  }
+  // (3) this warp's part of R row j, then hand it on and acknowledge x_j
+#pragma unroll
+  for (int L2 = 0; L2 < 2; ++L2) {
+    const int GS = pr_gslot(ROLE, L2);
+    if (GS < G) continue;
+    const int c = 32 * GS + lane;
+    if (c > j) Rj[c] = rv[L2] - qv[L2];
+  }
+  if constexpr (OWN) {
+    if (lane == jj) Rj[j] = bcur;
+    if (lane == 0 && tau_tile) tau_tile[j] = tau;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    st_release(verMine + j, t + 1);
+    st_release(ackMine, sq + 1);
+  }
+}
+
+template <int ROLE, int G>
+__device__ __forceinline__ void pair_segment(PairState& st, double (&X)[PAIR_HT][2], double* Rs,
+                                             int* verMine, int* pub, int* ackMine, int* ackOther,
+                                             double* buf, int n, int t, int seq0,
+                                             double* tau_tile) {
+  for (int jj = 0; jj < 31; ++jj) {
+    if (32 * G + jj >= n) return;
+    pair_step<ROLE, G, false>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, jj,
+                              tau_tile);
+  }
+  if (32 * G + 31 >= n) return;
+  pair_step<ROLE, G, true>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, 31,
+                           tau_tile);
+}
+
+// One chain tile for one role.  On return X holds this role's columns of V.
+template <int ROLE>
+__device__ __forceinline__ void pair_tile(double (&X)[PAIR_HT][2], double* Rs, int* verMine,
+                                          int* pub, int* ackMine, int* ackOther, double* buf,
+                                          int n, int t, int seq0, double* tau_tile) {
+  constexpr int HT = PAIR_HT;
+  const int lane = threadIdx.x & 31;
+  PairState st;
+  st.mysc[0] = 1.0;
+  st.mysc[1] = 1.0;
+  st.beta = 0.0;
+  if constexpr (ROLE == 0) {  // reflector 0 of the tile
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 2) {
+      s0 = fma(X[k][0], X[k][0], s0);
+      s1 = fma(X[k + 1][0], X[k + 1][0], s1);
+    }
+    const double sg = __shfl_sync(FULL, s0 + s1, 0);
+    while (ld_acquire(verMine) != t) { }
+    double beta, tau, scale;
+    house_lean(Rs[0], sg, beta, tau, scale);
+    while (ld_acquire(ackOther) < seq0 - 1) { }
+    double* vn = buf + (seq0 & 1) * PBUF;
+    if (lane == 0) {
+      st.mysc[0] = scale;
+#pragma unroll
+      for (int k = 0; k < HT; k += 2)
+        *reinterpret_cast<double2*>(vn + k) = make_double2(X[k][0], X[k + 1][0]);
+      vn[32] = tau;
+      vn[33] = scale;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      st_release(pub, seq0 + 1);
+    }
+    st.beta = beta;
+    pair_segment<0, 0>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    pair_segment<0, 1>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    pair_segment<0, 2>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    pair_segment<0, 3>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+  } else {
+    pair_segment<1, 0>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    pair_segment<1, 1>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    pair_segment<1, 2>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
+    __syncwarp();
+    if (lane == 0) st_release(ackMine, seq0 + 128);  // B has no columns right of 95
+  }
+#pragma unroll
+  for (int L = 0; L < 2; ++L)
+#pragma unroll
+    for (int k = 0; k < HT; ++k) X[k][L] *= st.mysc[L];
+}
+
+// ---------------------------------------------------------------------------
 // Ring tile: one warp applies the n reflectors of its triangle-on-rectangle
 // tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
 // (stride NP) under the version protocol ver[j] == t.  The broadcast vector

@@ -246,6 +246,90 @@ k_leaf_chain2(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
 }
 
 // ---------------------------------------------------------------------------
+// Pair-ring chain kernel (padded width 128, chain tile height 32): 8 warps =
+// 4 pairs; pair p runs tiles p, p+4, ...; warp 2p is role A (global column
+// slots 0 and 3), warp 2p+1 role B (slots 1 and 2).
+// ---------------------------------------------------------------------------
+struct PairSmem {
+  static constexpr size_t bytes = sizeof(double) * ((size_t)128 * 128 + 4 * 2 * PBUF) +
+                                  sizeof(int) * (2 * 128 + 4 * 4);
+};
+
+__global__ void __launch_bounds__(256, 1)
+k_leaf_chain_pair(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+                  double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
+  constexpr int HT = PAIR_HT, H0 = WARPS * Geo<128>::HD;
+  extern __shared__ __align__(16) double sm[];
+  double* Rs = sm;
+  double* bufs = Rs + 128 * 128;
+  int* verA = reinterpret_cast<int*>(bufs + 4 * 2 * PBUF);
+  int* verB = verA + 128;
+  int* sync = verB + 128;  // per pair: pub, ackA, ackB, pad
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int pair = w >> 1, role = w & 1;
+  bool bad = false;
+  const int leaf = blockIdx.x;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const int64_t rest = b - H0;
+  const int T = rest > 0 ? (int)((rest + HT - 1) / HT) : 0;
+  if (T == 0) return;
+  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
+  double* Rl = Rio + (int64_t)leaf * n * n;
+  for (int idx = threadIdx.x; idx < 128 * 128; idx += 256) {
+    const int r = idx / 128, c = idx - r * 128;
+    Rs[idx] = (r < n && c < n && c >= r) ? Rl[r * n + c] : 0.0;
+  }
+  for (int j = threadIdx.x; j < 256; j += 256) verA[j] = 0;  // verA and verB
+  if (threadIdx.x < 16) sync[threadIdx.x] = 0;  // pub = 0; ack = 0: "consumed up to seq -1"
+  __syncthreads();
+  int* pub = sync + 4 * pair;
+  int* ackA = pub + 1;
+  int* ackB = pub + 2;
+  double* buf = bufs + pair * 2 * PBUF;
+  double X[HT][2];
+  int seq0 = 0;
+  for (int t = pair; t < T; t += 4, seq0 += 128) {
+    const int64_t row = r0 + H0 + (int64_t)t * HT;
+    const int valid = (int)min64((int64_t)HT, r0 + b - row);
+    const double* src = A + row * lda;
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+#pragma unroll
+      for (int L = 0; L < 2; ++L) {
+        const int c = 32 * pr_gslot(0, L) + lane + (role ? 32 * (pr_gslot(1, L) - pr_gslot(0, L)) : 0);
+        double x = 0.0;
+        if (k < valid && c < n) x = __ldg(src + (int64_t)k * lda + c);
+        bad |= !isfinite(x);
+        X[k][L] = x;
+      }
+    }
+    double* tt = tl ? tl + (int64_t)(t + 1) * n : nullptr;
+    if (role == 0)
+      pair_tile<0>(X, Rs, verA, pub, ackA, ackB, buf, n, t, seq0, tt);
+    else
+      pair_tile<1>(X, Rs, verB, pub, ackB, ackA, buf, n, t, seq0, tt);
+    if (Y) {
+#pragma unroll
+      for (int k = 0; k < HT; ++k) {
+        if (k >= valid) continue;
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+          const int c = 32 * pr_gslot(0, L) + lane + (role ? 32 * (pr_gslot(1, L) - pr_gslot(0, L)) : 0);
+          if (c < n) Y[(row + k) * ldy + c] = X[k][L];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += 256) {
+    const int r = idx / n, c = idx - r * n;
+    Rl[idx] = (c >= r) ? Rs[r * 128 + c] : 0.0;
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
 // Lane l owns an 8x8 upper-triangular R in registers and runs the flat chain
 // of triangle-on-rectangle steps (Alg. 2) over its own rows: K rows per step,
@@ -858,9 +942,11 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
     k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
         base, Y, ldy, tau, tau_stride, R, flag);                                                \
     if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                                    \
-      if (NPV == 128 && g_dual && g_ht[np_index(NPV)] == 8) {                                    \
-        rc = launch_dual(A, lda, m, n, P, base, Y, ldy, tau, tau_stride, R, flag, st);           \
+      if (NPV == 128 && g_ht[np_index(NPV)] == 32) {                                           \
+        rc = prep(k_leaf_chain_pair, PairSmem::bytes);                                          \
         if (rc) return rc;                                                                      \
+        k_leaf_chain_pair<<<grid, 256, PairSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
+                                                              Y, ldy, tau, tau_stride, R, flag);\
       } else if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)     \
     }                                                                                           \
     break;                                                                                      \
@@ -969,7 +1055,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     return set_err(CAQR_ERR_ARG, "S / zero_init / tri_skip only apply to Q (not Q^T)");
   const int64_t base = m / P;
   cudaStream_t st = (cudaStream_t)stream;
-  const int kbs = (p == 128) ? (g_ht[2] == 24 ? 2 : 4) : 1;
+  const int kbs = (p == 128) ? (g_ht[2] >= 24 ? 2 : 4) : 1;
   dim3 grid((unsigned)P, (unsigned)((ncols + 32 * kbs - 1) / (32 * kbs)));
 #define LA_LAUNCH(NPV, KB_, HTV)                                                                  \
   {                                                                                               \
@@ -993,7 +1079,9 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     LA_CASE(32, 1, 16, 32)
     LA_CASE(64, 1, 16, 32)
     case 128: {
-      if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24) else LA_LAUNCH(128, 4, 16)
+      if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
+      else if (g_ht[2] == 32) LA_LAUNCH(128, 2, 32)
+      else LA_LAUNCH(128, 4, 16)
       break;
     }
   }
@@ -1061,7 +1149,8 @@ int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
     const int a = 16, b = i == 2 ? 24 : 32;
-    if (value != a && value != b) return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
+    if (value != a && value != b && !(i == 2 && value == 32))
+      return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
     return CAQR_OK;
   }
