@@ -1055,7 +1055,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     return set_err(CAQR_ERR_ARG, "S / zero_init / tri_skip only apply to Q (not Q^T)");
   const int64_t base = m / P;
   cudaStream_t st = (cudaStream_t)stream;
-  const int kbs = (p == 128) ? (g_ht[2] >= 24 ? 2 : 4) : 1;
+  const int kbs = (p == 128) ? (g_ht[2] >= 24 ? 2 : 4) : (p == 64 ? 2 : 1);
   dim3 grid((unsigned)P, (unsigned)((ncols + 32 * kbs - 1) / (32 * kbs)));
 #define LA_LAUNCH(NPV, KB_, HTV)                                                                  \
   {                                                                                               \
@@ -1077,7 +1077,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
   }
   switch (p) {
     LA_CASE(32, 1, 16, 32)
-    LA_CASE(64, 1, 16, 32)
+    LA_CASE(64, 2, 16, 32)
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
       else if (g_ht[2] == 32) LA_LAUNCH(128, 2, 32)
