@@ -564,6 +564,124 @@ k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, 
 }
 
 // ---------------------------------------------------------------------------
+// Warp-level tree kernels for n <= 32: one warp per combine event (or per
+// event x 32-column block for the apply); lane c owns column c of both
+// stacked blocks, so the reflector arithmetic is lane-local and only the
+// reflector vector is broadcast (shuffles).  Same STACKED semantics as
+// k_tree_factor / k_tree_apply (householder.py:263-294, 377-396).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, double* Ynode,
+                  double* taunode, int bin_level) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (e >= nev) return;
+  int a, b, id;
+  if (ev) {
+    a = ev[3 * e]; b = ev[3 * e + 1]; id = ev[3 * e + 2];
+  } else {
+    a = e << bin_level; b = a + (1 << (bin_level - 1)); id = 0;
+  }
+  __shared__ double vsm[8][32];
+  double* vs = vsm[threadIdx.x >> 5];
+  double* Ra = Rslots + (int64_t)a * n * n;
+  const double* Rb = Rslots + (int64_t)b * n * n;
+  double ca[32], cb[32];  // column `lane` of R_a and R_b
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const bool ok = (r < n && lane < n && lane >= r);
+    ca[r] = ok ? Ra[r * n + lane] : 0.0;
+    cb[r] = ok ? Rb[r * n + lane] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j >= n) break;
+    double sg = 0.0;
+#pragma unroll
+    for (int r = 0; r <= j; ++r) sg = fma(cb[r], cb[r], sg);
+    sg = __shfl_sync(FULL, sg, j);
+    const double x0 = __shfl_sync(FULL, ca[j], j);
+    double beta, tau, scale;
+    house_lean(x0, sg, beta, tau, scale);
+    __syncwarp();
+    if (lane == j) {
+#pragma unroll
+      for (int r = 0; r <= j; ++r) vs[r] = cb[r] * scale;
+    }
+    __syncwarp();
+    double d = ca[j];
+#pragma unroll
+    for (int r = 0; r <= j; ++r) d = fma(vs[r], cb[r], d);
+    const double w = (lane > j) ? tau * d : 0.0;
+    ca[j] -= w;
+#pragma unroll
+    for (int r = 0; r <= j; ++r) cb[r] = fma(-vs[r], w, cb[r]);
+    if (lane == j) {
+      ca[j] = beta;
+#pragma unroll
+      for (int r = 0; r <= j; ++r) cb[r] = vs[r];
+    }
+    if (lane == 0 && taunode) taunode[(int64_t)id * n + j] = tau;
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    if (r < n && lane < n) {
+      Ra[r * n + lane] = (lane >= r) ? ca[r] : 0.0;
+      if (Ynode) Ynode[(int64_t)id * n * n + r * n + lane] = (lane >= r) ? cb[r] : 0.0;
+    }
+  }
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256)
+k_tree_apply_w32(const double* __restrict__ Ynode, const double* __restrict__ taunode, int n,
+                 const int* __restrict__ ev, int nev, double* C, int64_t ldc, int64_t slot_rows,
+                 int64_t ncols, int zero_partner) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (e >= nev) return;
+  const int a = ev[3 * e], b = ev[3 * e + 1], id = ev[3 * e + 2];
+  const int64_t col = (int64_t)blockIdx.y * 32 + lane;
+  const bool okc = col < ncols;
+  double* Ca = C + (int64_t)a * slot_rows * ldc + col;
+  double* Cb = C + (int64_t)b * slot_rows * ldc + col;
+  const double* Yn = Ynode + (int64_t)id * n * n;
+  const double* tn = taunode + (int64_t)id * n;
+  __shared__ double vsm[8][32];
+  double* vs = vsm[threadIdx.x >> 5];
+  double ca[32], cb[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    ca[r] = (okc && r < n) ? Ca[(int64_t)r * ldc] : 0.0;
+    cb[r] = (okc && r < n && !zero_partner) ? Cb[(int64_t)r * ldc] : 0.0;
+  }
+  // lane r holds column j of Ybot for the broadcast: ycol = Ybot[lane][j]
+#pragma unroll
+  for (int jx = 0; jx < 32; ++jx) {
+    const int j = TRANS ? jx : 31 - jx;
+    if (j >= n) continue;
+    const double tj = __ldg(tn + j);
+    __syncwarp();
+    vs[lane] = (lane <= j) ? __ldg(Yn + (int64_t)lane * n + j) : 0.0;
+    __syncwarp();
+    double d = ca[j];
+#pragma unroll
+    for (int r = 0; r <= j; ++r) d = fma(vs[r], cb[r], d);
+    const double w = tj * d;
+    ca[j] -= w;
+#pragma unroll
+    for (int r = 0; r <= j; ++r) cb[r] = fma(-vs[r], w, cb[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    if (okc && r < n) {
+      Ca[(int64_t)r * ldc] = ca[r];
+      Cb[(int64_t)r * ldc] = cb[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // tree apply: [C_a; C_b] <- Q_node^(T?) [C_a; C_b] on one column block.
 // C_a = C + a*slot_rows*ldc, C_b = C + b*slot_rows*ldc (n rows each).
 // ---------------------------------------------------------------------------
@@ -986,7 +1104,12 @@ int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_
         nullptr, nullptr, nullptr, k);                                                   \
     break;                                                                               \
   }
-    switch (p) { TB_CASE(32) TB_CASE(64) TB_CASE(128) }
+    if (p == 32) {
+      k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, nullptr, (int)nev,
+                                                             nullptr, nullptr, k);
+    } else {
+      switch (p) { TB_CASE(32) TB_CASE(64) TB_CASE(128) }
+    }
 #undef TB_CASE
     rc = check_launch("k_tree_factor");
     if (rc) return rc;
@@ -1008,6 +1131,11 @@ int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events,
     k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
         events, Ynode, taunode, 0);                                                      \
     break;                                                                               \
+  }
+  if (p == 32) {
+    k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, events, (int)nev, Ynode,
+                                                           taunode, 0);
+    return check_launch("k_tree_factor_w32");
   }
   switch (p) { TREE_CASE(32) TREE_CASE(64) TREE_CASE(128) }
 #undef TREE_CASE
@@ -1038,6 +1166,16 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
           C, ldc, slot_rows, ncols, zero_partner);                                              \
     }                                                                                           \
     break;                                                                                      \
+  }
+  if (p == 32) {
+    dim3 g32((unsigned)((nev + 7) / 8), (unsigned)((ncols + 31) / 32));
+    if (transpose)
+      k_tree_apply_w32<true><<<g32, 256, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+                                                  slot_rows, ncols, zero_partner);
+    else
+      k_tree_apply_w32<false><<<g32, 256, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+                                                   slot_rows, ncols, zero_partner);
+    return check_launch("k_tree_apply_w32");
   }
   switch (p) { TA_CASE(32) TA_CASE(64) TA_CASE(128) }
 #undef TA_CASE
