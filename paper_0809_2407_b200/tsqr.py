@@ -87,10 +87,16 @@ class TsqrFactor:
     node_tau: torch.Tensor | None = None
     host: bool = False
     levels: list = field(default_factory=list)
+    flag: torch.Tensor | None = None
 
     @property
     def m(self) -> int:
         return self.layout.m
+
+    def check_finite(self) -> None:
+        """Raise ValueError if the factored matrix held NaN/Inf (core.py:26-27)."""
+        if self.flag is not None:
+            _check_flag(self.flag)
 
     @property
     def P(self) -> int:
@@ -157,8 +163,14 @@ def _count(counter, layout, n, h0, ht, P):
 
 
 def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: ReductionTree | None = None,
-                  Y_out: torch.Tensor | None = None, counter=None, host=False) -> TsqrFactor:
-    """TSQR of a CUDA float64 matrix (m x n, n <= 128) over P leaves."""
+                  Y_out: torch.Tensor | None = None, counter=None, host=False,
+                  check: bool = True) -> TsqrFactor:
+    """TSQR of a CUDA float64 matrix (m x n, n <= 128) over P leaves.
+
+    ``check=False`` skips the (host-synchronising) NaN/Inf check; the device
+    flag is returned as ``factor.flag`` for a deferred ``check_finite`` --
+    this is what makes the call capturable in a CUDA graph.
+    """
     lib = _lib.load()
     if A.ndim != 2:
         raise DimensionError("A must be 2-D")
@@ -184,10 +196,12 @@ def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: Reduction
         tickets = torch.empty(nlev * P, dtype=torch.int32, device=dev)
         _lib.check(lib.tsqr_f64_r_binary(_ptr(A), n, m, n, P, _ptr(Rs), _ptr(tickets), _ptr(flag),
                                          st), "tsqr_f64_r_binary")
-        _check_flag(flag)
+        if check:
+            _check_flag(flag)
         if counter is not None:
             _count(counter, layout, n, h0, ht, P)
-        return TsqrFactor(tree=tree, layout=layout, R=Rs[0], n=n, h0=h0, ht=ht, host=host)
+        return TsqrFactor(tree=tree, layout=layout, R=Rs[0], n=n, h0=h0, ht=ht, host=host,
+                          flag=flag)
     Y = tau = None
     if want_q:
         Y = Y_out if Y_out is not None else torch.empty_like(A)
@@ -204,11 +218,12 @@ def factor_device(A: torch.Tensor, P: int, want_q: bool = False, tree: Reduction
             _lib.check(lib.tsqr_f64_tree_factor_level(_ptr(Rs), n, _ptr(ev), ev.shape[0],
                                                       _ptr(node_Y), _ptr(node_tau), st),
                        "tsqr_f64_tree_factor_level")
-    _check_flag(flag)
+    if check:
+        _check_flag(flag)
     if counter is not None:
         _count(counter, layout, n, h0, ht, P)
     return TsqrFactor(tree=tree, layout=layout, R=Rs[tree.root], n=n, h0=h0, ht=ht, Y=Y, tau=tau,
-                      node_Y=node_Y, node_tau=node_tau, host=host, levels=levels)
+                      node_Y=node_Y, node_tau=node_tau, host=host, levels=levels, flag=flag)
 
 
 def _tree_apply(f: TsqrFactor, C: torch.Tensor, slot_rows: int, transpose: bool, zero_partner: bool):
