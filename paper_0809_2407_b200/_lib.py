@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcaqr_sm100.so")
+LIB_PATH = os.environ.get("CAQR_SM100_LIB") or os.path.join(_HERE, "lib", "libcaqr_sm100.so")
 ABI_VERSION = 1
 
 # exported symbols, in header order (tests check each one is present)

@@ -452,6 +452,145 @@ __device__ __forceinline__ void ring_slot(double (&X)[HT][NP / 32], double (&v)[
 }
 
 // ---------------------------------------------------------------------------
+// Ring step, register-broadcast form.  Same arithmetic as ring_step, but the
+// raw column x_{j+1} is broadcast by shuffles into a second vector (vn) right
+// after its rank-1 update, so its dot products and the scalars of reflector
+// j+1 overlap the rest of reflector j's update; the two vectors swap roles
+// every step (ring_slot3 unrolls by two).  Pivot rows are acquired two at a
+// time (spin on even steps only) and the R row hand-off is a plain release
+// after __syncwarp (which orders the other lanes' R stores before it).
+// ---------------------------------------------------------------------------
+template <int NP, int HT, int s, int SN, bool SPIN>
+__device__ __forceinline__ void ring_step3(double (&X)[HT][NP / 32], const double (&v)[HT],
+                                           double (&vn)[HT], double (&p)[NP / 32],
+                                           double (&mysc)[NP / 32], double& beta, double& tau,
+                                           double& scale, double* Rs, int* ver, int n, int t,
+                                           int jj, double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  const int j = 32 * s + jj;
+  const int jn = j + 1;
+  const bool more = (SN < S) && (jn < n);
+  constexpr int SNc = (SN < S) ? SN : S - 1;
+  double* Rj = Rs + j * NP;
+  double x0n = 1.0;
+  if (more) {
+    if (SPIN) {
+      const int jw = (jn + 1 < n) ? jn + 1 : jn;
+      while (ld_acquire(ver + jw) != t) { }
+    }
+    x0n = Rs[jn * NP + jn];
+  }
+  double sg = 0.0;
+  if (SN < S) {
+    const double r = Rj[32 * SNc + lane];
+    const bool act = (SNc > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[SNc], r) : 0.0;
+    const double w = q * scale;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HT; k += 4) {
+      X[k][SNc] = fma(-v[k], w, X[k][SNc]);
+      X[k + 1][SNc] = fma(-v[k + 1], w, X[k + 1][SNc]);
+      X[k + 2][SNc] = fma(-v[k + 2], w, X[k + 2][SNc]);
+      X[k + 3][SNc] = fma(-v[k + 3], w, X[k + 3][SNc]);
+      s0 = fma(X[k][SNc], X[k][SNc], s0);
+      s1 = fma(X[k + 1][SNc], X[k + 1][SNc], s1);
+      s2 = fma(X[k + 2][SNc], X[k + 2][SNc], s2);
+      s3 = fma(X[k + 3][SNc], X[k + 3][SNc], s3);
+    }
+    sg = (s0 + s1) + (s2 + s3);
+    if (32 * SNc + lane > j) Rj[32 * SNc + lane] = r - q;
+  }
+  const int src = jn & 31;
+  sg = __shfl_sync(FULL, sg, src);
+  if (more) {
+#pragma unroll
+    for (int k = 0; k < HT; ++k) vn[k] = __shfl_sync(FULL, X[k][SNc], src);
+  }
+  double nbeta, ntau, nscale;
+  house_lean(x0n, sg, nbeta, ntau, nscale);
+#pragma unroll
+  for (int s2 = s; s2 < S; ++s2) {
+    if (s2 == SN) continue;
+    if (s2 == s && SN != s) continue;
+    const double r = Rj[32 * s2 + lane];
+    const bool act = (s2 > s) || (lane > jj);
+    const double q = act ? tau * fma(scale, p[s2], r) : 0.0;
+    const double w = q * scale;
+#pragma unroll
+    for (int k = 0; k < HT; ++k) X[k][s2] = fma(-v[k], w, X[k][s2]);
+    if (32 * s2 + lane > j) Rj[32 * s2 + lane] = r - q;
+  }
+  if (lane == jj) Rj[j] = beta;
+  if (lane == 0 && tau_tile) tau_tile[j] = tau;
+  __syncwarp();
+  if (lane == 0) st_release(ver + j, t + 1);
+  if (!more) return;
+  if (lane == src) mysc[SNc] = nscale;
+  raw_dots<NP, HT, SNc>(X, vn, p);
+  beta = nbeta;
+  tau = ntau;
+  scale = nscale;
+}
+
+template <int NP, int HT, int s>
+__device__ __forceinline__ void ring_slot3(double (&X)[HT][NP / 32], double (&va)[HT],
+                                           double (&vb)[HT], double (&p)[NP / 32],
+                                           double (&mysc)[NP / 32], double& beta, double& tau,
+                                           double& scale, double* Rs, int* ver, int n, int t,
+                                           double* tau_tile) {
+  for (int jj = 0; jj < 30; jj += 2) {
+    if (32 * s + jj >= n) return;
+    ring_step3<NP, HT, s, s, true>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, jj, tau_tile);
+    if (32 * s + jj + 1 >= n) return;
+    ring_step3<NP, HT, s, s, false>(X, vb, va, p, mysc, beta, tau, scale, Rs, ver, n, t, jj + 1,
+                                    tau_tile);
+  }
+  if (32 * s + 30 >= n) return;
+  ring_step3<NP, HT, s, s, true>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, 30, tau_tile);
+  if (32 * s + 31 >= n) return;
+  ring_step3<NP, HT, s, s + 1, false>(X, vb, va, p, mysc, beta, tau, scale, Rs, ver, n, t, 31,
+                                      tau_tile);
+}
+
+template <int NP, int HW>
+__device__ __forceinline__ void ring_factor_tile3(double (&X)[HW][NP / 32], double* Rs, int* ver,
+                                                  int n, int t, double* tau_tile) {
+  constexpr int S = NP / 32;
+  const int lane = threadIdx.x & 31;
+  double mysc[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) mysc[s] = 1.0;
+  double va[HW], vb[HW];
+  double p[S];
+  double beta, tau, scale;
+  {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < HW; k += 2) {
+      s0 = fma(X[k][0], X[k][0], s0);
+      s1 = fma(X[k + 1][0], X[k + 1][0], s1);
+    }
+    const double sg = __shfl_sync(FULL, s0 + s1, 0);
+#pragma unroll
+    for (int k = 0; k < HW; ++k) va[k] = __shfl_sync(FULL, X[k][0], 0);
+    while (ld_acquire(ver) != t) { }
+    house_lean(Rs[0], sg, beta, tau, scale);
+    if (lane == 0) mysc[0] = scale;
+    raw_dots<NP, HW, 0>(X, va, p);
+  }
+  ring_slot3<NP, HW, 0>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, tau_tile);
+  if constexpr (S > 1) ring_slot3<NP, HW, 1>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, tau_tile);
+  if constexpr (S > 2) ring_slot3<NP, HW, 2>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, tau_tile);
+  if constexpr (S > 3) ring_slot3<NP, HW, 3>(X, va, vb, p, mysc, beta, tau, scale, Rs, ver, n, t, tau_tile);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int k = 0; k < HW; ++k) X[k][s] *= mysc[s];
+}
+
+// ---------------------------------------------------------------------------
 // Shared-vector variant of the ring step: the broadcast column x_j is read
 // from a double-buffered per-warp shared slot (vb + (j&1)*HT) at its point of
 // use instead of being held in registers, which frees 2*HT registers per

@@ -139,6 +139,8 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
     if constexpr (NP == 128 && HW > 16)
       ring_factor_tile_vs<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
                                   tl ? tl + (int64_t)(t + 1) * n : nullptr);
+    else if constexpr (NP == 128 && HW == 16)  // two broadcast vectors fit in 255 registers
+      ring_factor_tile3<NP, HW>(X, Rs, ver, n, t, tl ? tl + (int64_t)(t + 1) * n : nullptr);
     else
       ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
                                tl ? tl + (int64_t)(t + 1) * n : nullptr);

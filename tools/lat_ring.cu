@@ -21,7 +21,11 @@ k_chain_rw(const double* __restrict__ A, int64_t lda, int n, int64_t rows, doubl
   double X[HT][S];
   for (int t = w; t < T; t += RW) {
     load_rows<HT, S>(X, Al + (int64_t)t * HT * lda, lda, HT, n, 0, bad);
+#ifdef RING3
+    ring_factor_tile3<NP, HT>(X, Rs, ver, n, t, nullptr);
+#else
     ring_factor_tile<NP, HT>(X, Rs, ver, vbuf + w * HT, n, t, nullptr);
+#endif
   }
   __syncthreads();
   if (threadIdx.x == 0) Rio[blockIdx.x] = Rs[NP * NP - 1] + (bad ? 1.0 : 0.0);
