@@ -1371,6 +1371,9 @@ __device__ __forceinline__ void ring_apply_tile(double (&X)[HW][KBS], double* Cs
       __syncwarp();
     }
     const int jlim = min(32, n - 32 * jb);
+    // one reflector at a time; the pivot rows are acquired two at a time
+    // (a spin on even steps only), a zero tau simply gives w = 0, and the
+    // hand-off is __syncwarp (orders the lanes' Cs stores) + lane 0 release.
     for (int jx = 0; jx < jlim; ++jx) {
       const int jj = TRANS ? jx : jlim - 1 - jx;
       const int j = 32 * jb + jj;
@@ -1382,31 +1385,29 @@ __device__ __forceinline__ void ring_apply_tile(double (&X)[HW][KBS], double* Cs
         v[k] = t2.x;
         v[k + 1] = t2.y;
       }
-      while (ld_acquire(ver + j) != order) { }
-      if (tj != 0.0) {
+      if ((jx & 1) == 0) {
+        const int jw = (jx + 1 < jlim) ? (TRANS ? j + 1 : j - 1) : j;
+        while (ld_acquire(ver + jw) != order) { }
+      }
 #pragma unroll
-        for (int s2 = 0; s2 < KBS; ++s2) {
-          if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
-          const double cold = Cs[j * KB + 32 * s2 + lane];
-          double p0 = cold, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      for (int s2 = 0; s2 < KBS; ++s2) {
+        if (tri_skip && col0 + 32 * s2 + 31 < j) continue;
+        const double cold = Cs[j * KB + 32 * s2 + lane];
+        double p0 = cold, p1 = 0.0, p2 = 0.0, p3 = 0.0;
 #pragma unroll
-          for (int k = 0; k < HW; k += 4) {
-            p0 = fma(v[k], X[k][s2], p0);
-            p1 = fma(v[k + 1], X[k + 1][s2], p1);
-            p2 = fma(v[k + 2], X[k + 2][s2], p2);
-            p3 = fma(v[k + 3], X[k + 3][s2], p3);
-          }
-          const double wv = tj * ((p0 + p1) + (p2 + p3));
-          Cs[j * KB + 32 * s2 + lane] = cold - wv;
-#pragma unroll
-          for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+        for (int k = 0; k < HW; k += 4) {
+          p0 = fma(v[k], X[k][s2], p0);
+          p1 = fma(v[k + 1], X[k + 1][s2], p1);
+          p2 = fma(v[k + 2], X[k + 2][s2], p2);
+          p3 = fma(v[k + 3], X[k + 3][s2], p3);
         }
+        const double wv = tj * ((p0 + p1) + (p2 + p3));
+        Cs[j * KB + 32 * s2 + lane] = cold - wv;
+#pragma unroll
+        for (int k = 0; k < HW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
       }
       __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        st_release(ver + j, order + 1);
-      }
+      if (lane == 0) st_release(ver + j, order + 1);
     }
   }
 }
