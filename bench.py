@@ -441,7 +441,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--graph", type=int, default=1,
                     help="replay each TSQR step as one captured CUDA graph (1 GPU, not CAQR)")
-    ap.add_argument("--panel-chains", type=int, default=1,
+    ap.add_argument("--panel-chains", type=int, default=2,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

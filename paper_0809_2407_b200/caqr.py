@@ -75,15 +75,18 @@ def _panel_leaves(mj: int, w: int, leaf_rows: int) -> int:
 
 
 def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_rows: int = 2048,
-                device=None, counter=None, lookahead: bool = False,
-                panel_chains: int = 1) -> CaqrResult:
+                device=None, counter=None, lookahead: bool = True,
+                panel_chains: int = 2) -> CaqrResult:
     """CAQR of A (m x n, m >= n) with panel width b <= 128.
 
-    With ``lookahead`` the panels run on a high-priority stream:
+    With ``lookahead`` (default) the panels run on a high-priority stream:
     panel j+1's columns are updated by Q_j and factored there while the
     low-priority stream applies Q_j to the rest of the trailing matrix
     (depth-1 lookahead; the data dependencies are the same as the
-    sequential right-looking order, so results are identical).
+    sequential right-looking order, so results are identical).  The panel
+    factor then only needs a few SMs' worth of work to hide behind the
+    trailing update; ``panel_chains`` splits each panel leaf into that many
+    ring chains (a deeper binary tree, see tsqr.split_leaves).
     """
     lib = _lib.load()
     if layout is not None:

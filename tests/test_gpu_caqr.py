@@ -62,3 +62,15 @@ def test_caqr_device_tensor_stays_on_device():
     assert res.R.is_cuda
     Rref = torch.linalg.qr(A.cpu(), mode="r")[1].numpy()
     assert oracle.r_diff(res.R.cpu().numpy(), Rref) <= 1000 * EPS
+
+
+def test_caqr_lookahead_matches_sequential_order():
+    """The two-stream lookahead schedule keeps the right-looking data flow:
+    R must agree with the single-stream order to rounding."""
+    from paper_0809_2407_b200.caqr import caqr_factor
+
+    A = torch.from_numpy(philox(21).standard_normal((3000, 1000))).cuda()
+    R1 = caqr_factor(A, b=128, leaf_rows=512, lookahead=False, panel_chains=1).R
+    R2 = caqr_factor(A, b=128, leaf_rows=512, lookahead=True, panel_chains=2).R
+    scale = float(torch.linalg.matrix_norm(A, 2))
+    assert oracle.r_diff(R1.cpu().numpy(), R2.cpu().numpy(), scale) <= 100 * EPS
