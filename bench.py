@@ -217,6 +217,49 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 # our path
 # ---------------------------------------------------------------------------
+def caqr_roofline(A, cfg, args):
+    """Roofline of CAQR's dominant kernel, the leaf-level trailing update
+    (k_leaf_apply, Q_0^T applied to the n - b trailing columns of panel 0):
+    4 m b (n - b) algorithmic flops per launch over its event-timed duration.
+    Also returns the number of library kernels one caqr_factor launches."""
+    from paper_0809_2407_b200.caqr import _panel_leaves, caqr_factor
+    import torch
+
+    from paper_0809_2407_b200.tsqr import _leaf_apply, factor_device
+
+    m, n = A.shape
+    b = 128
+    full = caqr_factor(A, b=b, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+    launches = full.launches
+    del full
+    P = _panel_leaves(m, b, cfg["leaf"])
+    f = factor_device(A[:, :b].contiguous(), P, want_q=True)
+    C = A[:, b:].contiguous()
+    for _ in range(2):
+        _leaf_apply(f, C, transpose=True)
+    ts = []
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _leaf_apply(f, C, transpose=True)
+        e1.record(st)
+        ts.append((e0, e1))
+    torch.cuda.synchronize()
+    t = float(np.mean([a.elapsed_time(c) for a, c in ts])) * 1e-3
+    F = 4.0 * m * b * (n - b)
+    ach = F / t / 1e12
+    del C, f
+    torch.cuda.empty_cache()
+    return ({"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+             "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+             "kernel": "k_leaf_apply (trailing update of panel 0: Q_0^T on m x (n-b))",
+             "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
+                            "entry in MEASURED_PEAKS.json)",
+             "algorithmic_flops_per_launch": F, "launch_ms": t * 1e3}, launches)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -335,6 +378,9 @@ def run_ours(args, cfg):
     # roofline of the dominant kernel: the leaf factorization (factor_device's
     # leaf + tree events bracket; the tree is < 2% of it, see profiles/)
     roof = None
+    caqr_launches = None
+    if is_caqr:
+        roof, caqr_launches = caqr_roofline(A, cfg, args)
     if leaf_ev:
         t_leaf = float(np.mean([a.elapsed_time(b) for a, b in leaf_ev])) * 1e-3
         F_leaf = flops(hi - lo, n)
@@ -408,7 +454,7 @@ def run_ours(args, cfg):
     if cfg["q"] == "explicit":
         launches += (levels + 1) * args.steps
     if is_caqr:
-        launches = None
+        launches = caqr_launches * args.steps
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,

@@ -61,6 +61,7 @@ class CaqrResult:
     b: int
     host: bool = False
     recorders: list = field(default_factory=list)
+    launches: int = 0            # kernels of this library launched by the factorization
 
     @property
     def R(self):
@@ -105,6 +106,7 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     starts = list(range(0, n, b))
     nb = len(starts)
     panels = [None] * nb
+    nlaunch = [0]
 
     def factor(jp, st):
         c0 = starts[jp]
@@ -125,6 +127,7 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
                    "tsqr_f64_leaf_factor")
         tree = ReductionTree(P=P, shape=BINARY)
         levels = _levels_on(tree, dev)
+        nlaunch[0] += 1 + (mj - lay.base * (P - 1) > h0) + (len(levels) if P > 1 else 0)
         node_Y = node_tau = None
         if P > 1:
             node_Y = torch.zeros((P - 1, w, w), dtype=torch.float64, device=dev)
@@ -148,6 +151,7 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         base_ptr = _ptr(W) + 8 * (c0 * n + c0)
         cptr = _ptr(W) + 8 * (c0 * n + lo)
         sh = int(st.cuda_stream)
+        nlaunch[0] += 1 + len(pnl.levels)
         _lib.check(lib.tsqr_f64_leaf_apply(base_ptr, n, _ptr(pnl.tau), pnl.tau.shape[1] * w, mj, w,
                                            P, cptr, n, hi - lo, 0, 0, 0, 1, 0, 0, sh),
                    "tsqr_f64_leaf_apply")
@@ -200,7 +204,7 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     _check_flag(flag)
     if counter is not None:
         counter.add(2 * m * n * n - (2 * n ** 3) // 3)
-    return CaqrResult(W=W, panels=panels, m=m, n=n, b=b, host=host)
+    return CaqrResult(W=W, panels=panels, m=m, n=n, b=b, host=host, launches=nlaunch[0])
 
 
 def gather_R(result: CaqrResult):
