@@ -8,6 +8,13 @@ size): at level k rank f + 2^(k-1) sends its packed R
 stacked-triangle combine kernel.  Reduce mode leaves R on rank 0;
 all-reduce mode broadcasts it back so every rank holds the bitwise-identical R.
 
+Q across ranks: with Q = diag(Q_r) Q_cross,
+Q C applies the cross tree top-down to each rank's top n rows and then the
+local Q; Q^T C applies the local Q^T and then the cross tree bottom-up
+(``cross_apply``).  Each tree event moves one n x k block to the receiver
+and back; forming Q explicitly skips the upward message (the partner's
+block is still zero on the way down).
+
 Transport: ``torch.distributed`` point-to-point (NCCL over NVLink on GPUs,
 gloo on CPU for the host-logic tests).  ``combine`` and ``local`` are
 injectable so the host logic is testable without a GPU.
@@ -79,6 +86,100 @@ def cross_tree(R_local: torch.Tensor, combine, group=None, all_reduce: bool = Fa
     return (R if is_root else None), nodes
 
 
+def cross_apply(nodes, C_top: torch.Tensor, apply_node, transpose: bool = False, group=None,
+                zero_partner: bool = False, recorder=None) -> torch.Tensor:
+    """Apply Q_cross (top-down) or Q_cross^T (bottom-up) of the cross-rank tree
+    to this rank's top block C_top (n x k); ``nodes`` is this rank's list from
+    ``cross_tree``.  ``apply_node(node, Ca, Cb, transpose) -> (Ca, Cb)`` runs
+    on the receiver of each event (apply_stacked semantics, householder.py:377-396).
+    ``zero_partner`` (top-down only): the partner's block is zero on arrival,
+    so it is not sent (explicit-Q formation)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    tree = ReductionTree(P=world)
+    levels = list(enumerate(tree.levels, start=1))
+    if not transpose:
+        levels = levels[::-1]
+    skip_up = zero_partner and not transpose
+    node_of = {(lvl, partner): node for (lvl, partner, node) in nodes}
+    C = C_top.contiguous()
+    words = C.numel()
+    for lvl, grp in levels:
+        for (a, b) in grp:
+            if rank == b:
+                if not skip_up:
+                    dist.send(C, dst=a, group=group)
+                    if recorder is not None:
+                        recorder.record_send(words)
+                buf = torch.empty_like(C)
+                dist.recv(buf, src=a, group=group)
+                if recorder is not None:
+                    recorder.record_recv(words, stage=(lvl, "Q"))
+                C = buf
+            elif rank == a:
+                if skip_up:
+                    Cb = torch.zeros_like(C)
+                else:
+                    Cb = torch.empty_like(C)
+                    dist.recv(Cb, src=b, group=group)
+                    if recorder is not None:
+                        recorder.record_recv(words, stage=(lvl, "Q"))
+                C, Cb = apply_node(node_of[(lvl, b)], C, Cb, transpose)
+                C = C.contiguous()
+                dist.send(Cb.contiguous(), dst=b, group=group)
+                if recorder is not None:
+                    recorder.record_send(words)
+    return C
+
+
+def sharded_apply_q(local_factor, nodes, C_shard: torch.Tensor, n: int, local_apply, apply_node,
+                    transpose: bool = False, group=None, recorder=None) -> torch.Tensor:
+    """Q C or Q^T C for the row-sharded TSQR (C_shard = this rank's rows of C).
+    ``local_apply(local_factor, C, transpose)`` applies the rank's local Q
+    (C with m_loc rows: full Q; C with n rows and transpose False: thin Q)."""
+    if transpose:
+        C = local_apply(local_factor, C_shard, True)
+        C = C.clone()
+        C[:n] = cross_apply(nodes, C[:n].clone(), apply_node, True, group, recorder=recorder)
+        return C
+    C = C_shard.clone()
+    C[:n] = cross_apply(nodes, C[:n].clone(), apply_node, False, group, recorder=recorder)
+    return local_apply(local_factor, C, False)
+
+
+def sharded_explicit_q(local_factor, nodes, n: int, local_apply, apply_node,
+                       group=None, device=None, recorder=None) -> torch.Tensor:
+    """This rank's rows of the thin Q (Q [I; 0])."""
+    rank = dist.get_rank(group)
+    root = ReductionTree(P=dist.get_world_size(group)).root
+    S = torch.eye(n, dtype=torch.float64, device=device) if rank == root else \
+        torch.zeros((n, n), dtype=torch.float64, device=device)
+    S = cross_apply(nodes, S, apply_node, False, group, zero_partner=True, recorder=recorder)
+    return local_apply(local_factor, S, False)  # thin: Q_local [S; 0]
+
+
+def gpu_apply_node(node, Ca: torch.Tensor, Cb: torch.Tensor, transpose: bool):
+    """Q or Q^T of one stacked-triangle node on [Ca; Cb] (tsqr_f64_tree_apply_level)."""
+    from . import _lib
+    from .tsqr import _ptr, _stream
+
+    lib = _lib.load()
+    Yn, tn = node
+    n, k = Ca.shape
+    C = torch.cat([Ca, Cb]).contiguous()
+    ev = torch.tensor([[0, 1, 0]], dtype=torch.int32, device=C.device)
+    _lib.check(lib.tsqr_f64_tree_apply_level(_ptr(Yn), _ptr(tn), n, _ptr(ev), 1, _ptr(C), k, n, k,
+                                             int(bool(transpose)), 0, _stream(C.device)),
+               "tsqr_f64_tree_apply_level")
+    return C[:n], C[n:]
+
+
+def gpu_local_apply(f, C: torch.Tensor, transpose: bool) -> torch.Tensor:
+    from .tsqr import apply_q_device
+
+    return apply_q_device(f, C, transpose)
+
+
 def gpu_combine(Ra: torch.Tensor, Rb: torch.Tensor):
     """Stacked-triangle combine on the GPU (tsqr_f64_tree_factor_level, one event)."""
     from . import _lib
@@ -105,3 +206,14 @@ def tsqr_sharded(A_shard: torch.Tensor, leaf_rows: int = 8192, want_q: bool = Fa
     f = factor_device(A_shard, P, want_q=want_q)
     R, nodes = cross_tree(f.R, gpu_combine, group=group, all_reduce=all_reduce)
     return R, f, nodes
+
+
+def tsqr_sharded_apply_q(f, nodes, C_shard: torch.Tensor, transpose: bool = False, group=None):
+    """Q C / Q^T C on the GPU for a ``tsqr_sharded(..., want_q=True)`` factorization."""
+    return sharded_apply_q(f, nodes, C_shard, f.n, gpu_local_apply, gpu_apply_node, transpose, group)
+
+
+def tsqr_sharded_explicit_q(f, nodes, group=None) -> torch.Tensor:
+    """This rank's rows of the thin Q of a ``tsqr_sharded(..., want_q=True)`` factorization."""
+    return sharded_explicit_q(f, nodes, f.n, gpu_local_apply, gpu_apply_node, group,
+                              device=f.R.device)

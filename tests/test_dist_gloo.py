@@ -70,3 +70,91 @@ def test_cross_tree_gloo(world, all_reduce):
     lv = int(np.log2(world))
     assert out[0][2] == lv and out[0][3] == lv * n * (n + 1) // 2
     assert sum(out[r][4] for r in range(world)) == world - 1
+
+
+def _local_apply(f, C, transpose):
+    """Full (or thin) local Q of an oracle.tsqr_reference factor (test helper)."""
+    import oracle
+
+    C = C.numpy().copy()
+    n, offs = f["n"], f["offs"]
+    if transpose:
+        for i, (Y, tau) in enumerate(f["leaves"]):
+            C[offs[i]:offs[i + 1]] = oracle.apply_dense(Y, tau, C[offs[i]:offs[i + 1]], transpose=True)
+        for (lvl, a, b, Yb, tau) in f["nodes"]:
+            ta, tb = oracle.apply_stacked(Yb, tau, C[offs[a]:offs[a] + n], C[offs[b]:offs[b] + n],
+                                          transpose=True)
+            C[offs[a]:offs[a] + n], C[offs[b]:offs[b] + n] = ta, tb
+        return torch.from_numpy(C)
+    if C.shape[0] == n and offs[-1] != n:
+        full = np.zeros((offs[-1], C.shape[1]))
+        full[:n] = C
+        C = full
+    for (lvl, a, b, Yb, tau) in reversed(f["nodes"]):
+        ta, tb = oracle.apply_stacked(Yb, tau, C[offs[a]:offs[a] + n], C[offs[b]:offs[b] + n])
+        C[offs[a]:offs[a] + n], C[offs[b]:offs[b] + n] = ta, tb
+    for i, (Y, tau) in enumerate(f["leaves"]):
+        C[offs[i]:offs[i + 1]] = oracle.apply_dense(Y, tau, C[offs[i]:offs[i + 1]])
+    return torch.from_numpy(C)
+
+
+def _q_worker(rank, world, port, A, leaf_rows, Cfull, out):
+    import oracle
+    from paper_0809_2407_b200.counters import CommRecorder
+    from paper_0809_2407_b200.dist import (cross_tree, shard_rows, sharded_apply_q,
+                                           sharded_explicit_q)
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, n = A.shape
+        lo, hi = shard_rows(m, world, rank)
+        P = max(1, (hi - lo) // leaf_rows)
+        f = oracle.tsqr_reference(A[lo:hi], P)
+
+        def combine(Ra, Rb):
+            Yb, tau, R = oracle.stacked_qr(Ra.numpy(), Rb.numpy())
+            return torch.from_numpy(R), (Yb, tau)
+
+        def apply_node(node, Ca, Cb, transpose):
+            ta, tb = oracle.apply_stacked(node[0], node[1], Ca.numpy(), Cb.numpy(), transpose)
+            return torch.from_numpy(ta), torch.from_numpy(tb)
+
+        _, nodes = cross_tree(torch.from_numpy(f["R"]), combine)
+        rec = CommRecorder()
+        Q = sharded_explicit_q(f, nodes, n, _local_apply, apply_node, recorder=rec)
+        C = torch.from_numpy(Cfull[lo:hi].copy())
+        QtC = sharded_apply_q(f, nodes, C, n, _local_apply, apply_node, transpose=True)
+        back = sharded_apply_q(f, nodes, QtC, n, _local_apply, apply_node, transpose=False)
+        out[rank] = (Q.numpy(), QtC.numpy(), back.numpy(), rec.messages_received)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_cross_tree_q_gloo(world):
+    """Q across ranks: explicit Q and Q^T C / Q (Q^T C) against the single-process
+    oracle over the same binary tree (power-of-two leaves per rank)."""
+    import oracle
+
+    rng = np.random.Generator(np.random.Philox(10 + world))
+    m, n, leaf = 2048, 12, 128
+    A = rng.standard_normal((m, n))
+    Cfull = rng.standard_normal((m, 3))
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_q_worker, args=(world, _free_port(), A, leaf, Cfull, out), nprocs=world, join=True)
+    Q = np.vstack([out[r][0] for r in range(world)])
+    QtC = np.vstack([out[r][1] for r in range(world)])
+    back = np.vstack([out[r][2] for r in range(world)])
+    fref = oracle.tsqr_reference(A, m // leaf)
+    Qref = oracle.tsqr_reference_q(fref)
+    eps = oracle.EPS
+    assert np.max(np.abs(Q - Qref)) <= 100 * eps
+    assert oracle.orthogonality(Q) <= 10 * n * eps
+    # Q^T C: its first n rows are Q_thin^T C; the rest is the complement
+    assert np.max(np.abs(QtC[:n] - Qref.T @ Cfull)) <= 100 * n * eps * np.linalg.norm(Cfull, 2)
+    assert np.linalg.norm(back - Cfull) <= 10 * n * eps * np.linalg.norm(Cfull)
+    # down the tree: every non-root rank receives exactly one n x n block
+    assert out[0][3] == 0 and all(out[r][3] == 1 for r in range(1, world))
