@@ -77,6 +77,20 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
 int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
                       int* tickets, int* flag, void* stream);
 
+/* tsqr_f64_r_binary over leaves of `base` rows, the last taking the remainder
+ * (m - (P-1) base >= base): one chunk of a larger BlockRowLayout whose base is
+ * not m / P of the chunk (streamed / out-of-core TSQR; the
+ * chunk's leaves must form whole subtrees of the global binary tree). */
+int tsqr_f64_r_binary_rows(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                           int64_t base, double* Rslots, int* tickets, int* flag, void* stream);
+
+/* One R-only combine level (events as in tsqr_f64_tree_factor_level, no node
+ * factors kept) with the same arithmetic as tsqr_f64_r_binary's own tree
+ * (qr_stacked_triangles, householder.py:263-294; for n <= 8 the narrow
+ * path's half-step combine), so a tree split across calls gives the same R. */
+int tsqr_f64_r_combine_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,
+                             void* stream);
+
 /* One level of the binary reduce tree: for every event e (int32 triples
  * {receiver, partner, node} in `events`, device memory), QR of
  * [R[receiver]; R[partner]] -> R[receiver]; node factor -> Ynode[node] (n x n

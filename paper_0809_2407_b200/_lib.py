@@ -21,6 +21,8 @@ SYMBOLS = (
     "tsqr_f64_geometry",
     "tsqr_f64_leaf_factor",
     "tsqr_f64_r_binary",
+    "tsqr_f64_r_binary_rows",
+    "tsqr_f64_r_combine_level",
     "tsqr_f64_tree_factor_level",
     "tsqr_f64_tree_apply_level",
     "tsqr_f64_leaf_apply",
@@ -54,6 +56,10 @@ def _sig(lib):
     lib.tsqr_f64_leaf_factor.argtypes = [dp, i64, i64, i64, i64, dp, i64, dp, i64, dp, ip, vp]
     lib.tsqr_f64_r_binary.restype = i32
     lib.tsqr_f64_r_binary.argtypes = [dp, i64, i64, i64, i64, dp, ip, ip, vp]
+    lib.tsqr_f64_r_binary_rows.restype = i32
+    lib.tsqr_f64_r_binary_rows.argtypes = [dp, i64, i64, i64, i64, i64, dp, ip, ip, vp]
+    lib.tsqr_f64_r_combine_level.restype = i32
+    lib.tsqr_f64_r_combine_level.argtypes = [dp, i64, ip, i64, vp]
     lib.tsqr_f64_tree_factor_level.restype = i32
     lib.tsqr_f64_tree_factor_level.argtypes = [dp, i64, ip, i64, dp, dp, vp]
     lib.tsqr_f64_tree_apply_level.restype = i32

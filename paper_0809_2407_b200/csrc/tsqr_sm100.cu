@@ -498,6 +498,42 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
   put(node);  // the root (node 0)
 }
 
+// One level of the narrow fused tree as its own launch (streamed TSQR's upper
+// levels): event e combines slot a (on top) with slot b exactly as
+// k_leaf_narrow's ticket tree does, one thread per event.
+__global__ void __launch_bounds__(128)
+k_narrow_combine(double* Rslots, int n, const int* __restrict__ ev, int nev) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nev) return;
+  double* Ra = Rslots + (int64_t)ev[3 * e] * n * n;
+  const double* Rb = Rslots + (int64_t)ev[3 * e + 1] * n * n;
+  double R[36], Ro8[36];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = i; c < 8; ++c) {
+      R[pk8(i, c)] = (i < n && c < n) ? Ra[i * n + c] : 0.0;
+      Ro8[pk8(i, c)] = (i < n && c < n) ? Rb[i * n + c] : 0.0;
+    }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    double Bs[4][8];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int i = 4 * half + kk;
+        Bs[kk][c] = (c >= i) ? Ro8[pk8(i, c < i ? i : c)] : 0.0;
+      }
+    narrow_step<4>(R, Bs, n);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (i < n && c < n) Ra[i * n + c] = (c >= i) ? R[pk8(i, c < i ? i : c)] : 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // tree combine: [R_a; R_b] -> R_a' with STACKED factor (Ybot, tau)
 // events: int32 triples (receiver slot, partner slot, node id)
@@ -1031,15 +1067,16 @@ static int launch_dual(const double* A, int64_t lda, int64_t m, int64_t n, int64
   return CAQR_OK;
 }
 
-int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Y,
-                         int64_t ldy, double* tau, int64_t tau_stride, double* R, int* flag,
-                         void* stream) {
+// Leaves of `base` rows, the last one taking the remainder (m - (P-1) base >= base).
+static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                            int64_t base, double* Y, int64_t ldy, double* tau, int64_t tau_stride,
+                            double* R, int* flag, void* stream) {
   const int p = padded(n);
   if (!p || !A || !R || P < 1 || m < n * P || lda < n || (Y && ldy < n))
     return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor: bad arguments");
   if ((Y == nullptr) != (tau == nullptr)) return set_err(CAQR_ERR_ARG, "Y and tau go together");
-  const int64_t base = m / P;
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
+  if (m - (P - 1) * base < base) return set_err(CAQR_ERR_ARG, "last leaf shorter than base");
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)P;
   if (n <= 8 && !Y && g_narrow) {
@@ -1077,13 +1114,20 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
   return check_launch("k_leaf_dense/k_leaf_chain");
 }
 
-int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
-                      int* tickets, int* flag, void* stream) {
+int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Y,
+                         int64_t ldy, double* tau, int64_t tau_stride, double* R, int* flag,
+                         void* stream) {
+  if (P < 1) return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor: bad arguments");
+  return leaf_factor_impl(A, lda, m, n, P, m / P, Y, ldy, tau, tau_stride, R, flag, stream);
+}
+
+static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                         int64_t base, double* Rslots, int* tickets, int* flag, void* stream) {
   const int p = padded(n);
   if (!p || !A || !Rslots || P < 1 || m < n * P || lda < n || (!tickets && n <= 8 && P > 1))
     return set_err(CAQR_ERR_ARG, "tsqr_f64_r_binary: bad arguments");
-  const int64_t base = m / P;
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
+  if (m - (P - 1) * base < base) return set_err(CAQR_ERR_ARG, "last leaf shorter than base");
   cudaStream_t st = (cudaStream_t)stream;
   int levels = 0;
   while ((1LL << levels) < P) ++levels;
@@ -1094,7 +1138,7 @@ int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_
         A, lda, m, (int)n, (int)P, base, Rslots, flag, P > 1 ? tickets : nullptr);
     return check_launch("k_leaf_narrow");
   }
-  int rc = tsqr_f64_leaf_factor(A, lda, m, n, P, nullptr, 0, nullptr, 0, Rslots, flag, stream);
+  int rc = leaf_factor_impl(A, lda, m, n, P, base, nullptr, 0, nullptr, 0, Rslots, flag, stream);
   if (rc) return rc;
   for (int k = 1; k <= levels; ++k) {
     const int64_t nev = (P - 1 - (1LL << (k - 1))) / (1LL << k) + 1;  // f + 2^(k-1) < P, f = e 2^k
@@ -1117,6 +1161,46 @@ int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_
     if (rc) return rc;
   }
   return CAQR_OK;
+}
+
+int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
+                      int* tickets, int* flag, void* stream) {
+  if (P < 1) return set_err(CAQR_ERR_ARG, "tsqr_f64_r_binary: bad arguments");
+  return r_binary_impl(A, lda, m, n, P, m / P, Rslots, tickets, flag, stream);
+}
+
+int tsqr_f64_r_binary_rows(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                           int64_t base, double* Rslots, int* tickets, int* flag, void* stream) {
+  return r_binary_impl(A, lda, m, n, P, base, Rslots, tickets, flag, stream);
+}
+
+int tsqr_f64_r_combine_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,
+                             void* stream) {
+  const int p = padded(n);
+  if (!p || !Rslots || !events || nev < 0)
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_r_combine_level: bad arguments");
+  if (nev == 0) return CAQR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 8 && g_narrow) {
+    k_narrow_combine<<<(int)((nev + 127) / 128), 128, 0, st>>>(Rslots, (int)n, events, (int)nev);
+    return check_launch("k_narrow_combine");
+  }
+  if (p == 32) {
+    k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, events, (int)nev,
+                                                           nullptr, nullptr, 0);
+    return check_launch("k_tree_factor_w32");
+  }
+#define RC_CASE(NPV)                                                                     \
+  case NPV: {                                                                            \
+    int rc = prep(k_tree_factor<NPV>, TreeSmem<NPV>::bytes);                             \
+    if (rc) return rc;                                                                   \
+    k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
+        events, nullptr, nullptr, 0);                                                    \
+    break;                                                                               \
+  }
+  switch (p) { RC_CASE(64) RC_CASE(128) }
+#undef RC_CASE
+  return check_launch("k_tree_factor");
 }
 
 int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events, int64_t nev,

@@ -327,17 +327,44 @@ def split_leaves(m: int, n: int, P: int, min_chains: int | None = None,
 
 
 def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None = None,
-         device=None, counter=None, split: bool = True):
+         device=None, counter=None, split: bool = True, stream: bool = True):
     """Convenience TSQR: returns R, (R, factor) or (R, Q).
 
     q = "none" (R only), "implicit" (R + TsqrFactor) or "explicit" (R + thin Q).
     Leaves follow BlockRowLayout(m, n, floor(m / leaf_rows)); with ``split``
     (default, binary tree only) each leaf runs as 2^k GPU chains when there
     are fewer leaves than SMs (``split_leaves``).  R follows the reference's
-    sign convention (beta = -sign(x0)||x||: mixed-sign diagonal).
+    sign convention (beta = -sign(x0)||x||: mixed-sign diagonal).  A host
+    matrix with q = "none" on the binary tree is streamed through the GPU in
+    row chunks with the copies overlapped (``stream.tsqr_stream``; same
+    leaves and tree, bitwise-identical R); ``stream=False`` copies it whole.
     """
     if q not in ("none", "implicit", "explicit"):
         raise ValueError(f"q must be none / implicit / explicit, got {q!r}")
+    host_in = isinstance(A, np.ndarray) or (isinstance(A, torch.Tensor) and not A.is_cuda)
+    if stream and host_in and q == "none" and (tree is None or tree.shape == BINARY):
+        from .stream import tsqr_stream
+
+        Ah = A if isinstance(A, torch.Tensor) else np.asarray(A, dtype=np.float64)
+        if Ah.ndim != 2:
+            raise DimensionError(f"matrix must be 2-D, got ndim={Ah.ndim}")
+        m, n = Ah.shape
+        if m < n:
+            raise DimensionError(f"need m >= n, got {m} x {n}")
+        if n < 1 or n > MAX_N:
+            raise DimensionError(f"GPU TSQR supports 1 <= n <= {MAX_N}, got n = {n}")
+        if tree is not None:
+            P = tree.P
+        else:
+            P = _leaves_for(m, n, leaf_rows)
+            if split:
+                P *= split_leaves(m, n, P)
+        BlockRowLayout(m, n, P)  # raises DimensionError for short leaves
+        R = tsqr_stream(Ah, P, device=device)
+        if counter is not None:
+            _, h0, ht = _lib.geometry(n)
+            _count(counter, BlockRowLayout(m, n, P), n, h0, ht, P)
+        return _out(R, True)
     At, host = to_device(A, device)
     m, n = At.shape
     if m < n:

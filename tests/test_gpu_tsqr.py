@@ -242,3 +242,33 @@ def test_narrow_rejects_nonfinite():
     A[12345, 7] = np.inf
     with pytest.raises(ValueError):
         tsqr(A, leaf_rows=4096)
+
+
+@pytest.mark.parametrize("m,n,leaf,K", [(100037, 128, 4096, 4), (65536 + 999, 64, 2048, 2),
+                                        (1 << 20, 8, 16384, 8), (50000, 32, 1000, 16)])
+def test_streamed_r_is_bitwise_the_device_r(m, n, leaf, K):
+    """Host-resident A streamed in chunks of K leaves (paper_0809_2407_b200.stream)
+    gives the device-resident path's R bit for bit (same leaves, same tree)."""
+    from paper_0809_2407_b200.stream import tsqr_stream
+    from paper_0809_2407_b200.tsqr import _leaves_for, factor_device, split_leaves, tsqr
+
+    A = philox(m + n).standard_normal((m, n))
+    P = _leaves_for(m, n, leaf)
+    P *= split_leaves(m, n, P)
+    Rdev = factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy()
+    Rs = tsqr_stream(A, P, chunk_leaves=K).cpu().numpy()  # pageable: staged
+    assert np.array_equal(Rs, Rdev)
+    Ap = torch.from_numpy(A).pin_memory()
+    assert np.array_equal(tsqr_stream(Ap, P, chunk_leaves=K, buffers=2).cpu().numpy(), Rdev)
+    # the public entry point streams host input by default
+    assert np.array_equal(tsqr(A, leaf_rows=leaf), Rdev)
+    assert oracle.r_diff(Rdev, np.linalg.qr(A, mode="r")) <= 1000 * EPS
+
+
+def test_streamed_rejects_nonfinite():
+    from paper_0809_2407_b200.tsqr import tsqr
+
+    A = philox(5).standard_normal((40000, 16))
+    A[33333, 3] = np.inf
+    with pytest.raises(ValueError):
+        tsqr(A, leaf_rows=1000)

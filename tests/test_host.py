@@ -179,3 +179,29 @@ def test_dropin_package_imports():
     assert caqr.trees.ReductionTree is ReductionTree
     assert callable(caqr.tsqr.tsqr_parallel) and callable(caqr.caqr.caqr_factor)
     assert callable(caqr.householder.qr_stacked_triangles)
+
+
+def test_stream_plan_is_the_binary_tree():
+    """Chunk subtrees + upper levels of the streamed TSQR are exactly the
+    pairs of the global binary tree (trees.py:52-66), and the chunks tile the
+    rows of BlockRowLayout(m, n, P)."""
+    from paper_0809_2407_b200.core import BlockRowLayout
+    from paper_0809_2407_b200.stream import plan_chunks, upper_events
+    from paper_0809_2407_b200.trees import ReductionTree
+
+    for P in [1, 2, 3, 5, 8, 13, 64, 100, 257]:
+        m, n = P * 50 + 7, 4
+        ref = {(a, b) for grp in ReductionTree(P=P).levels for (a, b) in grp}
+        lay = BlockRowLayout(m, n, P)
+        for K in [1, 2, 4, 8, 16, 128, 512]:
+            got, rows = set(), 0
+            for (l0, k, r0, nr) in plan_chunks(m, n, P, K):
+                assert r0 == rows == l0 * lay.base
+                rows += nr
+                assert nr == (k * lay.base if l0 + k < P else m - r0)
+                if k > 1:
+                    got |= {(l0 + a, l0 + b) for grp in ReductionTree(P=k).levels for (a, b) in grp}
+            assert rows == m
+            for e in upper_events(P, K):
+                got |= {(int(a), int(b)) for a, b, _ in e}
+            assert got == ref, (P, K)
