@@ -141,6 +141,9 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 #define CAQR_TUNE_NARROW 4
 /* CAQR_TUNE_DUAL: 1 (default) = two leaves per CTA in the n <= 128 chain kernel when its tile height is 8. */
 #define CAQR_TUNE_DUAL 5
+/* CAQR_TUNE_ZSTART: 1 (default) = R-only leaves (no Y stored) run the chain from
+ * R = 0 over all their rows instead of a dense first tile + chain. */
+#define CAQR_TUNE_ZSTART 6
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

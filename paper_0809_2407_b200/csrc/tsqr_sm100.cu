@@ -49,6 +49,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // the implicit-Q storage format, so factor and apply calls must agree.
 static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 1;
+static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_dual = 1;  // CAQR_TUNE_DUAL: two-leaf chain kernel for NP = 128, HT = 8  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -107,8 +108,12 @@ k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
 template <int NP, int HT>
 __global__ void __launch_bounds__(RingCfg<NP, HT>::WARPS_R * 32, 1)
 k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
-  constexpr int S = Geo<NP>::S, H0 = WARPS * Geo<NP>::HD, HW = HT;
+             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag,
+             int zstart) {
+  // zstart (R only): no dense first tile -- the chain starts from R = 0 at
+  // the leaf's first row (the QR of [0; A_leaf] has the same R up to signs).
+  constexpr int S = Geo<NP>::S, HW = HT;
+  const int H0 = zstart ? 0 : WARPS * Geo<NP>::HD;
   constexpr int RING_WARPS = RingCfg<NP, HT>::WARPS_R;
   constexpr int NT = RING_WARPS * 32;
   extern __shared__ __align__(16) double sm[];
@@ -127,7 +132,7 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   double* Rl = Rio + (int64_t)leaf * n * n;
   for (int idx = threadIdx.x; idx < NP * NP; idx += NT) {
     const int r = idx / NP, c = idx - r * NP;
-    Rs[idx] = (r < n && c < n && c >= r) ? Rl[r * n + c] : 0.0;
+    Rs[idx] = (!zstart && r < n && c < n && c >= r) ? Rl[r * n + c] : 0.0;
   }
   for (int j = threadIdx.x; j < NP; j += NT) ver[j] = 0;
   __syncthreads();
@@ -1090,16 +1095,21 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
     if (rc) return rc;                                                                          \
     k_leaf_chain<NPV, HTV><<<grid, RingCfg<NPV, HTV>::WARPS_R * 32, ChainSmem<NPV, HTV>::bytes,  \
                              st>>>(A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R,  \
-                                   flag);                                                        \
+                                   flag, zs ? 1 : 0);                                            \
   }
 #define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
-    int rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                    \
-    if (rc) return rc;                                                                          \
-    k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
-        base, Y, ldy, tau, tau_stride, R, flag);                                                \
-    if (m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                                    \
-      if (NPV == 128 && g_ht[np_index(NPV)] == 32) {                                           \
+    const bool pair = (NPV == 128 && g_ht[np_index(NPV)] == 32);                                \
+    const bool zs = !Y && g_zstart && !pair;                                                    \
+    int rc = 0;                                                                                 \
+    if (!zs) {                                                                                  \
+      rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                      \
+      if (rc) return rc;                                                                        \
+      k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
+          (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
+    }                                                                                           \
+    if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                              \
+      if (pair) {                                                                               \
         rc = prep(k_leaf_chain_pair, PairSmem::bytes);                                          \
         if (rc) return rc;                                                                      \
         k_leaf_chain_pair<<<grid, 256, PairSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
@@ -1384,6 +1394,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_NARROW) {
     g_narrow = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_ZSTART) {
+    g_zstart = value ? 1 : 0;
     return CAQR_OK;
   }
   return set_err(CAQR_ERR_ARG, "unknown tuning key");

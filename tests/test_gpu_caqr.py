@@ -49,9 +49,12 @@ def test_caqr_single_panel_equals_tsqr():
     from paper_0809_2407_b200.tsqr import tsqr
 
     A = philox(9).standard_normal((4096, 128))
-    R1 = caqr_factor(A, b=128, leaf_rows=1024).R
-    R2 = tsqr(A, leaf_rows=1024, split=False)
+    R1 = caqr_factor(A, b=128, leaf_rows=1024, panel_chains=1).R
+    R2, _ = tsqr(A, leaf_rows=1024, split=False, q="implicit")  # same leaf structure
     assert np.max(np.abs(R1 - R2)) <= 10 * EPS * np.linalg.norm(A, 2)
+    # R only starts every leaf chain from R = 0 (no dense tile): same R up to signs
+    R3 = tsqr(A, leaf_rows=1024, split=False)
+    assert oracle.r_diff(R1, R3, np.linalg.norm(A, 2)) <= 1000 * EPS
 
 
 def test_caqr_device_tensor_stays_on_device():
