@@ -503,6 +503,62 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
   put(node);  // the root (node 0)
 }
 
+// R-only tree combine as a warp ring: [R_a; R_b] -> R_a with R_a's rows as
+// the ring's pivot rows in shared memory and R_b's rows as ring tiles (the
+// zero lower part of R_b stays zero, so the reflectors keep the stacked
+// structure of qr_stacked_triangles, householder.py:263-294).  No node factor
+// is kept (R only).  Events from ev, or the binary level bin_level.
+template <int NP, int HT>
+__global__ void __launch_bounds__(RingCfg<NP, HT>::WARPS_R * 32, 1)
+k_tree_ring(double* Rslots, int n, const int* __restrict__ ev, int bin_level) {
+  constexpr int S = NP / 32;
+  constexpr int RING_WARPS = RingCfg<NP, HT>::WARPS_R;
+  constexpr int NT = RING_WARPS * 32;
+  extern __shared__ __align__(16) double sm[];
+  double* Rs = sm;
+  double* vbuf = Rs + NP * NP;
+  int* ver = reinterpret_cast<int*>(vbuf + RING_WARPS * 2 * HT);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int a, b;
+  if (ev) {
+    a = ev[3 * blockIdx.x];
+    b = ev[3 * blockIdx.x + 1];
+  } else {
+    a = blockIdx.x << bin_level;
+    b = a + (1 << (bin_level - 1));
+  }
+  double* Ra = Rslots + (int64_t)a * n * n;
+  const double* Rb = Rslots + (int64_t)b * n * n;
+  for (int idx = threadIdx.x; idx < NP * NP; idx += NT) {
+    const int r = idx / NP, c = idx - r * NP;
+    Rs[idx] = (r < n && c < n && c >= r) ? Ra[r * n + c] : 0.0;
+  }
+  for (int j = threadIdx.x; j < NP; j += NT) ver[j] = 0;
+  __syncthreads();
+  const int T = (n + HT - 1) / HT;
+  double X[HT][S];
+  for (int t = w; t < T; t += RING_WARPS) {
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+      const int r = t * HT + k;
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int c = 32 * s2 + lane;
+        X[k][s2] = (r < n && c < n && c >= r) ? Rb[r * n + c] : 0.0;
+      }
+    }
+    if constexpr (NP == 128 && HT == 16)
+      ring_factor_tile3<NP, HT>(X, Rs, ver, n, t, nullptr);
+    else
+      ring_factor_tile<NP, HT>(X, Rs, ver, vbuf + w * 2 * HT, n, t, nullptr);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+    const int r = idx / n, c = idx - r * n;
+    Ra[idx] = (c >= r) ? Rs[r * NP + c] : 0.0;
+  }
+}
+
 // One level of the narrow fused tree as its own launch (streamed TSQR's upper
 // levels): event e combines slot a (on top) with slot b exactly as
 // k_leaf_narrow's ticket tree does, one thread per event.
@@ -1154,17 +1210,17 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
     const int64_t nev = (P - 1 - (1LL << (k - 1))) / (1LL << k) + 1;  // f + 2^(k-1) < P, f = e 2^k
 #define TB_CASE(NPV)                                                                     \
   case NPV: {                                                                            \
-    rc = prep(k_tree_factor<NPV>, TreeSmem<NPV>::bytes);                                 \
+    rc = prep(k_tree_ring<NPV, 16>, ChainSmem<NPV, 16>::bytes);                          \
     if (rc) return rc;                                                                   \
-    k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
-        nullptr, nullptr, nullptr, k);                                                   \
+    k_tree_ring<NPV, 16><<<(int)nev, RingCfg<NPV, 16>::WARPS_R * 32,                     \
+                           ChainSmem<NPV, 16>::bytes, st>>>(Rslots, (int)n, nullptr, k); \
     break;                                                                               \
   }
     if (p == 32) {
       k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, nullptr, (int)nev,
                                                              nullptr, nullptr, k);
     } else {
-      switch (p) { TB_CASE(32) TB_CASE(64) TB_CASE(128) }
+      switch (p) { TB_CASE(64) TB_CASE(128) }
     }
 #undef TB_CASE
     rc = check_launch("k_tree_factor");
@@ -1202,10 +1258,10 @@ int tsqr_f64_r_combine_level(double* Rslots, int64_t n, const int32_t* events, i
   }
 #define RC_CASE(NPV)                                                                     \
   case NPV: {                                                                            \
-    int rc = prep(k_tree_factor<NPV>, TreeSmem<NPV>::bytes);                             \
+    int rc = prep(k_tree_ring<NPV, 16>, ChainSmem<NPV, 16>::bytes);                      \
     if (rc) return rc;                                                                   \
-    k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
-        events, nullptr, nullptr, 0);                                                    \
+    k_tree_ring<NPV, 16><<<(int)nev, RingCfg<NPV, 16>::WARPS_R * 32,                     \
+                           ChainSmem<NPV, 16>::bytes, st>>>(Rslots, (int)n, events, 0);  \
     break;                                                                               \
   }
   switch (p) { RC_CASE(64) RC_CASE(128) }
