@@ -386,10 +386,10 @@ def run_ours(args, cfg):
         F_leaf = flops(hi - lo, n)
         ach = F_leaf / t_leaf / 1e12
         # DRAM traffic of the chain kernel from the committed ncu capture
-        # (profiles/r01/chain_kernel_ncu_summary.txt: 1.233e9 B read + 5.9e6 B
-        # written for 148 leaves of 8192 x 128 = 1.020x the 8mn algorithmic
+        # (profiles/r01/chain_kernel_ncu_summary.txt: 1.2417e9 B read + 3.5e6 B
+        # written for 148 leaves of 8192 x 128 = 1.0030x the 8mn algorithmic
         # bytes), scaled to this launch's rows; None for other widths.
-        traffic = 8.0 * (hi - lo) * n * 1.0245 if (n == 128 and cfg["q"] == "none") else None
+        traffic = 8.0 * (hi - lo) * n * 1.0030 if (n == 128 and cfg["q"] == "none") else None
         roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "traffic_source": "ncu --set full, profiles/r01 (scaled per launch)",

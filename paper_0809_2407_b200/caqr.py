@@ -107,9 +107,12 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     nb = len(starts)
     panels = [None] * nb
     nlaunch = [0]
-
-    def factor(jp, st):
-        c0 = starts[jp]
+    # plan every panel and carve all device buffers out of four allocations up
+    # front, so the enqueue loop below never allocates (no allocator stalls
+    # between the two streams)
+    plan = []
+    n_tau = n_rs = n_ny = n_nt = 0
+    for c0 in starts:
         c1 = min(c0 + b, n)
         w = c1 - c0
         mj = m - c0
@@ -118,27 +121,41 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
             P *= 2  # split leaves into GPU chains (hybrid tree, see tsqr.split_leaves)
         lay = BlockRowLayout(mj, w, P)
         _, h0, ht = _lib.geometry(w)
-        tau = torch.zeros((P, _tiles_per_leaf(lay, h0, ht), w), dtype=torch.float64, device=dev)
-        Rs = torch.empty((P, w, w), dtype=torch.float64, device=dev)
+        tiles = _tiles_per_leaf(lay, h0, ht)
+        tree = ReductionTree(P=P, shape=BINARY)
+        plan.append((c0, c1, w, mj, P, lay, h0, tiles, tree, _levels_on(tree, dev),
+                     n_tau, n_rs, n_ny, n_nt))
+        n_tau += P * tiles * w
+        n_rs += P * w * w
+        n_ny += (P - 1) * w * w
+        n_nt += (P - 1) * w
+    tau_all = torch.zeros(max(1, n_tau), dtype=torch.float64, device=dev)
+    rs_all = torch.empty(max(1, n_rs), dtype=torch.float64, device=dev)
+    ny_all = torch.zeros(max(1, n_ny), dtype=torch.float64, device=dev)
+    nt_all = torch.zeros(max(1, n_nt), dtype=torch.float64, device=dev)
+    roots = [None] * nb
+
+    def factor(jp, st):
+        c0, c1, w, mj, P, lay, h0, tiles, tree, levels, o_t, o_r, o_y, o_n = plan[jp]
+        tau = tau_all[o_t:o_t + P * tiles * w].view(P, tiles, w)
+        Rs = rs_all[o_r:o_r + P * w * w].view(P, w, w)
         base_ptr = _ptr(W) + 8 * (c0 * n + c0)
         sh = int(st.cuda_stream)
-        _lib.check(lib.tsqr_f64_leaf_factor(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
-                                            tau.shape[1] * w, _ptr(Rs), _ptr(flag), sh),
-                   "tsqr_f64_leaf_factor")
-        tree = ReductionTree(P=P, shape=BINARY)
-        levels = _levels_on(tree, dev)
         nlaunch[0] += 1 + (mj - lay.base * (P - 1) > h0) + (len(levels) if P > 1 else 0)
+        _lib.check(lib.tsqr_f64_leaf_factor(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
+                                            tiles * w, _ptr(Rs), _ptr(flag), sh),
+                   "tsqr_f64_leaf_factor")
         node_Y = node_tau = None
         if P > 1:
-            node_Y = torch.zeros((P - 1, w, w), dtype=torch.float64, device=dev)
-            node_tau = torch.zeros((P - 1, w), dtype=torch.float64, device=dev)
+            node_Y = ny_all[o_y:o_y + (P - 1) * w * w].view(P - 1, w, w)
+            node_tau = nt_all[o_n:o_n + (P - 1) * w].view(P - 1, w)
             for ev in levels:
                 _lib.check(lib.tsqr_f64_tree_factor_level(_ptr(Rs), w, _ptr(ev), ev.shape[0],
                                                           _ptr(node_Y), _ptr(node_tau), sh),
                            "tsqr_f64_tree_factor_level")
-        # root R onto the diagonal block (its strict lower part keeps leaf 0's Y)
-        blk = W[c0:c1, c0:c1]
-        blk.copy_(torch.tril(blk, -1) + Rs[tree.root])
+        # the root R goes onto the diagonal block after the loop (no later
+        # panel reads it); its strict lower part keeps leaf 0's Y
+        roots[jp] = Rs[tree.root]
         panels[jp] = CaqrPanel(c0, c1, lay, tree, tau, node_Y, node_tau, levels)
 
     def apply(jp, lo, hi, st):
@@ -174,33 +191,30 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         sB.wait_stream(cur)
         evF = [None] * nb
         evB = [None] * nb
-        with torch.cuda.stream(sA):
-            factor(0, sA)
-            evF[0] = torch.cuda.Event()
-            evF[0].record(sA)
+        factor(0, sA)
+        evF[0] = torch.cuda.Event()
+        evF[0].record(sA)
         for jp in range(nb):
             if jp + 1 < nb:
                 # near: block jp+1 already carries Q_0..Q_{jp-1} (far updates on sB)
                 if jp >= 1:
                     sA.wait_event(evB[jp - 1])
-                with torch.cuda.stream(sA):
-                    nxt = starts[jp + 1]
-                    apply(jp, nxt, min(nxt + b, n), sA)
-                    factor(jp + 1, sA)
-                    evF[jp + 1] = torch.cuda.Event()
-                    evF[jp + 1].record(sA)
+                nxt = starts[jp + 1]
+                apply(jp, nxt, min(nxt + b, n), sA)
+                factor(jp + 1, sA)
+                evF[jp + 1] = torch.cuda.Event()
+                evF[jp + 1].record(sA)
             sB.wait_event(evF[jp])
-            with torch.cuda.stream(sB):
-                if jp + 2 < nb:
-                    apply(jp, starts[jp + 2], n, sB)
-                evB[jp] = torch.cuda.Event()
-                evB[jp].record(sB)
+            if jp + 2 < nb:
+                apply(jp, starts[jp + 2], n, sB)
+            evB[jp] = torch.cuda.Event()
+            evB[jp].record(sB)
         cur.wait_stream(sA)
         cur.wait_stream(sB)
-        for pnl in panels:  # device buffers created on sA are read on sB
-            for t in (pnl.tau, pnl.node_Y, pnl.node_tau):
-                if t is not None:
-                    t.record_stream(sB)
+    for jp in range(nb):
+        c0, c1 = plan[jp][0], plan[jp][1]
+        blk = W[c0:c1, c0:c1]
+        blk.copy_(torch.tril(blk, -1) + roots[jp])
     _check_flag(flag)
     if counter is not None:
         counter.add(2 * m * n * n - (2 * n ** 3) // 3)

@@ -54,7 +54,16 @@ def to_device(A, device=None, name="matrix"):
 
 
 def _out(t, host: bool):
-    return t.cpu().numpy() if host else t
+    """Result in the caller's memory space: numpy for host callers.  Large
+    results go through a pinned buffer (full-bandwidth D2H; the caching host
+    allocator recycles it once the array is dropped)."""
+    if not host:
+        return t
+    if t.numel() * t.element_size() < (1 << 22):
+        return t.cpu().numpy()
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
 
 
 def _check_flag(flag) -> None:
