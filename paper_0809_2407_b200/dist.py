@@ -49,54 +49,68 @@ def shard_rows(m: int, world: int, rank: int):
     return lo, hi
 
 
+def _members(group, members):
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    mem = list(range(world)) if members is None else list(members)
+    return mem, (mem.index(me) if me in mem else None)
+
+
 def cross_tree(R_local: torch.Tensor, combine, group=None, all_reduce: bool = False,
-               recorder=None):
+               recorder=None, members=None):
     """Combine per-rank R factors up the binary tree over the ranks.
 
-    ``combine(Ra, Rb) -> (R, node)`` runs on the receiver.  Returns (R or None,
-    list of (level, partner, node) factors kept by this rank).
+    ``combine(Ra, Rb) -> (R, node)`` runs on the receiver.  ``members`` (group
+    ranks in tree order; default all, in rank order) lets a subset take part
+    with any rank as the root (virtual index 0) -- CAQR's panel tree is rooted
+    at the diagonal-block owner.  Returns (R or None, list of (level, partner,
+    node) factors kept by this rank); non-members return (None, []).
     """
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
+    mem, v = _members(group, members)
+    if v is None:
+        return None, []
     n = R_local.shape[0]
-    tree = ReductionTree(P=world)
+    tree = ReductionTree(P=len(mem))
     R = R_local
     nodes = []
     words = n * (n + 1) // 2
     for lvl, grp in enumerate(tree.levels, start=1):
         for (a, b) in grp:
-            if rank == b:
-                dist.send(pack_upper(R), dst=a, group=group)
+            if v == b:
+                dist.send(pack_upper(R), group=group, group_dst=mem[a])
                 if recorder is not None:
                     recorder.record_send(words)
-            elif rank == a:
+            elif v == a:
                 buf = torch.empty(words, dtype=R.dtype, device=R.device)
-                dist.recv(buf, src=b, group=group)
+                dist.recv(buf, group=group, group_src=mem[b])
                 if recorder is not None:
                     recorder.record_recv(words, stage=(lvl, "R"))
                 R, node = combine(R, unpack_upper(buf, n))
                 nodes.append((lvl, b, node))
         # ranks that already sent are done with the factorization
-    is_root = rank == tree.root
+    is_root = v == tree.root
     if all_reduce:
+        if len(mem) != dist.get_world_size(group):
+            raise ValueError("all-reduce mode needs every rank of the group")
         buf = pack_upper(R) if is_root else torch.empty(words, dtype=R.dtype, device=R.device)
-        dist.broadcast(buf, src=tree.root, group=group)
+        dist.broadcast(buf, group=group, group_src=mem[tree.root])
         R = unpack_upper(buf, n)
         return R, nodes
     return (R if is_root else None), nodes
 
 
 def cross_apply(nodes, C_top: torch.Tensor, apply_node, transpose: bool = False, group=None,
-                zero_partner: bool = False, recorder=None) -> torch.Tensor:
+                zero_partner: bool = False, recorder=None, members=None) -> torch.Tensor:
     """Apply Q_cross (top-down) or Q_cross^T (bottom-up) of the cross-rank tree
     to this rank's top block C_top (n x k); ``nodes`` is this rank's list from
-    ``cross_tree``.  ``apply_node(node, Ca, Cb, transpose) -> (Ca, Cb)`` runs
-    on the receiver of each event (apply_stacked semantics, householder.py:377-396).
-    ``zero_partner`` (top-down only): the partner's block is zero on arrival,
-    so it is not sent (explicit-Q formation)."""
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    tree = ReductionTree(P=world)
+    ``cross_tree`` (same ``members``).  ``apply_node(node, Ca, Cb, transpose)
+    -> (Ca, Cb)`` runs on the receiver of each event (apply_stacked semantics,
+    householder.py:377-396).  ``zero_partner`` (top-down only): the partner's
+    block is zero on arrival, so it is not sent (explicit-Q formation)."""
+    mem, v = _members(group, members)
+    if v is None:
+        return C_top
+    tree = ReductionTree(P=len(mem))
     levels = list(enumerate(tree.levels, start=1))
     if not transpose:
         levels = levels[::-1]
@@ -106,27 +120,27 @@ def cross_apply(nodes, C_top: torch.Tensor, apply_node, transpose: bool = False,
     words = C.numel()
     for lvl, grp in levels:
         for (a, b) in grp:
-            if rank == b:
+            if v == b:
                 if not skip_up:
-                    dist.send(C, dst=a, group=group)
+                    dist.send(C, group=group, group_dst=mem[a])
                     if recorder is not None:
                         recorder.record_send(words)
                 buf = torch.empty_like(C)
-                dist.recv(buf, src=a, group=group)
+                dist.recv(buf, group=group, group_src=mem[a])
                 if recorder is not None:
                     recorder.record_recv(words, stage=(lvl, "Q"))
                 C = buf
-            elif rank == a:
+            elif v == a:
                 if skip_up:
                     Cb = torch.zeros_like(C)
                 else:
                     Cb = torch.empty_like(C)
-                    dist.recv(Cb, src=b, group=group)
+                    dist.recv(Cb, group=group, group_src=mem[b])
                     if recorder is not None:
                         recorder.record_recv(words, stage=(lvl, "Q"))
                 C, Cb = apply_node(node_of[(lvl, b)], C, Cb, transpose)
                 C = C.contiguous()
-                dist.send(Cb.contiguous(), dst=b, group=group)
+                dist.send(Cb.contiguous(), group=group, group_dst=mem[b])
                 if recorder is not None:
                     recorder.record_send(words)
     return C
@@ -150,9 +164,9 @@ def sharded_apply_q(local_factor, nodes, C_shard: torch.Tensor, n: int, local_ap
 def sharded_explicit_q(local_factor, nodes, n: int, local_apply, apply_node,
                        group=None, device=None, recorder=None) -> torch.Tensor:
     """This rank's rows of the thin Q (Q [I; 0])."""
-    rank = dist.get_rank(group)
-    root = ReductionTree(P=dist.get_world_size(group)).root
-    S = torch.eye(n, dtype=torch.float64, device=device) if rank == root else \
+    mem, v = _members(group, None)
+    root = ReductionTree(P=len(mem)).root
+    S = torch.eye(n, dtype=torch.float64, device=device) if v == root else \
         torch.zeros((n, n), dtype=torch.float64, device=device)
     S = cross_apply(nodes, S, apply_node, False, group, zero_partner=True, recorder=recorder)
     return local_apply(local_factor, S, False)  # thin: Q_local [S; 0]

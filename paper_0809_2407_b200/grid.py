@@ -1,0 +1,304 @@
+"""CAQR on a Pr x Pc process grid: Algorithm 3.
+
+One rank per GPU; rank (r, c) = r * Pc + c owns the b x b blocks (i, j) with
+(i mod Pr, j mod Pc) = (r, c) (``BlockCyclicLayout``, core.py:64-91), stored
+as one local row-major matrix (local block (i // Pr, j // Pc)).  For panel j
+(block column j, held by process column cj = j mod Pc):
+
+1. TSQR of the panel over the process column (Alg. 3 line 2): each rank
+   with active rows (block rows >= j) factors its piece on the GPU (local
+   leaves + local tree, implicit Q kept), then the column tree combines the
+   R factors with the diagonal-block owner as root (reduce variant, "the
+   panel's R factor need only be stored on one processor").
+2. Row broadcast (line 3): the factor of each piece -- leaf Y, tau, local
+   tree factors and the rank's cross-tree node factors -- goes to the other
+   ranks of its process row.
+3. Leaf-level update (line 4): every rank applies its row's Q^T to its
+   local trailing blocks.
+4. Tree-level updates (lines 5-10): per process column, the top b rows of
+   the trailing blocks go up the column tree; the receiver applies the node's
+   Q^T to [C_a; C_b] and returns the partner's part (``dist.cross_apply``).
+
+Compute is a backend object (``GpuBackend`` drives the sm_100a kernels); the
+communication pattern is backend independent, which is what the gloo tests
+exercise with an injected CPU backend.  R ends in the upper triangle of the
+distributed matrix (diagonal blocks on their owners); ``gather_R`` assembles
+it on rank 0.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from .core import BlockCyclicLayout, BlockRowLayout, DimensionError
+from .dist import cross_apply, cross_tree
+from .trees import BINARY, ReductionTree
+
+
+def _cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+@dataclass
+class GridInfo:
+    layout: BlockCyclicLayout
+    r: int
+    c: int
+    row_group: object
+    col_group: object
+
+    @property
+    def b(self) -> int:
+        return self.layout.b
+
+    def local_blocks(self):
+        L = self.layout
+        return (max(0, _cdiv(L.m_blocks - self.r, L.Pr)), max(0, _cdiv(L.n_blocks - self.c, L.Pc)))
+
+    def first_local_row_block(self, j: int, r: int | None = None) -> int:
+        """Local index of the first block row >= j held by process row r."""
+        r = self.r if r is None else r
+        return max(0, _cdiv(j - r, self.layout.Pr))
+
+    def active_rows(self, j: int, r: int | None = None) -> int:
+        r = self.r if r is None else r
+        mb = max(0, _cdiv(self.layout.m_blocks - r, self.layout.Pr))
+        return max(0, mb - self.first_local_row_block(j, r)) * self.b
+
+    def panel_members(self, j: int):
+        """Process rows with active rows for panel j, diagonal owner first."""
+        Pr = self.layout.Pr
+        rd = j % Pr
+        return [(rd + k) % Pr for k in range(Pr) if self.active_rows(j, (rd + k) % Pr) > 0]
+
+    def first_local_col_block(self, jmin: int) -> int:
+        """Local index of the first block column >= jmin held by this process column."""
+        return max(0, _cdiv(jmin - self.c, self.layout.Pc))
+
+
+def make_grid(layout: BlockCyclicLayout, backend: str | None = None) -> GridInfo:
+    """Row / column communicators of the Pr x Pc grid over the default group."""
+    world = dist.get_world_size()
+    if world != layout.Pr * layout.Pc:
+        raise DimensionError(f"grid {layout.Pr}x{layout.Pc} needs {layout.Pr * layout.Pc} ranks, have {world}")
+    rank = dist.get_rank()
+    r, c = divmod(rank, layout.Pc)
+    row_group = col_group = None
+    for rr in range(layout.Pr):  # every rank creates every group, in the same order
+        g = dist.new_group([rr * layout.Pc + cc for cc in range(layout.Pc)], backend=backend)
+        if rr == r:
+            row_group = g
+    for cc in range(layout.Pc):
+        g = dist.new_group([rr * layout.Pc + cc for rr in range(layout.Pr)], backend=backend)
+        if cc == c:
+            col_group = g
+    return GridInfo(layout, r, c, row_group, col_group)
+
+
+def scatter_local(A: torch.Tensor, grid: GridInfo) -> torch.Tensor:
+    """This rank's local matrix of the block-cyclic distribution of A."""
+    L, b = grid.layout, grid.b
+    mb, nb = grid.local_blocks()
+    out = torch.empty((mb * b, nb * b), dtype=torch.float64, device=A.device)
+    for li in range(mb):
+        i = grid.r + li * L.Pr
+        for lj in range(nb):
+            j = grid.c + lj * L.Pc
+            out[li * b:(li + 1) * b, lj * b:(lj + 1) * b] = A[i * b:(i + 1) * b, j * b:(j + 1) * b]
+    return out
+
+
+@dataclass
+class GridCaqrResult:
+    local: torch.Tensor          # this rank's blocks; R in the global upper triangle
+    grid: GridInfo
+    panels: dict = field(default_factory=dict)   # j -> (local factor, cross nodes) on ranks that hold them
+    recorder: object = None
+    broadcast_words: int = 0
+
+
+class GpuBackend:
+    """sm_100a kernels for the per-rank compute of grid CAQR."""
+
+    def __init__(self, leaf_rows: int = 2048, device=None):
+        self.leaf_rows = leaf_rows
+        self.device = device
+
+    def _leaves(self, m_r: int, b: int) -> int:
+        from .caqr import _panel_leaves
+
+        return _panel_leaves(m_r, b, self.leaf_rows)
+
+    def local_factor(self, piece: torch.Tensor):
+        from .tsqr import factor_device
+
+        m_r, b = piece.shape
+        f = factor_device(piece.contiguous(), self._leaves(m_r, b), want_q=True)
+        return f, f.R.clone()
+
+    def combine(self, Ra, Rb):
+        from .dist import gpu_combine
+
+        return gpu_combine(Ra, Rb)
+
+    def apply_node(self, node, Ca, Cb, transpose):
+        from .dist import gpu_apply_node
+
+        return gpu_apply_node(node, Ca, Cb, transpose)
+
+    def local_apply(self, f, C, transpose):
+        from .tsqr import apply_q_device
+
+        return apply_q_device(f, C.contiguous(), transpose)
+
+    def pack(self, f, nodes):
+        ts = [f.Y, f.tau]
+        if f.node_Y is not None:
+            ts += [f.node_Y, f.node_tau]
+        for (_, _, (Yn, tn)) in nodes:
+            ts += [Yn, tn]
+        return [t.contiguous() for t in ts]
+
+    def shapes(self, m_r: int, b: int, node_keys):
+        from . import _lib
+        from .tsqr import _tiles_per_leaf
+
+        P = self._leaves(m_r, b)
+        _, h0, ht = _lib.geometry(b)
+        tiles = _tiles_per_leaf(BlockRowLayout(m_r, b, P), h0, ht)
+        out = [(m_r, b), (P, tiles, b)]
+        if P > 1:
+            out += [(P - 1, b, b), (P - 1, b)]
+        for _ in node_keys:
+            out += [(b, b), (b,)]
+        return out
+
+    def unpack(self, ts, m_r: int, b: int, node_keys):
+        from . import _lib
+        from .tsqr import TsqrFactor, _levels_on
+
+        P = self._leaves(m_r, b)
+        _, h0, ht = _lib.geometry(b)
+        tree = ReductionTree(P=P, shape=BINARY)
+        k = 2
+        nY = nt = None
+        if P > 1:
+            nY, nt = ts[2], ts[3]
+            k = 4
+        f = TsqrFactor(tree=tree, layout=BlockRowLayout(m_r, b, P),
+                       R=torch.zeros((b, b), dtype=torch.float64, device=ts[0].device), n=b, h0=h0,
+                       ht=ht, Y=ts[0], tau=ts[1], node_Y=nY, node_tau=nt,
+                       levels=_levels_on(tree, ts[0].device))
+        nodes = []
+        for (lvl, partner) in node_keys:
+            nodes.append((lvl, partner, (ts[k], ts[k + 1])))
+            k += 2
+        return f, nodes
+
+
+def _node_keys(n_members: int, v: int):
+    """(level, partner) of the events where virtual index v receives."""
+    tree = ReductionTree(P=n_members)
+    return [(lvl, b) for lvl, grp in enumerate(tree.levels, start=1) for (a, b) in grp if a == v]
+
+
+def caqr_grid(local: torch.Tensor, grid: GridInfo, backend, recorder=None) -> GridCaqrResult:
+    """Algorithm 3 on this rank's local blocks (modified in place)."""
+    L = grid.layout
+    b = grid.b
+    if L.m < L.n:
+        raise DimensionError(f"need m >= n, got {L.m} x {L.n}")
+    if L.Pr & (L.Pr - 1):
+        raise DimensionError(f"Pr must be a power of two (PAPER.md Alg. 3), got {L.Pr}")
+    mb, nb = grid.local_blocks()
+    if tuple(local.shape) != (mb * b, nb * b):
+        raise DimensionError("local matrix does not match the grid layout")
+    res = GridCaqrResult(local=local, grid=grid, recorder=recorder)
+    dev = local.device
+    for j in range(L.n_blocks):
+        cj = j % L.Pc
+        members = grid.panel_members(j)
+        m_r = grid.active_rows(j)
+        mine = m_r > 0
+        t0 = grid.first_local_row_block(j) * b
+        v = members.index(grid.r) if mine else None
+        keys = _node_keys(len(members), v) if mine else []
+        f = nodes = None
+        # 1. panel TSQR over process column cj
+        if grid.c == cj and mine:
+            lj = j // L.Pc
+            piece = local[t0:, lj * b:(lj + 1) * b]
+            f, R = backend.local_factor(piece)
+            Rroot, nodes = cross_tree(R, backend.combine, group=grid.col_group, members=members,
+                                      recorder=recorder)
+            piece.zero_()
+            if Rroot is not None:  # diagonal owner: R_jj on the diagonal block
+                local[t0:t0 + b, lj * b:(lj + 1) * b] = torch.triu(Rroot)
+        # 2. row broadcast of the factors of this process row's piece
+        if mine and L.Pc > 1:
+            if grid.c == cj:
+                ts = backend.pack(f, nodes)
+            else:
+                ts = [torch.empty(s, dtype=torch.float64, device=dev)
+                      for s in backend.shapes(m_r, b, keys)]
+            for t in ts:
+                dist.broadcast(t, group=grid.row_group, group_src=cj)
+                res.broadcast_words += t.numel() if grid.c == cj else 0
+            if grid.c != cj:
+                f, nodes = backend.unpack(ts, m_r, b, keys)
+        if mine:
+            res.panels[j] = (f, nodes)
+        # 3. leaf-level update of the local trailing blocks (block columns > j)
+        lc0 = grid.first_local_col_block(j + 1) * b
+        if not mine or lc0 >= local.shape[1]:
+            continue
+        C = backend.local_apply(f, local[t0:, lc0:], True)
+        local[t0:, lc0:] = C
+        # 4. tree-level updates up the column tree (every process column)
+        top = cross_apply(nodes, local[t0:t0 + b, lc0:].clone(), backend.apply_node, True,
+                          group=grid.col_group, members=members, recorder=recorder)
+        local[t0:t0 + b, lc0:] = top
+    return res
+
+
+def gather_R(res: GridCaqrResult):
+    """n x n R on rank 0 (None elsewhere), from the blocks (i, j), i <= j < n_blocks."""
+    grid = res.grid
+    L, b = grid.layout, grid.b
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    nbk = L.n_blocks
+
+    def rows_of(r):
+        return min(max(0, _cdiv(L.m_blocks - r, L.Pr)), max(0, _cdiv(nbk - r, L.Pr))) * b
+
+    def cols_of(c):
+        return max(0, _cdiv(nbk - c, L.Pc)) * b
+
+    if rank != 0:
+        mine = res.local[:rows_of(grid.r), :cols_of(grid.c)].contiguous()
+        if mine.numel():
+            dist.send(mine, dst=0)
+        return None
+    R = torch.zeros((L.n, L.n), dtype=torch.float64, device=res.local.device)
+    for src in range(world):
+        r, c = divmod(src, L.Pc)
+        shape = (rows_of(r), cols_of(c))
+        if shape[0] * shape[1] == 0:
+            continue
+        if src == 0:
+            blk = res.local[:shape[0], :shape[1]]
+        else:
+            blk = torch.empty(shape, dtype=torch.float64, device=res.local.device)
+            dist.recv(blk, src=src)
+        for li in range(shape[0] // b):
+            i = r + li * L.Pr
+            for lj in range(shape[1] // b):
+                jj = c + lj * L.Pc
+                if i <= jj:
+                    R[i * b:(i + 1) * b, jj * b:(jj + 1) * b] = blk[li * b:(li + 1) * b,
+                                                                    lj * b:(lj + 1) * b]
+    return torch.triu(R)
