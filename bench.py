@@ -260,6 +260,98 @@ def caqr_roofline(A, cfg, args):
              "algorithmic_flops_per_launch": F, "launch_ms": t * 1e3}, launches)
 
 
+def run_grid(args, cfg, ws, rank, local):
+    """C5 on a 2 x (N/2) process grid (Algorithm 3, paper_0809_2407_b200.grid):
+    block-cyclic 128 x 128 blocks, one rank per GPU, NCCL row / column groups.
+    Every rank generates the same seeded A and keeps its own blocks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_0809_2407_b200.core import BlockCyclicLayout
+    from paper_0809_2407_b200.grid import GpuBackend, caqr_grid, gather_R, make_grid, scatter_local
+
+    dev = torch.device("cuda", local)
+    m, n, b = cfg["m"], cfg["n"], 128
+    Pr = 2 if ws % 2 == 0 else 1  # C5: 2 x 4 at 8 GPUs (SURVEY 8(e))
+    Pc = ws // Pr
+    grid = make_grid(BlockCyclicLayout(m, n, b, Pr, Pc))
+    A = make_input(cfg, dev)
+    base = scatter_local(A, grid)
+    del A
+    be = GpuBackend(leaf_rows=cfg["leaf"])
+    work = torch.empty_like(base)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        work.copy_(base)
+        return caqr_grid(work, grid, be)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    copy_ms = 0.0
+    with Clocks(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        dist.barrier()
+        torch.cuda.synchronize()
+    # the per-step reset copy of the local blocks is not CAQR work: time it alone
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(args.steps):
+        work.copy_(base)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    copy_ms = c0.elapsed_time(c1) / args.steps
+    ms = t0.elapsed_time(t1) / args.steps - copy_ms
+    ms_t = torch.tensor([ms], device=dev)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    F = flops(m, n)
+    value = F / (ms * 1e-3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        # host blocks (pinned) -> device, Algorithm 3, R gathered back to rank 0's host
+        hostb = torch.empty(base.shape, dtype=torch.float64, pin_memory=True)
+        hostb.copy_(base)
+        dist.barrier()
+        ts = time.perf_counter()
+        loc = hostb.to(dev, non_blocking=True)
+        R = gather_R(caqr_grid(loc, grid, be))
+        Rh = R.cpu() if R is not None else None
+        dist.barrier()
+        dt = time.perf_counter() - ts
+        dt_t = torch.tensor([dt], device=dev)
+        dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+        dt = float(dt_t.item())
+        e2e = {"value": F / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(m * n * 8),
+               "d2h_bytes_per_step": int(n * n * 8), "ms_per_step": dt * 1e3}
+        del Rh
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic iid " + cfg["dist"] + " (torch Philox on device, same seed on every rank)",
+            "config": {"workload": cfg["name"] + f", {Pr}x{Pc} grid", "m": m, "n": n, "b": b,
+                       "leaf_rows": cfg["leaf"], "parallelism": f"2-D block-cyclic {Pr}x{Pc}",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "timing": "events around K steps minus the per-step block reset copy"},
+            "roofline": None, "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": None, "gflops_roofline_frac": value / (FP64_PEAK_TFLOPS * 1e3 * ws),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -275,8 +367,17 @@ def run_ours(args, cfg):
     _lib.load()
     m, n = cfg["m"], cfg["n"]
     is_caqr = cfg is CONFIGS["c5"]
-    if is_caqr and ws > 1:
-        raise SystemExit("c5 multi-GPU grid run is not part of this bench yet")
+    if is_caqr and (ws > 1 or args.grid):
+        if not dist.is_initialized():  # --grid on one GPU: a 1 x 1 grid
+            import socket
+
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=torch.device("cuda", local))
+        return run_grid(args, cfg, ws, rank, local)
     # shard rows (1-D block rows); A resident in HBM
     from paper_0809_2407_b200.dist import shard_rows, tsqr_sharded
 
@@ -487,6 +588,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--graph", type=int, default=1,
                     help="replay each TSQR step as one captured CUDA graph (1 GPU, not CAQR)")
+    ap.add_argument("--grid", action="store_true",
+                    help="c5: run the Pr x Pc grid driver even on one GPU (1 x 1 grid)")
     ap.add_argument("--panel-chains", type=int, default=2,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()
