@@ -318,21 +318,43 @@ def _leaves_for(m: int, n: int, leaf_rows: int) -> int:
 
 
 def split_leaves(m: int, n: int, P: int, min_chains: int | None = None,
-                 min_rows: int = 512) -> int:
+                 min_rows: int = 512, fill: bool = False) -> int:
     """GPU chains per leaf (a power of two) for a leaf count P.
 
     A leaf processed as 2^k equal chains whose R factors are combined by a
     binary tree is the paper's hybrid tree: the
     binary tree over P*2^k chains combines every leaf's chains in its first
-    k levels.  Leaves are split until there is at least one chain per SM
-    (``min_chains``), keeping chains >= max(min_rows, 4n) rows.
+    k levels.  Chains stay >= max(min_rows, 4n) rows.  Default: split until
+    there is one chain per SM (``min_chains``, default the SM count).  With
+    ``fill`` (R-only chain kernel) the split maximises the wave fill
+    chains / (waves x SMs) instead; a further split must gain > 2% fill
+    (measured: C3's per-GPU shard at 4 GPUs runs 10% faster as 2 chains per
+    leaf; splitting R + Q or the narrow kernel's leaves only adds tree and
+    per-chain overhead, tools/prof_split.py).
     """
     if min_chains is None:
         min_chains = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+    def ok(k):
+        return m // (P * 2 * k) >= max(min_rows, 4 * n)
+
+    if not fill:
+        k = 1
+        while P * k < min_chains and ok(k):
+            k *= 2
+        return k
+
+    def frac(k):
+        c = P * k
+        return c / (-(-c // min_chains) * min_chains)
+
+    best_k, best = 1, frac(1)
     k = 1
-    while P * k < min_chains and m // (P * 2 * k) >= max(min_rows, 4 * n):
+    while ok(k) and P * k < 16 * min_chains:
         k *= 2
-    return k
+        if frac(k) > best + 0.02:
+            best_k, best = k, frac(k)
+    return best_k
 
 
 def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None = None,
@@ -367,7 +389,7 @@ def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None =
         else:
             P = _leaves_for(m, n, leaf_rows)
             if split:
-                P *= split_leaves(m, n, P)
+                P *= split_leaves(m, n, P, fill=n > 8)
         BlockRowLayout(m, n, P)  # raises DimensionError for short leaves
         R = tsqr_stream(Ah, P, device=device)
         if counter is not None:
@@ -383,7 +405,7 @@ def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None =
     else:
         P = _leaves_for(m, n, leaf_rows)
         if split:
-            P *= split_leaves(m, n, P)
+            P *= split_leaves(m, n, P, fill=(n > 8 and q == "none"))
     f = factor_device(At, P, want_q=(q != "none"), tree=tree, counter=counter, host=host)
     if q == "none":
         return f.R_out()

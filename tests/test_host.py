@@ -205,3 +205,18 @@ def test_stream_plan_is_the_binary_tree():
             for e in upper_events(P, K):
                 got |= {(int(a), int(b)) for a, b, _ in e}
             assert got == ref, (P, K)
+
+
+def test_split_leaves_wave_fill():
+    """Chains per leaf (148 SMs): one chain per SM by default, wave fill for
+    the R-only chain kernel."""
+    from paper_0809_2407_b200.tsqr import split_leaves
+
+    S = 148
+    assert split_leaves(65536, 32, 8, S) == 16                        # C1: 128 chains of 512 rows
+    assert split_leaves(1048576, 64, 256, S) == 1                     # C2 (R + Q)
+    assert split_leaves(1 << 24, 128, 2048, S, fill=True) == 1        # C3, 1 GPU: 13.8 waves
+    assert split_leaves(1 << 22, 128, 512, S, fill=True) == 2         # C3 per GPU at 4 GPUs
+    assert split_leaves(1 << 21, 128, 256, S, fill=True) == 4         # C3 per GPU at 8 GPUs
+    assert split_leaves(1 << 24, 8, 1024, S) == 1                     # C4 per GPU at 8 GPUs
+    assert split_leaves(4096, 64, 1, S) == 8                          # chains stay >= 512 rows
