@@ -132,15 +132,14 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 
 /* Process-wide tuning knobs (not thread-safe; set before launching work).
  * CAQR_TUNE_CHAIN_HT_{32,64,128}: chain tile height for padded width 32/64
- * (16 or 32) and 128 (8 or 16).  It fixes the implicit-Q format: factor and
+ * (16 or 32) and 128 (16 or 24).  It fixes the implicit-Q format: factor and
  * apply calls on the same factor must see the same value. */
 #define CAQR_TUNE_CHAIN_HT_32 1
 #define CAQR_TUNE_CHAIN_HT_64 2
 #define CAQR_TUNE_CHAIN_HT_128 3
 /* CAQR_TUNE_NARROW: 1 (default) = lane-private chains for n <= 8 when no Q is stored. */
 #define CAQR_TUNE_NARROW 4
-/* CAQR_TUNE_DUAL: 1 (default) = two leaves per CTA in the n <= 128 chain kernel when its tile height is 8. */
-#define CAQR_TUNE_DUAL 5
+/* 5: reserved (retired experimental kernel). */
 /* CAQR_TUNE_ZSTART: 1 (default) = R-only leaves (no Y stored) run the chain from
  * R = 0 over all their rows instead of a dense first tile + chain. */
 #define CAQR_TUNE_ZSTART 6

@@ -117,7 +117,6 @@ def check(rc: int, what: str) -> None:
 
 TUNE_CHAIN_HT = {32: 1, 64: 2, 128: 3}
 TUNE_NARROW = 4
-TUNE_DUAL = 5
 TUNE_ZSTART = 6
 
 

@@ -753,234 +753,6 @@ __device__ __forceinline__ void ring_factor_tile_vs(double (&X)[HW][NP / 32], do
 }
 
 // ---------------------------------------------------------------------------
-// Pair ring (n in (64, 128]): two warps share one 32-row chain tile and split
-// its 128 columns into global slots {0, 3} (role A) and {1, 2} (role B), which
-// balances their update work.  Reflector j is generated by the role that owns
-// column j (A: j < 32 or j >= 96, B: 32 <= j < 96) and its raw column, tau and
-// scale are broadcast to the partner through a double-buffered per-pair
-// shared slot (pub / ack sequence counters).  R rows are split the same way:
-// each role keeps its own column part of the ring (verA / verB).
-// ---------------------------------------------------------------------------
-constexpr int PAIR_HT = 32;
-constexpr int PBUF = 36;  // 32 raw values, tau, scale, pad
-
-__host__ __device__ constexpr int pr_owner(int g) { return (g == 1 || g == 2) ? 1 : 0; }
-__host__ __device__ constexpr int pr_gslot(int role, int l) {
-  return role == 0 ? (l == 0 ? 0 : 3) : (l == 0 ? 1 : 2);
-}
-__host__ __device__ constexpr int pr_lslot(int role, int g) {
-  return role == 0 ? (g == 0 ? 0 : (g == 3 ? 1 : -1)) : (g == 1 ? 0 : (g == 2 ? 1 : -1));
-}
-
-struct PairState {
-  double mysc[2];
-  double beta;  // beta of the reflector this warp generated last (written into R[j][j])
-};
-
-template <int ROLE, int G, bool LAST>
-__device__ __forceinline__ void pair_step(PairState& st, double (&X)[PAIR_HT][2], double* Rs,
-                                          int* verMine, int* pub, int* ackMine, int* ackOther,
-                                          double* buf, int n, int t, int seq0, int jj,
-                                          double* tau_tile) {
-  constexpr int HT = PAIR_HT;
-  constexpr bool OWN = (pr_owner(G) == ROLE);
-  constexpr int GN = LAST ? G + 1 : G;
-  constexpr bool OWNN = (GN < 4) && (pr_owner(GN) == ROLE);
-  constexpr int LSN = OWNN ? pr_lslot(ROLE, GN) : -1;
-  const int lane = threadIdx.x & 31;
-  const int j = 32 * G + jj;
-  const int jn = j + 1;
-  const int sq = seq0 + j;
-  const bool more = OWNN && (jn < n);
-  if (!OWN) {
-    while (ld_acquire(pub) < sq + 1) { }
-  }
-  const double* vx = buf + (sq & 1) * PBUF;
-  const double tau = vx[32], scale = vx[33];
-  const double bcur = st.beta;
-  while (ld_acquire(verMine + j) != t) { }
-  double* Rj = Rs + j * 128;
-  double qv[2] = {0.0, 0.0}, rv[2] = {0.0, 0.0};
-  // (1) the slot holding column j+1 (if this warp generates reflector j+1)
-  if constexpr (OWNN) {
-    constexpr int L = LSN;
-    constexpr int GS = pr_gslot(ROLE, L);
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll
-    for (int k = 0; k < HT; k += 4) {
-      const double2 va = *reinterpret_cast<const double2*>(vx + k);
-      const double2 vc = *reinterpret_cast<const double2*>(vx + k + 2);
-      p0 = fma(va.x, X[k][L], p0);
-      p1 = fma(va.y, X[k + 1][L], p1);
-      p2 = fma(vc.x, X[k + 2][L], p2);
-      p3 = fma(vc.y, X[k + 3][L], p3);
-    }
-    const double r = Rj[32 * GS + lane];
-    const bool act = (GS > G) || (lane > jj);
-    const double q = act ? tau * fma(scale, (p0 + p1) + (p2 + p3), r) : 0.0;
-    const double w = q * scale;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int k = 0; k < HT; k += 4) {
-      const double2 va = *reinterpret_cast<const double2*>(vx + k);
-      const double2 vc = *reinterpret_cast<const double2*>(vx + k + 2);
-      X[k][L] = fma(-va.x, w, X[k][L]);
-      X[k + 1][L] = fma(-va.y, w, X[k + 1][L]);
-      X[k + 2][L] = fma(-vc.x, w, X[k + 2][L]);
-      X[k + 3][L] = fma(-vc.y, w, X[k + 3][L]);
-      s0 = fma(X[k][L], X[k][L], s0);
-      s1 = fma(X[k + 1][L], X[k + 1][L], s1);
-      s2 = fma(X[k + 2][L], X[k + 2][L], s2);
-      s3 = fma(X[k + 3][L], X[k + 3][L], s3);
-    }
-    rv[L] = r;
-    qv[L] = q;
-    const double sg = __shfl_sync(FULL, (s0 + s1) + (s2 + s3), jn & 31);
-    double x0n = 1.0;
-    if (more) {
-      while (ld_acquire(verMine + jn) != t) { }
-      x0n = Rs[jn * 128 + jn];
-    }
-    double nbeta, ntau, nscale;
-    house_lean(x0n, sg, nbeta, ntau, nscale);
-    if (more) {
-      while (ld_acquire(ackOther) < sq) { }  // partner done with reflector j-1's slot
-      double* vn = buf + ((sq + 1) & 1) * PBUF;
-      if (lane == (jn & 31)) {
-        st.mysc[L] = nscale;
-#pragma unroll
-        for (int k = 0; k < HT; k += 2)
-          *reinterpret_cast<double2*>(vn + k) = make_double2(X[k][L], X[k + 1][L]);
-        vn[32] = ntau;
-        vn[33] = nscale;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        st_release(pub, sq + 2);
-      }
-      st.beta = nbeta;
-    }
-  }
-  // (2) the other active slots of this warp
-#pragma unroll
-  for (int L2 = 0; L2 < 2; ++L2) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    if (L2 == LSN) continue;
-    const int GS = pr_gslot(ROLE, L2);
-    if (GS < G) continue;  // finished columns
-    double p0 = 0.0, p1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      const double2 va = *reinterpret_cast<const double2*>(vx + k);
-      p0 = fma(va.x, X[k][L2], p0);
-      p1 = fma(va.y, X[k + 1][L2], p1);
-    }
-    const double r = Rj[32 * GS + lane];
-    const bool act = (GS > G) || (lane > jj);
-    const double q = act ? tau * fma(scale, p0 + p1, r) : 0.0;
-    const double w = q * scale;
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      const double2 va = *reinterpret_cast<const double2*>(vx + k);
-      X[k][L2] = fma(-va.x, w, X[k][L2]);
-      X[k + 1][L2] = fma(-va.y, w, X[k + 1][L2]);
-    }
-    rv[L2] = r;
-    qv[L2] = q;
-  }
-  // (3) this warp's part of R row j, then hand it on and acknowledge x_j
-#pragma unroll
-  for (int L2 = 0; L2 < 2; ++L2) {
-    const int GS = pr_gslot(ROLE, L2);
-    if (GS < G) continue;
-    const int c = 32 * GS + lane;
-    if (c > j) Rj[c] = rv[L2] - qv[L2];
-  }
-  if constexpr (OWN) {
-    if (lane == jj) Rj[j] = bcur;
-    if (lane == 0 && tau_tile) tau_tile[j] = tau;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence_block();
-    st_release(verMine + j, t + 1);
-    st_release(ackMine, sq + 1);
-  }
-}
-
-template <int ROLE, int G>
-__device__ __forceinline__ void pair_segment(PairState& st, double (&X)[PAIR_HT][2], double* Rs,
-                                             int* verMine, int* pub, int* ackMine, int* ackOther,
-                                             double* buf, int n, int t, int seq0,
-                                             double* tau_tile) {
-  for (int jj = 0; jj < 31; ++jj) {
-    if (32 * G + jj >= n) return;
-    pair_step<ROLE, G, false>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, jj,
-                              tau_tile);
-  }
-  if (32 * G + 31 >= n) return;
-  pair_step<ROLE, G, true>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, 31,
-                           tau_tile);
-}
-
-// One chain tile for one role.  On return X holds this role's columns of V.
-template <int ROLE>
-__device__ __forceinline__ void pair_tile(double (&X)[PAIR_HT][2], double* Rs, int* verMine,
-                                          int* pub, int* ackMine, int* ackOther, double* buf,
-                                          int n, int t, int seq0, double* tau_tile) {
-  constexpr int HT = PAIR_HT;
-  const int lane = threadIdx.x & 31;
-  PairState st;
-  st.mysc[0] = 1.0;
-  st.mysc[1] = 1.0;
-  st.beta = 0.0;
-  if constexpr (ROLE == 0) {  // reflector 0 of the tile
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      s0 = fma(X[k][0], X[k][0], s0);
-      s1 = fma(X[k + 1][0], X[k + 1][0], s1);
-    }
-    const double sg = __shfl_sync(FULL, s0 + s1, 0);
-    while (ld_acquire(verMine) != t) { }
-    double beta, tau, scale;
-    house_lean(Rs[0], sg, beta, tau, scale);
-    while (ld_acquire(ackOther) < seq0 - 1) { }
-    double* vn = buf + (seq0 & 1) * PBUF;
-    if (lane == 0) {
-      st.mysc[0] = scale;
-#pragma unroll
-      for (int k = 0; k < HT; k += 2)
-        *reinterpret_cast<double2*>(vn + k) = make_double2(X[k][0], X[k + 1][0]);
-      vn[32] = tau;
-      vn[33] = scale;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      st_release(pub, seq0 + 1);
-    }
-    st.beta = beta;
-    pair_segment<0, 0>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    pair_segment<0, 1>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    pair_segment<0, 2>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    pair_segment<0, 3>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-  } else {
-    pair_segment<1, 0>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    pair_segment<1, 1>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    pair_segment<1, 2>(st, X, Rs, verMine, pub, ackMine, ackOther, buf, n, t, seq0, tau_tile);
-    __syncwarp();
-    if (lane == 0) st_release(ackMine, seq0 + 128);  // B has no columns right of 95
-  }
-#pragma unroll
-  for (int L = 0; L < 2; ++L)
-#pragma unroll
-    for (int k = 0; k < HT; ++k) X[k][L] *= st.mysc[L];
-}
-
-// ---------------------------------------------------------------------------
 // Ring tile: one warp applies the n reflectors of its triangle-on-rectangle
 // tile [R; X] (householder.py:297-332), R rows taken from / returned to Rs
 // (stride NP) under the version protocol ver[j] == t.  The broadcast vector
@@ -1039,198 +811,6 @@ __device__ __forceinline__ void ring_factor_tile(double (&X)[HW][NP / 32], doubl
 #ifdef TSQR_SPIN_PROBE
   if (lane == 0) atomicAdd(&g_spin_cycles[1], clock64() - tstart);
 #endif
-}
-
-// ---------------------------------------------------------------------------
-// Dual-chain ring (two leaves per CTA): every warp carries tile t of leaf 0
-// AND tile t of leaf 1 and runs both reflector chains in one instruction
-// stream, so the latency of one chain's norm / sqrt / reciprocal overlaps the
-// other chain's rank-1 updates.  Each leaf keeps its own ring (R rows stored
-// packed upper-triangular in shared memory, version counters, broadcast
-// buffer).  Packed row j starts at pk(j) = j*NP - j(j-1)/2; element (j, c),
-// c >= j, at pk(j) + c - j.
-// ---------------------------------------------------------------------------
-template <int NP>
-__host__ __device__ __forceinline__ int pk(int j) { return j * NP - (j * (j - 1)) / 2; }
-
-template <int NP, int HT, int C>
-struct Chains {
-  double X[C][HT][NP / 32];
-  double v[C][HT];
-  double p[C][NP / 32];
-  double mysc[C][NP / 32];
-  double beta[C], tau[C], scale[C];
-};
-
-// Per-chain buffers: chain c uses Rs0 + c*RSTR (packed R), ver0 + c*NP,
-// vb0 + c*VSTR and tau0 + c*tstr (tau0 may be null).
-#define CH_RS(c) (Rs0 + (c) * RSTR)
-#define CH_VER(c) (ver0 + (c) * NP)
-#define CH_VB(c) (vb0 + (c) * VSTR)
-template <int NP, int HT, int C, int RSTR, int VSTR, int s, int SN>
-__device__ __forceinline__ void ring_step_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
-                                            double* vb0, int n, int t, int jj, double* tau0,
-                                            int64_t tstr) {
-  constexpr int S = NP / 32;
-  const int lane = threadIdx.x & 31;
-  const int j = 32 * s + jj;
-  const int jn = j + 1;
-  const bool more = (SN < S) && (jn < n);
-  constexpr int SNc = (SN < S) ? SN : S - 1;
-  const int rj = pk<NP>(j) - j;  // element (j, c) at rj + c
-  double x0n[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    x0n[c] = 1.0;
-    if (more) {
-      while (ld_acquire(CH_VER(c) + jn) != t) { }
-      x0n[c] = CH_RS(c)[pk<NP>(jn)];
-    }
-  }
-  double sg[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    sg[c] = 0.0;
-    if (SN < S) {
-      const int col = 32 * SNc + lane;
-      const double r = (col >= j) ? CH_RS(c)[rj + col] : 0.0;
-      const bool act = (SNc > s) || (lane > jj);
-      const double qq = act ? q.tau[c] * fma(q.scale[c], q.p[c][SNc], r) : 0.0;
-      const double w = qq * q.scale[c];
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < HT; k += 2) {
-        q.X[c][k][SNc] = fma(-q.v[c][k], w, q.X[c][k][SNc]);
-        q.X[c][k + 1][SNc] = fma(-q.v[c][k + 1], w, q.X[c][k + 1][SNc]);
-        s0 = fma(q.X[c][k][SNc], q.X[c][k][SNc], s0);
-        s1 = fma(q.X[c][k + 1][SNc], q.X[c][k + 1][SNc], s1);
-      }
-      sg[c] = s0 + s1;
-      if (col > j) CH_RS(c)[rj + col] = r - qq;
-    }
-  }
-  double nbeta[C], ntau[C], nscale[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    sg[c] = __shfl_sync(FULL, sg[c], jn & 31);
-    house_lean(x0n[c], sg[c], nbeta[c], ntau[c], nscale[c]);
-  }
-#pragma unroll
-  for (int s2 = s; s2 < S; ++s2) {
-    if (s2 == SN) continue;
-    if (s2 == s && SN != s) continue;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const int col = 32 * s2 + lane;
-      const double r = (col >= j) ? CH_RS(c)[rj + col] : 0.0;
-      const bool act = (s2 > s) || (lane > jj);
-      const double qq = act ? q.tau[c] * fma(q.scale[c], q.p[c][s2], r) : 0.0;
-      const double w = qq * q.scale[c];
-#pragma unroll
-      for (int k = 0; k < HT; ++k) q.X[c][k][s2] = fma(-q.v[c][k], w, q.X[c][k][s2]);
-      if (col > j) CH_RS(c)[rj + col] = r - qq;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (lane == jj) CH_RS(c)[rj + j] = q.beta[c];
-    if (lane == 0 && tau0) tau0[c * tstr + j] = q.tau[c];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence_block();
-#pragma unroll
-    for (int c = 0; c < C; ++c) st_release(CH_VER(c) + j, t + 1);
-  }
-  if (!more) return;
-  if (lane == (jn & 31)) {
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      q.mysc[c][SNc] = nscale[c];
-#pragma unroll
-      for (int k = 0; k < HT; k += 2)
-        *reinterpret_cast<double2*>(CH_VB(c) + k) = make_double2(q.X[c][k][SNc], q.X[c][k + 1][SNc]);
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      const double2 t2 = *reinterpret_cast<const double2*>(CH_VB(c) + k);
-      q.v[c][k] = t2.x;
-      q.v[c][k + 1] = t2.y;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    raw_dots<NP, HT, SNc>(q.X[c], q.v[c], q.p[c]);
-    q.beta[c] = nbeta[c];
-    q.tau[c] = ntau[c];
-    q.scale[c] = nscale[c];
-  }
-}
-
-template <int NP, int HT, int C, int RSTR, int VSTR, int s>
-__device__ __forceinline__ void ring_slot_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
-                                            double* vb0, int n, int t, double* tau0, int64_t tstr) {
-  for (int jj = 0; jj < 31; ++jj) {
-    if (32 * s + jj >= n) return;
-    ring_step_c<NP, HT, C, RSTR, VSTR, s, s>(q, Rs0, ver0, vb0, n, t, jj, tau0, tstr);
-  }
-  if (32 * s + 31 >= n) return;
-  ring_step_c<NP, HT, C, RSTR, VSTR, s, s + 1>(q, Rs0, ver0, vb0, n, t, 31, tau0, tstr);
-}
-
-template <int NP, int HT, int C, int RSTR, int VSTR>
-__device__ __forceinline__ void ring_tile_c(Chains<NP, HT, C>& q, double* Rs0, int* ver0,
-                                            double* vb0, int n, int t, double* tau0, int64_t tstr) {
-  constexpr int S = NP / 32;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) q.mysc[c][s] = 1.0;
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      s0 = fma(q.X[c][k][0], q.X[c][k][0], s0);
-      s1 = fma(q.X[c][k + 1][0], q.X[c][k + 1][0], s1);
-    }
-    const double sg = __shfl_sync(FULL, s0 + s1, 0);
-    while (ld_acquire(CH_VER(c)) != t) { }
-    house_lean(CH_RS(c)[0], sg, q.beta[c], q.tau[c], q.scale[c]);
-    if (lane == 0) {
-      q.mysc[c][0] = q.scale[c];
-#pragma unroll
-      for (int k = 0; k < HT; k += 2)
-        *reinterpret_cast<double2*>(CH_VB(c) + k) = make_double2(q.X[c][k][0], q.X[c][k + 1][0]);
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-#pragma unroll
-    for (int k = 0; k < HT; k += 2) {
-      const double2 t2 = *reinterpret_cast<const double2*>(CH_VB(c) + k);
-      q.v[c][k] = t2.x;
-      q.v[c][k + 1] = t2.y;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < C; ++c) raw_dots<NP, HT, 0>(q.X[c], q.v[c], q.p[c]);
-  ring_slot_c<NP, HT, C, RSTR, VSTR, 0>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
-  if constexpr (S > 1) ring_slot_c<NP, HT, C, RSTR, VSTR, 1>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
-  if constexpr (S > 2) ring_slot_c<NP, HT, C, RSTR, VSTR, 2>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
-  if constexpr (S > 3) ring_slot_c<NP, HT, C, RSTR, VSTR, 3>(q, Rs0, ver0, vb0, n, t, tau0, tstr);
-#pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-#pragma unroll
-      for (int k = 0; k < HT; ++k) q.X[c][k][s] *= q.mysc[c][s];
 }
 
 // ---------------------------------------------------------------------------

@@ -48,9 +48,8 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
 static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
-static int g_narrow = 1;
+static int g_narrow = 1;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
-static int g_dual = 1;  // CAQR_TUNE_DUAL: two-leaf chain kernel for NP = 128, HT = 8  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -159,182 +158,6 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   if (bad && flag) atomicOr(flag, 1);
 }
 
-// ---------------------------------------------------------------------------
-// Dual-leaf chain kernel: CTA b runs the chains of leaves 2b and 2b+1 with
-// every warp carrying one tile of each (ring_tile_c, C = 2).  A CTA whose two
-// leaves have different tile counts (the ragged last leaf) or only one leaf
-// falls back to one chain per warp.
-// ---------------------------------------------------------------------------
-constexpr int DUAL_WARPS = 8;
-template <int NP, int HT>
-struct DualSmem {
-  static constexpr size_t bytes =
-      sizeof(double) * (2 * (size_t)(NP * (NP + 1) / 2) + 2 * DUAL_WARPS * HT) + sizeof(int) * 2 * NP;
-};
-
-template <int NP, int HT>
-__global__ void __launch_bounds__(DUAL_WARPS * 32, 1)
-k_leaf_chain2(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
-  constexpr int S = NP / 32, H0 = WARPS * Geo<NP>::HD, NT = DUAL_WARPS * 32;
-  constexpr int PKN = NP * (NP + 1) / 2;
-  constexpr int VSTR = DUAL_WARPS * HT;
-  extern __shared__ __align__(16) double sm[];
-  const int w = threadIdx.x >> 5;
-  bool bad = false;
-  const int L0 = 2 * (int)blockIdx.x;
-  const bool two = (L0 + 1 < P);
-  const int64_t r00 = (int64_t)L0 * base;
-  const int64_t b0 = (L0 == P - 1) ? m - r00 : base;
-  const int64_t r01 = r00 + base;
-  const int64_t b1 = two ? ((L0 + 1 == P - 1) ? m - r01 : base) : 0;
-  const int T0 = b0 > H0 ? (int)((b0 - H0 + HT - 1) / HT) : 0;
-  const int T1 = b1 > H0 ? (int)((b1 - H0 + HT - 1) / HT) : 0;
-  double* Rs0 = sm;
-  double* vball = sm + 2 * PKN;
-  int* ver0 = reinterpret_cast<int*>(vball + 2 * VSTR);
-  double* vb0 = vball + w * HT;
-  for (int c = 0; c < 2; ++c) {
-    if ((c == 0 ? T0 : T1) == 0) continue;
-    const double* Rl = Rio + (int64_t)(L0 + c) * n * n;
-    double* Rc = Rs0 + c * PKN;
-    for (int idx = threadIdx.x; idx < NP * NP; idx += NT) {
-      const int r = idx / NP, col = idx - r * NP;
-      if (col >= r) Rc[pk<NP>(r) + col - r] = (r < n && col < n) ? Rl[r * n + col] : 0.0;
-    }
-  }
-  for (int j = threadIdx.x; j < 2 * NP; j += NT) ver0[j] = 0;
-  __syncthreads();
-  double* tl0 = tau ? tau + (int64_t)L0 * tau_stride : nullptr;
-  if (T0 > 0 && T0 == T1) {
-    Chains<NP, HT, 2> q;
-    for (int t = w; t < T0; t += DUAL_WARPS) {
-      const int64_t row0 = r00 + H0 + (int64_t)t * HT, row1 = r01 + H0 + (int64_t)t * HT;
-      const int v0 = (int)min64((int64_t)HT, r00 + b0 - row0);
-      const int v1 = (int)min64((int64_t)HT, r01 + b1 - row1);
-      load_rows<HT, S>(q.X[0], A + row0 * lda, lda, v0, n, 0, bad);
-      load_rows<HT, S>(q.X[1], A + row1 * lda, lda, v1, n, 0, bad);
-      ring_tile_c<NP, HT, 2, PKN, VSTR>(q, Rs0, ver0, vb0, n, t,
-                                        tl0 ? tl0 + (int64_t)(t + 1) * n : nullptr, tau_stride);
-      if (Y) {
-        store_rows<HT, S>(q.X[0], Y + row0 * ldy, ldy, v0, n, 0);
-        store_rows<HT, S>(q.X[1], Y + row1 * ldy, ldy, v1, n, 0);
-      }
-    }
-  } else {
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      const int Tc = c == 0 ? T0 : T1;
-      if (Tc == 0) continue;
-      const int64_t rc0 = c == 0 ? r00 : r01, bc = c == 0 ? b0 : b1;
-      Chains<NP, HT, 1> q;
-      double* tlc = tau ? tau + (int64_t)(L0 + c) * tau_stride : nullptr;
-      for (int t = w; t < Tc; t += DUAL_WARPS) {
-        const int64_t row = rc0 + H0 + (int64_t)t * HT;
-        const int valid = (int)min64((int64_t)HT, rc0 + bc - row);
-        load_rows<HT, S>(q.X[0], A + row * lda, lda, valid, n, 0, bad);
-        ring_tile_c<NP, HT, 1, PKN, VSTR>(q, Rs0 + c * PKN, ver0 + c * NP, vb0 + c * VSTR, n, t,
-                                          tlc ? tlc + (int64_t)(t + 1) * n : nullptr, 0);
-        if (Y) store_rows<HT, S>(q.X[0], Y + row * ldy, ldy, valid, n, 0);
-      }
-    }
-  }
-  __syncthreads();
-  for (int c = 0; c < 2; ++c) {
-    if ((c == 0 ? T0 : T1) == 0) continue;
-    double* Rl = Rio + (int64_t)(L0 + c) * n * n;
-    const double* Rc = Rs0 + c * PKN;
-    for (int idx = threadIdx.x; idx < n * n; idx += NT) {
-      const int r = idx / n, col = idx - r * n;
-      Rl[idx] = (col >= r) ? Rc[pk<NP>(r) + col - r] : 0.0;
-    }
-  }
-  if (bad && flag) atomicOr(flag, 1);
-}
-
-// ---------------------------------------------------------------------------
-// Pair-ring chain kernel (padded width 128, chain tile height 32): 8 warps =
-// 4 pairs; pair p runs tiles p, p+4, ...; warp 2p is role A (global column
-// slots 0 and 3), warp 2p+1 role B (slots 1 and 2).
-// ---------------------------------------------------------------------------
-struct PairSmem {
-  static constexpr size_t bytes = sizeof(double) * ((size_t)128 * 128 + 4 * 2 * PBUF) +
-                                  sizeof(int) * (2 * 128 + 4 * 4);
-};
-
-__global__ void __launch_bounds__(256, 1)
-k_leaf_chain_pair(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-                  double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag) {
-  constexpr int HT = PAIR_HT, H0 = WARPS * Geo<128>::HD;
-  extern __shared__ __align__(16) double sm[];
-  double* Rs = sm;
-  double* bufs = Rs + 128 * 128;
-  int* verA = reinterpret_cast<int*>(bufs + 4 * 2 * PBUF);
-  int* verB = verA + 128;
-  int* sync = verB + 128;  // per pair: pub, ackA, ackB, pad
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int pair = w >> 1, role = w & 1;
-  bool bad = false;
-  const int leaf = blockIdx.x;
-  const int64_t r0 = (int64_t)leaf * base;
-  const int64_t b = (leaf == P - 1) ? m - r0 : base;
-  const int64_t rest = b - H0;
-  const int T = rest > 0 ? (int)((rest + HT - 1) / HT) : 0;
-  if (T == 0) return;
-  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
-  double* Rl = Rio + (int64_t)leaf * n * n;
-  for (int idx = threadIdx.x; idx < 128 * 128; idx += 256) {
-    const int r = idx / 128, c = idx - r * 128;
-    Rs[idx] = (r < n && c < n && c >= r) ? Rl[r * n + c] : 0.0;
-  }
-  for (int j = threadIdx.x; j < 256; j += 256) verA[j] = 0;  // verA and verB
-  if (threadIdx.x < 16) sync[threadIdx.x] = 0;  // pub = 0; ack = 0: "consumed up to seq -1"
-  __syncthreads();
-  int* pub = sync + 4 * pair;
-  int* ackA = pub + 1;
-  int* ackB = pub + 2;
-  double* buf = bufs + pair * 2 * PBUF;
-  double X[HT][2];
-  int seq0 = 0;
-  for (int t = pair; t < T; t += 4, seq0 += 128) {
-    const int64_t row = r0 + H0 + (int64_t)t * HT;
-    const int valid = (int)min64((int64_t)HT, r0 + b - row);
-    const double* src = A + row * lda;
-#pragma unroll
-    for (int k = 0; k < HT; ++k) {
-#pragma unroll
-      for (int L = 0; L < 2; ++L) {
-        const int c = 32 * pr_gslot(0, L) + lane + (role ? 32 * (pr_gslot(1, L) - pr_gslot(0, L)) : 0);
-        double x = 0.0;
-        if (k < valid && c < n) x = __ldg(src + (int64_t)k * lda + c);
-        bad |= !isfinite(x);
-        X[k][L] = x;
-      }
-    }
-    double* tt = tl ? tl + (int64_t)(t + 1) * n : nullptr;
-    if (role == 0)
-      pair_tile<0>(X, Rs, verA, pub, ackA, ackB, buf, n, t, seq0, tt);
-    else
-      pair_tile<1>(X, Rs, verB, pub, ackB, ackA, buf, n, t, seq0, tt);
-    if (Y) {
-#pragma unroll
-      for (int k = 0; k < HT; ++k) {
-        if (k >= valid) continue;
-#pragma unroll
-        for (int L = 0; L < 2; ++L) {
-          const int c = 32 * pr_gslot(0, L) + lane + (role ? 32 * (pr_gslot(1, L) - pr_gslot(0, L)) : 0);
-          if (c < n) Y[(row + k) * ldy + c] = X[k][L];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * n; idx += 256) {
-    const int r = idx / n, c = idx - r * n;
-    Rl[idx] = (c >= r) ? Rs[r * 128 + c] : 0.0;
-  }
-  if (bad && flag) atomicOr(flag, 1);
-}
 
 // ---------------------------------------------------------------------------
 // Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
@@ -1118,16 +941,6 @@ int tsqr_f64_geometry(int64_t n, int64_t* np, int64_t* h0, int64_t* ht) {
   return CAQR_OK;
 }
 
-static int launch_dual(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, int64_t base,
-                       double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* R,
-                       int* flag, cudaStream_t st) {
-  int rc = prep(k_leaf_chain2<128, 8>, DualSmem<128, 8>::bytes);
-  if (rc) return rc;
-  k_leaf_chain2<128, 8><<<(int)((P + 1) / 2), DUAL_WARPS * 32, DualSmem<128, 8>::bytes, st>>>(
-      A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag);
-  return CAQR_OK;
-}
-
 // Leaves of `base` rows, the last one taking the remainder (m - (P-1) base >= base).
 static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
                             int64_t base, double* Y, int64_t ldy, double* tau, int64_t tau_stride,
@@ -1155,8 +968,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   }
 #define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
-    const bool pair = (NPV == 128 && g_ht[np_index(NPV)] == 32);                                \
-    const bool zs = !Y && g_zstart && !pair;                                                    \
+    const bool zs = !Y && g_zstart;                                                             \
     int rc = 0;                                                                                 \
     if (!zs) {                                                                                  \
       rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                      \
@@ -1165,12 +977,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
     if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                              \
-      if (pair) {                                                                               \
-        rc = prep(k_leaf_chain_pair, PairSmem::bytes);                                          \
-        if (rc) return rc;                                                                      \
-        k_leaf_chain_pair<<<grid, 256, PairSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
-                                                              Y, ldy, tau, tau_stride, R, flag);\
-      } else if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)     \
+      if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)           \
     }                                                                                           \
     break;                                                                                      \
   }
@@ -1370,7 +1177,6 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     LA_CASE(64, 2, 16, 32)
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
-      else if (g_ht[2] == 32) LA_LAUNCH(128, 2, 32)
       else LA_LAUNCH(128, 4, 16)
       break;
     }
@@ -1439,13 +1245,9 @@ int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
     const int a = 16, b = i == 2 ? 24 : 32;
-    if (value != a && value != b && !(i == 2 && value == 32))
+    if (value != a && value != b)
       return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
-    return CAQR_OK;
-  }
-  if (key == CAQR_TUNE_DUAL) {
-    g_dual = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_NARROW) {

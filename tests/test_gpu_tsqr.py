@@ -276,3 +276,29 @@ def test_streamed_rejects_nonfinite():
     A[33333, 3] = np.inf
     with pytest.raises(ValueError):
         tsqr(A, leaf_rows=1000)
+
+
+def test_tuning_variants_keep_parity():
+    """The supported tuning knobs (CAQR_TUNE_CHAIN_HT_128 = 24, CAQR_TUNE_ZSTART
+    = 0) change the tiling / first tile only: parity holds for each."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import tsqr
+
+    A = philox(31).standard_normal((20000, 100))
+    Rref = np.linalg.qr(A, mode="r")
+    scale = np.linalg.norm(A, 2)
+    try:
+        _lib.tune(_lib.TUNE_CHAIN_HT[128], 24)
+        R, Q = tsqr(A, leaf_rows=5000, q="explicit")
+        assert oracle.r_diff(R, Rref, scale) <= 1000 * EPS
+        assert oracle.orthogonality(Q) <= 10 * 100 * EPS
+        assert oracle.residual(A, Q, R) <= 10 * 100 * EPS
+    finally:
+        _lib.tune(_lib.TUNE_CHAIN_HT[128], 16)
+    try:
+        _lib.tune(_lib.TUNE_ZSTART, 0)
+        R0 = tsqr(A, leaf_rows=5000)  # dense first tile, ring tree
+        assert oracle.r_diff(R0, Rref, scale) <= 1000 * EPS
+    finally:
+        _lib.tune(_lib.TUNE_ZSTART, 1)
+    assert oracle.r_diff(tsqr(A, leaf_rows=5000), Rref, scale) <= 1000 * EPS
