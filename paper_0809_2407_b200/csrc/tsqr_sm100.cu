@@ -48,7 +48,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
 static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
-static int g_narrow = 1;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only
+static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -162,25 +162,56 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
 // ---------------------------------------------------------------------------
 // Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
 // Lane l owns an 8x8 upper-triangular R in registers and runs the flat chain
-// of triangle-on-rectangle steps (Alg. 2) over its own rows: K rows per step,
-// rows [q*32K + l*K, +K) of round q (256 contiguous bytes per lane per round,
-// the next round prefetched into registers).  The 32 lane R factors are then
+// of triangle-on-rectangle steps (Alg. 2) over its own rows: K = 4 rows per
+// step, rows q*128 + 32k + l of round q (one round = 128 contiguous rows =
+// 8 KB per warp).  Rounds are prefetched either one ahead into registers or,
+// for contiguous 8-column rows, NARROW_STAGES ahead by cp.async into padded
+// shared-memory stages (80-byte rows: conflict-free LDS.128).  The 32 lane R factors are then
 // combined in-warp by the same step applied to the partner lane's R (shuffled
 // in two 4-row halves), a binary tree over lanes.  R-only: the chains start
 // from R = 0, which gives the QR of [0; A] -- the same R, no stored Q.
 // ---------------------------------------------------------------------------
 constexpr int NARROW_K = 4;
 constexpr int NARROW_WARPS = 8;
+// cp.async-staged variant: K rows per lane per round, W warps (leaves) per
+// CTA, two shared-memory stages per warp.  K = 4: 80-byte padded rows filled
+// by 16-byte copies, read by LDS.128 (conflict-free), 160 KB.  (K = 6 / 8 with
+// 72-byte rows and 8-byte copies fit in shared memory, but ptxas demotes R
+// and B -- 84 / 100 doubles -- to local memory: 8x slower; not instantiated.)
+template <int K>
+struct NarrowPipe {
+  static constexpr int W = 8;
+  static constexpr int STAGES = 2;
+  static constexpr int G = (K == 4) ? 16 : 8;     // copy granule (bytes)
+  static constexpr int ROW_B = (K == 4) ? 80 : 72;
+  static constexpr int STAGE_B = 32 * K * ROW_B;
+  static constexpr size_t SMEM = (size_t)W * STAGES * STAGE_B;
+};
+
+template <int G>
+__device__ __forceinline__ void cp_async(unsigned dst, const void* src, unsigned bytes) {
+  if constexpr (G == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 // Packed upper-triangular 8x8 R in registers: element (i, c), c >= i.
 __host__ __device__ constexpr int pk8(int i, int c) { return i * 8 - (i * (i - 1)) / 2 + (c - i); }
 
 // One triangle-on-rectangle step [R; B] (householder.py:297-332) on K rows.
-template <int K>
+// N8: n == 8 known at compile time -- the whole step is one basic block, so
+// the scalars of column j+1 can be scheduled under column j's updates.
+template <int K, bool N8 = false>
 __device__ __forceinline__ void narrow_step(double (&R)[36], double (&B)[K][8], int n) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    if (j >= n) break;
+    if (!N8 && j >= n) break;
     double sg = 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) sg = fma(B[k][j], B[k][j], sg);
@@ -225,12 +256,12 @@ __device__ __forceinline__ void narrow_load(double (&Bt)[K][8], const double* __
   }
 }
 
-__global__ void __launch_bounds__(NARROW_WARPS * 32, 1)
+template <bool PIPE, int K = NARROW_K, int W = NARROW_WARPS>
+__global__ void __launch_bounds__(W * 32, 1)
 k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
               double* Rout, int* flag, int* tickets) {
-  constexpr int K = NARROW_K;
   const int lane = threadIdx.x & 31;
-  const int leaf = blockIdx.x * NARROW_WARPS + (threadIdx.x >> 5);
+  const int leaf = blockIdx.x * W + (threadIdx.x >> 5);
   if (leaf >= P) return;
   const int64_t r0 = (int64_t)leaf * base;
   const int64_t b = (leaf == P - 1) ? m - r0 : base;
@@ -238,15 +269,69 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
 #pragma unroll
   for (int i = 0; i < 36; ++i) R[i] = 0.0;
   const int64_t rounds = (b + 32 * K - 1) / (32 * K);
-  // double-buffered prefetch without register copies: two rounds per trip
-  double B0[K][8], B1[K][8];
-  if (rounds > 0) narrow_load<K>(B0, A, lda, r0, b, 0, n, lane);
-  for (int64_t q = 0; q < rounds; q += 2) {
-    if (q + 1 < rounds) narrow_load<K>(B1, A, lda, r0, b, q + 1, n, lane);
-    narrow_step<K>(R, B0, n);
-    if (q + 1 >= rounds) break;
-    if (q + 2 < rounds) narrow_load<K>(B0, A, lda, r0, b, q + 2, n, lane);
-    narrow_step<K>(R, B1, n);
+  if constexpr (PIPE) {
+    // n == 8, lda == 8: round q is rows [q*32K, q*32K + 32K) of the leaf, one
+    // contiguous run; lane l copies granules l, l + 32, ... of it
+    using NP_ = NarrowPipe<K>;
+    constexpr int GPR = 64 / NP_::G;                 // granules per row
+    extern __shared__ __align__(16) double nsm[];
+    char* stage0 = reinterpret_cast<char*>(nsm) + (threadIdx.x >> 5) * NP_::STAGES * NP_::STAGE_B;
+    const unsigned s0 = (unsigned)__cvta_generic_to_shared(stage0);
+    const char* Al = reinterpret_cast<const char*>(A + r0 * 8);
+    auto issue = [&](int64_t q) {
+      const unsigned st = s0 + (unsigned)(q % NP_::STAGES) * NP_::STAGE_B;
+      const int64_t left = b - q * 32 * K;
+      const char* g = Al + q * 32 * K * 64;
+#pragma unroll
+      for (int i = 0; i < K * GPR; ++i) {
+        const int x = lane + 32 * i, row = x / GPR, part = x % GPR;
+        const bool ok = row < left;
+        cp_async<NP_::G>(st + row * NP_::ROW_B + part * NP_::G,
+                         ok ? (const void*)(g + row * 64 + part * NP_::G) : (const void*)A,
+                         ok ? (unsigned)NP_::G : 0u);
+      }
+    };
+#pragma unroll
+    for (int s2 = 0; s2 < NP_::STAGES; ++s2) {
+      if (s2 < rounds) issue(s2);
+      cp_async_commit();
+    }
+    for (int64_t q = 0; q < rounds; ++q) {
+      cp_async_wait<NP_::STAGES - 1>();  // round q has landed (one group per round)
+      __syncwarp();
+      const char* st = stage0 + (q % NP_::STAGES) * NP_::STAGE_B;
+      double B[K][8];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const char* rp = st + (32 * k + lane) * NP_::ROW_B;
+        if constexpr (NP_::G == 16) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double2 t = reinterpret_cast<const double2*>(rp)[c];
+            B[k][2 * c] = t.x;
+            B[k][2 * c + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) B[k][c] = reinterpret_cast<const double*>(rp)[c];
+        }
+      }
+      __syncwarp();  // every lane has read the stage before it is refilled
+      if (q + NP_::STAGES < rounds) issue(q + NP_::STAGES);
+      cp_async_commit();
+      narrow_step<K, true>(R, B, 8);
+    }
+  } else {
+    // double-buffered prefetch without register copies: two rounds per trip
+    double B0[K][8], B1[K][8];
+    if (rounds > 0) narrow_load<K>(B0, A, lda, r0, b, 0, n, lane);
+    for (int64_t q = 0; q < rounds; q += 2) {
+      if (q + 1 < rounds) narrow_load<K>(B1, A, lda, r0, b, q + 1, n, lane);
+      narrow_step<K>(R, B0, n);
+      if (q + 1 >= rounds) break;
+      if (q + 2 < rounds) narrow_load<K>(B0, A, lda, r0, b, q + 2, n, lane);
+      narrow_step<K>(R, B1, n);
+    }
   }
   // in-warp binary tree over the lane R factors (partner rows in two halves)
 #pragma unroll
@@ -294,20 +379,18 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
     const int t = atomicAdd(tickets + (int64_t)(k - 1) * P + p, 1);
     if (t == 0) return;  // first arrival: the sibling finishes this node
     __threadfence();
+    // receiver (lower index) on top: [R_p; R_sib].  Both operands were stored
+    // by put(); the top one is (re)loaded into R only when it is the sibling's,
+    // the bottom one streams from memory in two 4-row halves (keeps the live
+    // set at R + one half so the main loop's arrays stay in registers).
     const int other = (node == p) ? sib_hi : p;
-    const double* Ro = Rout + (int64_t)other * n * n;
-    double Ro8[36];
+    const double* Rbot = Rout + (int64_t)((node == p) ? other : node) * n * n;
+    if (node != p) {
+      const double* Rtop = Rout + (int64_t)other * n * n;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int c = i; c < 8; ++c) Ro8[pk8(i, c)] = (i < n && c < n) ? __ldcg(Ro + i * n + c) : 0.0;
-    if (node != p) {  // receiver (lower index) goes on top
-#pragma unroll
-      for (int i = 0; i < 36; ++i) {
-        const double tmp = R[i];
-        R[i] = Ro8[i];
-        Ro8[i] = tmp;
-      }
+        for (int c = i; c < 8; ++c) R[pk8(i, c)] = (i < n && c < n) ? __ldcg(Rtop + i * n + c) : 0.0;
     }
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -317,7 +400,7 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int i = 4 * half + kk;
-          Bs[kk][c] = (c >= i) ? Ro8[pk8(i, c < i ? i : c)] : 0.0;
+          Bs[kk][c] = (c >= i && i < n && c < n) ? __ldcg(Rbot + i * n + c) : 0.0;
         }
       narrow_step<4>(R, Bs, n);
     }
@@ -941,6 +1024,28 @@ int tsqr_f64_geometry(int64_t n, int64_t* np, int64_t* h0, int64_t* ht) {
   return CAQR_OK;
 }
 
+// Narrow leaves: the cp.async-staged kernel for contiguous 8-column rows
+// (CAQR_TUNE_NARROW = 2, default), else the register-prefetch kernel.
+static int launch_narrow(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
+                         int64_t base, double* R, int* flag, int* tickets, cudaStream_t st) {
+#define NARROW_PIPE(KK)                                                                       \
+  {                                                                                           \
+    using NP_ = NarrowPipe<KK>;                                                               \
+    int rc = prep(k_leaf_narrow<true, KK, NP_::W>, NP_::SMEM);                                \
+    if (rc) return rc;                                                                        \
+    k_leaf_narrow<true, KK, NP_::W><<<(int)((P + NP_::W - 1) / NP_::W), NP_::W * 32, NP_::SMEM, \
+                                      st>>>(A, lda, m, (int)n, (int)P, base, R, flag, tickets); \
+  }
+  if (g_narrow >= 2 && n == 8 && lda == 8) {
+    NARROW_PIPE(4)
+  } else {
+    k_leaf_narrow<false><<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
+        A, lda, m, (int)n, (int)P, base, R, flag, tickets);
+  }
+#undef NARROW_PIPE
+  return check_launch("k_leaf_narrow");
+}
+
 // Leaves of `base` rows, the last one taking the remainder (m - (P-1) base >= base).
 static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
                             int64_t base, double* Y, int64_t ldy, double* tau, int64_t tau_stride,
@@ -954,9 +1059,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)P;
   if (n <= 8 && !Y && g_narrow) {
-    k_leaf_narrow<<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
-        A, lda, m, (int)n, (int)P, base, R, flag, nullptr);
-    return check_launch("k_leaf_narrow");
+    return launch_narrow(A, lda, m, n, P, base, R, flag, nullptr, st);
   }
 #define CHAIN_LAUNCH(NPV, HTV)                                                                  \
   {                                                                                             \
@@ -1007,9 +1110,7 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
   if (n <= 8 && g_narrow) {
     if (P > 1 && cudaMemsetAsync(tickets, 0, sizeof(int) * (size_t)levels * P, st) != cudaSuccess)
       return check_launch("cudaMemsetAsync");
-    k_leaf_narrow<<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
-        A, lda, m, (int)n, (int)P, base, Rslots, flag, P > 1 ? tickets : nullptr);
-    return check_launch("k_leaf_narrow");
+    return launch_narrow(A, lda, m, n, P, base, Rslots, flag, P > 1 ? tickets : nullptr, st);
   }
   int rc = leaf_factor_impl(A, lda, m, n, P, base, nullptr, 0, nullptr, 0, Rslots, flag, stream);
   if (rc) return rc;
@@ -1251,7 +1352,8 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_NARROW) {
-    g_narrow = value ? 1 : 0;
+    if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW takes 0, 1 or 2");
+    g_narrow = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_ZSTART) {
