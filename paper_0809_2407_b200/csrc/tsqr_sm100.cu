@@ -47,7 +47,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // ---------------------------------------------------------------------------
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
-static int g_ht[3] = {16, 32, 16};  // NP = 32, 64, 128 (measured best)
+static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
@@ -143,7 +143,7 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
     if constexpr (NP == 128 && HW > 16)
       ring_factor_tile_vs<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
                                   tl ? tl + (int64_t)(t + 1) * n : nullptr);
-    else if constexpr (NP == 128 && HW == 16)  // two broadcast vectors fit in 255 registers
+    else if constexpr ((NP == 128 && HW == 16) || (NP == 64 && HW == 24))  // two vectors fit
       ring_factor_tile3<NP, HW>(X, Rs, ver, n, t, tl ? tl + (int64_t)(t + 1) * n : nullptr);
     else
       ring_factor_tile<NP, HW>(X, Rs, ver, vbuf + w * 2 * HW, n, t,
@@ -1080,7 +1080,9 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
     if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                              \
-      if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA) else CHAIN_LAUNCH(NPV, HB)           \
+      if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA)                                      \
+      else if (NPV == 64 && g_ht[1] == 24) CHAIN_LAUNCH(64, 24)                                 \
+      else CHAIN_LAUNCH(NPV, HB)                                                                \
     }                                                                                           \
     break;                                                                                      \
   }
@@ -1275,7 +1277,12 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
   }
   switch (p) {
     LA_CASE(32, 1, 16, 32)
-    LA_CASE(64, 2, 16, 32)
+    case 64: {
+      if (g_ht[1] == 16) LA_LAUNCH(64, 2, 16)
+      else if (g_ht[1] == 24) LA_LAUNCH(64, 2, 24)
+      else LA_LAUNCH(64, 2, 32)
+      break;
+    }
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
       else LA_LAUNCH(128, 4, 16)
@@ -1346,7 +1353,7 @@ int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
     const int a = 16, b = i == 2 ? 24 : 32;
-    if (value != a && value != b)
+    if (value != a && value != b && !(i == 1 && value == 24))
       return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
     return CAQR_OK;
