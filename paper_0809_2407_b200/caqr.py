@@ -92,6 +92,8 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     lib = _lib.load()
     if layout is not None:
         b = layout.b
+        if layout.Pr * layout.Pc > 1:
+            return _caqr_on_grid(A, layout, leaf_rows, device)
     At, host = to_device(A, device)
     m, n = At.shape
     if m < n:
@@ -219,6 +221,34 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     if counter is not None:
         counter.add(2 * m * n * n - (2 * n ** 3) // 3)
     return CaqrResult(W=W, panels=panels, m=m, n=n, b=b, host=host, launches=nlaunch[0])
+
+
+_GRIDS: dict = {}
+
+
+def _caqr_on_grid(A, layout: BlockCyclicLayout, leaf_rows: int, device):
+    """Algorithm 3 on the Pr x Pc process grid of the initialised
+    torch.distributed job (one rank per GPU, world = Pr * Pc); every rank
+    passes the same global A and keeps its own blocks (grid.py)."""
+    import torch.distributed as dist
+
+    from .executor import ExecutorError
+    from .grid import GpuBackend, caqr_grid, gather_R as grid_gather_R, make_grid, scatter_local
+
+    if not dist.is_initialized() or dist.get_world_size() != layout.Pr * layout.Pc:
+        raise ExecutorError(f"a {layout.Pr}x{layout.Pc} layout needs torch.distributed initialised "
+                            f"with {layout.Pr * layout.Pc} ranks (one per GPU)")
+    At, host = to_device(A, device)
+    if (layout.m, layout.n) != tuple(At.shape):
+        raise DimensionError("layout does not match A")
+    key = (layout.m, layout.n, layout.b, layout.Pr, layout.Pc)
+    grid = _GRIDS.get(key)
+    if grid is None:  # every rank reaches this call in the same order (collective)
+        grid = _GRIDS[key] = make_grid(layout)
+    res = caqr_grid(scatter_local(At, grid), grid, GpuBackend(leaf_rows=leaf_rows))
+    R = grid_gather_R(res)
+    res.R = None if R is None else _out(R, host)
+    return res
 
 
 def gather_R(result: CaqrResult):

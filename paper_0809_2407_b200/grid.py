@@ -118,6 +118,7 @@ class GridCaqrResult:
     panels: dict = field(default_factory=dict)   # j -> (local factor, cross nodes) on ranks that hold them
     recorder: object = None
     broadcast_words: int = 0
+    R: object = None             # gathered R on rank 0 (set by caqr.caqr_factor)
 
 
 class GpuBackend:

@@ -220,3 +220,15 @@ def test_split_leaves_wave_fill():
     assert split_leaves(1 << 21, 128, 256, S, fill=True) == 4         # C3 per GPU at 8 GPUs
     assert split_leaves(1 << 24, 8, 1024, S) == 1                     # C4 per GPU at 8 GPUs
     assert split_leaves(4096, 64, 1, S) == 8                          # chains stay >= 512 rows
+
+
+def test_caqr_grid_layout_needs_a_distributed_job():
+    """SPEC caqr_factor(A, layout) with Pr x Pc > 1 runs Algorithm 3 across
+    ranks; without a matching torch.distributed job it fails loudly."""
+    from paper_0809_2407_b200.caqr import caqr_factor
+    from paper_0809_2407_b200.core import BlockCyclicLayout
+    from paper_0809_2407_b200.executor import ExecutorError
+
+    A = np.zeros((256, 128))
+    with pytest.raises(ExecutorError):
+        caqr_factor(A, BlockCyclicLayout(256, 128, 64, 2, 1))
