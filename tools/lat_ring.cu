@@ -10,7 +10,7 @@ k_chain_rw(const double* __restrict__ A, int64_t lda, int n, int64_t rows, doubl
   extern __shared__ __align__(16) double sm[];
   double* Rs = sm;
   double* vbuf = Rs + NP * NP;
-  int* ver = reinterpret_cast<int*>(vbuf + RW * HT);
+  int* ver = reinterpret_cast<int*>(vbuf + RW * 2 * HT);
   const int w = threadIdx.x >> 5;
   for (int idx = threadIdx.x; idx < NP * NP; idx += RW * 32) Rs[idx] = (idx / NP == idx % NP) ? 1.0 : 0.0;
   for (int j = threadIdx.x; j < NP; j += RW * 32) ver[j] = 0;
@@ -24,32 +24,43 @@ k_chain_rw(const double* __restrict__ A, int64_t lda, int n, int64_t rows, doubl
 #ifdef RING3
     ring_factor_tile3<NP, HT>(X, Rs, ver, n, t, nullptr);
 #else
-    ring_factor_tile<NP, HT>(X, Rs, ver, vbuf + w * HT, n, t, nullptr);
+#ifdef RING3
+    ring_factor_tile3<NP, HT>(X, Rs, ver, n, t, nullptr);
+#else
+    ring_factor_tile<NP, HT>(X, Rs, ver, vbuf + w * 2 * HT, n, t, nullptr);
+#endif
 #endif
   }
   __syncthreads();
   if (threadIdx.x == 0) Rio[blockIdx.x] = Rs[NP * NP - 1] + (bad ? 1.0 : 0.0);
 }
+#ifndef HTV
+#define HTV 16
+#endif
 template <int RW>
 void run(const double* A, double* R, int64_t rows) {
-  const size_t sm = sizeof(double) * (128 * 128 + RW * 16) + 4 * 128;
-  cudaFuncSetAttribute(k_chain_rw<128, 16, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const size_t sm = sizeof(double) * (128 * 128 + RW * 2 * HTV) + 4 * 128;
+  cudaFuncSetAttribute(k_chain_rw<128, HTV, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  k_chain_rw<128, 16, RW><<<148, RW * 32, sm>>>(A, 128, 128, rows, R);
+  k_chain_rw<128, HTV, RW><<<148, RW * 32, sm>>>(A, 128, 128, rows, R);
   cudaEventRecord(e0);
-  k_chain_rw<128, 16, RW><<<148, RW * 32, sm>>>(A, 128, 128, rows, R);
+  k_chain_rw<128, HTV, RW><<<148, RW * 32, sm>>>(A, 128, 128, rows, R);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  const double cols = (double)(rows / 16) * 128 / RW;  // column steps per warp
-  printf("warps=%d: %.3f ms, %.0f cycles per column step per warp (@1.92GHz), err=%s\n", RW, ms,
-         ms * 1e-3 * 1.92e9 / cols, cudaGetErrorString(cudaGetLastError()));
+  const double cols = (double)(rows / HTV) * 128 / RW;  // column steps per warp
+  printf("HT=%d warps=%d: %.3f ms (%.1f rows/us/SM), %.0f cycles per column step per warp, err=%s\n",
+         HTV, RW, ms, rows / (ms * 1e3), ms * 1e-3 * 1.92e9 / cols, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
-  const int64_t rows = 2048;
+  const int64_t rows = 6144;
   const int64_t m = 148 * rows;
   std::vector<double> h(m * 128); std::mt19937_64 g(1); std::normal_distribution<double> d;
   for (auto& x : h) x = d(g);
   double *A, *R; cudaMalloc(&A, m * 128 * 8); cudaMalloc(&R, 148 * 8);
   cudaMemcpy(A, h.data(), m * 128 * 8, cudaMemcpyHostToDevice);
+#ifdef ONLY_RW
+  run<ONLY_RW>(A, R, rows);
+#else
   run<1>(A, R, rows); run<2>(A, R, rows); run<4>(A, R, rows); run<8>(A, R, rows);
+#endif
 }
