@@ -749,11 +749,17 @@ k_tree_apply(const double* __restrict__ Ynode, const double* __restrict__ taunod
 // S (nullable): source of the leaf's top n rows for Q (explicit-Q formation),
 // leaf i's block at S + i*s_slot_rows*lds.  zero_init: C tiles start at zero.
 // ---------------------------------------------------------------------------
-template <int NP, int KBS>
+// Per-warp V/tau staging: 32 reflectors x (rows + 2) for the taller of the
+// dense-tile rows per warp (HD) and the chain tile height.
+template <int NP, int HT>
+__host__ __device__ constexpr int apply_stage_doubles() {
+  return ApplyStage<(Geo<NP>::HD > HT ? Geo<NP>::HD : HT)>::DOUBLES;
+}
+template <int NP, int KBS, int HT>
 struct LeafApplySmem {
   static constexpr size_t bytes =
       sizeof(double) * ((size_t)NP * 32 * KBS + 2 * WARPS * 32 * KBS +
-                        (size_t)WARPS * ApplyStage<32>::DOUBLES) + sizeof(int) * NP;
+                        (size_t)WARPS * apply_stage_doubles<NP, HT>()) + sizeof(int) * NP;
 };
 
 template <int NP, int KBS, bool TRANS, int HT>
@@ -766,8 +772,9 @@ k_leaf_apply(const double* __restrict__ Y, int64_t ldy, const double* __restrict
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
   double* part = Cs + NP * KB;
-  double* vstage = part + 2 * WARPS * KB + (threadIdx.x >> 5) * ApplyStage<32>::DOUBLES;
-  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * KB + WARPS * ApplyStage<32>::DOUBLES);
+  constexpr int SD = apply_stage_doubles<NP, HT>();
+  double* vstage = part + 2 * WARPS * KB + (threadIdx.x >> 5) * SD;
+  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * KB + WARPS * SD);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int leaf = blockIdx.x;
   const int col0 = blockIdx.y * KB;
@@ -1259,7 +1266,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
   dim3 grid((unsigned)P, (unsigned)((ncols + 32 * kbs - 1) / (32 * kbs)));
 #define LA_LAUNCH(NPV, KB_, HTV)                                                                  \
   {                                                                                               \
-    const size_t sm = LeafApplySmem<NPV, KB_>::bytes;                                             \
+    const size_t sm = LeafApplySmem<NPV, KB_, HTV>::bytes;                                             \
     if (transpose) {                                                                              \
       int rc = prep(k_leaf_apply<NPV, KB_, true, HTV>, sm); if (rc) return rc;                    \
       k_leaf_apply<NPV, KB_, true, HTV><<<grid, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,    \
