@@ -149,6 +149,13 @@ int caqr_tune(int key, int value);
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */
 int caqr_f64_peak_probe(double* scratch, int mode, int iters, int blocks, void* stream);
 
+/* Transpose-on-load: rows x cols column-major src (column c at src + c*ld_src,
+ * the MAT1 on-disk order, pkg/src/caqr/matio.py:1-10) into row-major dst
+ * (row r at dst + r*ld_dst), as read_mat1's reshape(order="F") (:43-51)
+ * followed by the C-order layout the kernels use. */
+int tsqr_f64_colmajor_to_rowmajor(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                  double* dst, int64_t ld_dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

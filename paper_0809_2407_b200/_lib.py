@@ -23,6 +23,7 @@ SYMBOLS = (
     "tsqr_f64_r_binary",
     "tsqr_f64_r_binary_rows",
     "tsqr_f64_r_combine_level",
+    "tsqr_f64_colmajor_to_rowmajor",
     "tsqr_f64_tree_factor_level",
     "tsqr_f64_tree_apply_level",
     "tsqr_f64_leaf_apply",
@@ -60,6 +61,8 @@ def _sig(lib):
     lib.tsqr_f64_r_binary_rows.argtypes = [dp, i64, i64, i64, i64, i64, dp, ip, ip, vp]
     lib.tsqr_f64_r_combine_level.restype = i32
     lib.tsqr_f64_r_combine_level.argtypes = [dp, i64, ip, i64, vp]
+    lib.tsqr_f64_colmajor_to_rowmajor.restype = i32
+    lib.tsqr_f64_colmajor_to_rowmajor.argtypes = [dp, i64, i64, i64, dp, i64, vp]
     lib.tsqr_f64_tree_factor_level.restype = i32
     lib.tsqr_f64_tree_factor_level.argtypes = [dp, i64, ip, i64, dp, dp, vp]
     lib.tsqr_f64_tree_apply_level.restype = i32

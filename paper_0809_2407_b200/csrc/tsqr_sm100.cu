@@ -1015,6 +1015,33 @@ static int prep(K kernel, size_t smem) {
   return CAQR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Column-major -> row-major transpose on load (MAT1 files store columns,
+// matio.py:1-10; the kernels read rows): 32 x 32 tiles through padded shared
+// memory, coalesced on both sides.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_colmajor_to_rowmajor(const double* __restrict__ src, int64_t ld_src, int64_t rows, int cols,
+                       double* __restrict__ dst, int64_t ld_dst) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int c = c0 + ty + k;
+    const int64_t r = r0 + tx;
+    tile[ty + k][tx] = (c < cols && r < rows) ? src[(int64_t)c * ld_src + r] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t r = r0 + ty + k;
+    const int c = c0 + tx;
+    if (r < rows && c < cols) dst[r * ld_dst + c] = tile[tx][ty + k];
+  }
+}
+
 extern "C" {
 
 int caqr_sm100_abi_version(void) { return CAQR_SM100_ABI_VERSION; }
@@ -1375,6 +1402,17 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   return set_err(CAQR_ERR_ARG, "unknown tuning key");
+}
+
+int tsqr_f64_colmajor_to_rowmajor(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                  double* dst, int64_t ld_dst, void* stream) {
+  if (!src || !dst || rows < 0 || cols < 0 || cols > 65535 * 32 || ld_src < rows || ld_dst < cols)
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_colmajor_to_rowmajor: bad arguments");
+  if (rows == 0 || cols == 0) return CAQR_OK;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
+  k_colmajor_to_rowmajor<<<grid, 256, 0, (cudaStream_t)stream>>>(src, ld_src, rows, (int)cols, dst,
+                                                                 ld_dst);
+  return check_launch("k_colmajor_to_rowmajor");
 }
 
 int caqr_f64_peak_probe(double* scratch, int mode, int iters, int blocks, void* stream) {

@@ -74,23 +74,34 @@ def default_chunk_leaves(m: int, n: int, P: int, chunk_bytes: int = CHUNK_BYTES)
 
 def tsqr_stream(A, P: int, chunk_leaves: int | None = None, device=None, buffers: int = 3):
     """R (n x n, on the device) of the R-only binary-tree TSQR of the host
-    matrix A over P leaves, streamed in chunks (see module doc)."""
+    matrix A over P leaves, streamed in chunks (see module doc).
+
+    A: numpy array or CPU torch tensor, row-major (C order) or column-major
+    (a Fortran-ordered numpy array, e.g. a memory-mapped MAT1 file --
+    ``matio.open_mat1``): column-major chunks are staged as n column
+    segments and transposed on the device (``tsqr_f64_colmajor_to_rowmajor``).
+    """
     from .tsqr import _check_flag, _ptr
 
     lib = _lib.load()
+    colmajor = False
     if isinstance(A, np.ndarray):
+        if A.ndim != 2:
+            raise DimensionError("A must be 2-D")
         if A.dtype != np.float64:
             A = A.astype(np.float64)
-        At = torch.from_numpy(np.ascontiguousarray(A))
+        if A.flags.f_contiguous and not A.flags.c_contiguous:
+            colmajor = True
+            An = A
+        else:
+            At = torch.from_numpy(np.ascontiguousarray(A))
     elif isinstance(A, torch.Tensor):
         if A.is_cuda:
             raise ValueError("tsqr_stream takes a host matrix")
         At = A.to(torch.float64).contiguous()
     else:
         raise TypeError("A must be a numpy array or a CPU torch tensor")
-    if At.ndim != 2:
-        raise DimensionError("A must be 2-D")
-    m, n = At.shape
+    m, n = A.shape
     if m < n:
         raise DimensionError(f"need m >= n, got {m} x {n}")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -99,11 +110,12 @@ def tsqr_stream(A, P: int, chunk_leaves: int | None = None, device=None, buffers
     max_rows = max(c[3] for c in chunks)
     nbuf = max(1, min(buffers, len(chunks)))
     bufs = [torch.empty((max_rows, n), dtype=torch.float64, device=dev) for _ in range(nbuf)]
-    pinned = At.is_pinned()
+    pinned = (not colmajor) and At.is_pinned()
     stages = []
-    if not pinned:
-        stages = [torch.empty((max_rows, n), dtype=torch.float64, pin_memory=True)
+    if not pinned:  # host staging (column-major: n column segments per chunk)
+        stages = [torch.empty(max_rows * n, dtype=torch.float64, pin_memory=True)
                   for _ in range(min(2, len(chunks)))]
+    cm_scratch = torch.empty(max_rows * n, dtype=torch.float64, device=dev) if colmajor else None
     Rs = torch.empty((P, n, n), dtype=torch.float64, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     nlev = max(1, (K - 1).bit_length())
@@ -115,17 +127,30 @@ def tsqr_stream(A, P: int, chunk_leaves: int | None = None, device=None, buffers
     staged = [None] * len(stages)
     for c, (l0, k, r0, rows) in enumerate(chunks):
         slot = c % nbuf
-        src = At[r0:r0 + rows]
         if not pinned:
             si = c % len(stages)
             if staged[si] is not None:
                 staged[si].synchronize()  # the H2D that last read this staging buffer is done
-            stages[si][:rows].copy_(src)
-            src = stages[si][:rows]
+            if colmajor:
+                # n contiguous column segments (page cache / memmap reads)
+                np.copyto(stages[si][:rows * n].numpy().reshape(n, rows), An[r0:r0 + rows].T)
+                src = stages[si][:rows * n]
+            else:
+                stages[si][:rows * n].view(rows, n).copy_(At[r0:r0 + rows])
+                src = stages[si][:rows * n].view(rows, n)
+        else:
+            src = At[r0:r0 + rows]
         if done[slot] is not None:
             cs.wait_event(done[slot])
         with torch.cuda.stream(cs):
-            bufs[slot][:rows].copy_(src, non_blocking=True)
+            if colmajor:
+                cm_scratch[:rows * n].copy_(src, non_blocking=True)
+                _lib.check(lib.tsqr_f64_colmajor_to_rowmajor(_ptr(cm_scratch), rows, rows, n,
+                                                             _ptr(bufs[slot]), n,
+                                                             int(cs.cuda_stream)),
+                           "tsqr_f64_colmajor_to_rowmajor")
+            else:
+                bufs[slot][:rows].copy_(src, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(cs)
         if not pinned:
@@ -143,5 +168,7 @@ def tsqr_stream(A, P: int, chunk_leaves: int | None = None, device=None, buffers
                                                 int(st.cuda_stream)), "tsqr_f64_r_combine_level")
     for b in bufs:
         b.record_stream(cs)
+    if cm_scratch is not None:
+        cm_scratch.record_stream(cs)
     _check_flag(flag)
     return Rs[0]

@@ -302,3 +302,22 @@ def test_tuning_variants_keep_parity():
     finally:
         _lib.tune(_lib.TUNE_ZSTART, 1)
     assert oracle.r_diff(tsqr(A, leaf_rows=5000), Rref, scale) <= 1000 * EPS
+
+
+@pytest.mark.parametrize("m,n,leaf,K", [(70001, 128, 4096, 2), (200000, 8, 16384, 4), (30000, 50, 1000, 8)])
+def test_tsqr_from_mat1_file_is_bitwise_the_in_memory_r(tmp_path, m, n, leaf, K):
+    """TSQR streamed from a column-major MAT1 file (transpose on the GPU) gives
+    tsqr()'s R bit for bit; also through the chunked path with K leaves per chunk."""
+    from paper_0809_2407_b200.matio import open_mat1, tsqr_mat1, write_mat1
+    from paper_0809_2407_b200.stream import tsqr_stream
+    from paper_0809_2407_b200.tsqr import _leaves_for, factor_device, split_leaves, tsqr
+
+    A = philox(m * 3 + n).standard_normal((m, n))
+    p = tmp_path / "a.mat"
+    write_mat1(p, A)
+    R = tsqr(A, leaf_rows=leaf)
+    assert np.array_equal(tsqr_mat1(p, leaf_rows=leaf), R)
+    P = _leaves_for(m, n, leaf)
+    P *= split_leaves(m, n, P, fill=n > 8)
+    Rk = tsqr_stream(open_mat1(p), P, chunk_leaves=K).cpu().numpy()
+    assert np.array_equal(Rk, factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy())

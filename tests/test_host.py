@@ -232,3 +232,38 @@ def test_caqr_grid_layout_needs_a_distributed_job():
     A = np.zeros((256, 128))
     with pytest.raises(ExecutorError):
         caqr_factor(A, BlockCyclicLayout(256, 128, 64, 2, 1))
+
+
+def test_mat1_format_matches_the_reference_layout(tmp_path):
+    """MAT1 (matio.py:1-10): 24-byte little-endian header + column-major doubles;
+    bad magic / short files raise FormatError; CSV round trip."""
+    import struct
+
+    from paper_0809_2407_b200.matio import (FormatError, open_mat1, read_matrix, write_csv,
+                                            write_mat1, write_matrix)
+
+    A = np.arange(12, dtype=np.float64).reshape(4, 3) / 7.0
+    p = tmp_path / "a.mat"
+    write_mat1(p, A)
+    raw = p.read_bytes()
+    assert raw[:24] == struct.pack("<8sIIII", b"TSQRMAT1", 4, 3, 0, 0)
+    assert raw[24:] == A.tobytes(order="F")
+    assert np.array_equal(read_matrix(p), A)
+    mm = open_mat1(p)
+    assert mm.flags.f_contiguous and np.array_equal(np.asarray(mm), A)
+    c = tmp_path / "a.csv"
+    write_matrix(c, A)
+    assert np.array_equal(read_matrix(c), A)
+    (tmp_path / "bad.mat").write_bytes(b"NOTAMAT1" + raw[8:])
+    with pytest.raises(FormatError):
+        read_matrix(tmp_path / "bad.mat")
+    (tmp_path / "short.mat").write_bytes(raw[:-8])
+    with pytest.raises(FormatError):
+        read_matrix(tmp_path / "short.mat")
+    B = A.copy()
+    B[1, 1] = np.nan
+    with pytest.raises(ValueError):
+        write_csv(tmp_path / "nan.csv", B)  # as_matrix on write too (matio.py:54-55)
+    np.savetxt(tmp_path / "nan.csv", B, delimiter=",")
+    with pytest.raises(ValueError):
+        read_matrix(tmp_path / "nan.csv")
