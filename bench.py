@@ -407,9 +407,14 @@ def run_ours(args, cfg):
             e1.record(stream)
             leaf_ev.append((e0, e1))
         if ws > 1:
-            from paper_0809_2407_b200.dist import cross_tree, gpu_combine
+            # cross-GPU binary tree of the per-rank R factors; explicit Q walks
+            # back down it (dist.tsqr_sharded_explicit_q)
+            from paper_0809_2407_b200.dist import cross_tree, gpu_combine, tsqr_sharded_explicit_q
 
-            cross_tree(f.R, gpu_combine)
+            _, nodes = cross_tree(f.R, gpu_combine)
+            if cfg["q"] == "explicit":
+                tsqr_sharded_explicit_q(f, nodes)
+            return f
         if cfg["q"] == "explicit":
             explicit_q_device(f)
         return f
@@ -522,10 +527,24 @@ def run_ours(args, cfg):
             def e2e_step():
                 res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
                 return res.R
-        else:
+        elif ws == 1:
             def e2e_step():
                 out = tsqr(Ah, leaf_rows=cfg["leaf"], q=cfg["q"])
                 return out
+        else:
+            from paper_0809_2407_b200.dist import cross_tree, gpu_combine, tsqr_sharded_explicit_q
+
+            def e2e_step():
+                # this rank's shard from pinned host memory -> local TSQR (streamed
+                # when R only) -> cross-GPU tree -> R (and this rank's Q rows) to host
+                if cfg["q"] == "none":
+                    Rl = torch.from_numpy(tsqr(Ah, leaf_rows=cfg["leaf"])).to(dev)
+                    R, _ = cross_tree(Rl, gpu_combine)
+                    return None if R is None else R.cpu()
+                _, f = tsqr(Ah, leaf_rows=cfg["leaf"], q="implicit")
+                R, nodes = cross_tree(f.R, gpu_combine)
+                Q = tsqr_sharded_explicit_q(f, nodes).cpu()
+                return Q, (None if R is None else R.cpu())
         # two warm-up calls: results alternate between two host buffers, so the
         # caching pinned allocator is in steady state before timing
         out = e2e_step()
