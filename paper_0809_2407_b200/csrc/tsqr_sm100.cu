@@ -601,9 +601,10 @@ k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, do
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     if (j >= n) break;
-    double sg = 0.0;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: latency j/4 instead of j
 #pragma unroll
-    for (int r = 0; r <= j; ++r) sg = fma(cb[r], cb[r], sg);
+    for (int r = 0; r <= j; ++r) s4[r & 3] = fma(cb[r], cb[r], s4[r & 3]);
+    double sg = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     sg = __shfl_sync(FULL, sg, j);
     const double x0 = __shfl_sync(FULL, ca[j], j);
     double beta, tau, scale;
@@ -614,9 +615,10 @@ k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, do
       for (int r = 0; r <= j; ++r) vs[r] = cb[r] * scale;
     }
     __syncwarp();
-    double d = ca[j];
+    double d4[4] = {ca[j], 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int r = 0; r <= j; ++r) d = fma(vs[r], cb[r], d);
+    for (int r = 0; r <= j; ++r) d4[r & 3] = fma(vs[r], cb[r], d4[r & 3]);
+    const double d = (d4[0] + d4[1]) + (d4[2] + d4[3]);
     const double w = (lane > j) ? tau * d : 0.0;
     ca[j] -= w;
 #pragma unroll
