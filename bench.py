@@ -488,28 +488,49 @@ def run_ours(args, cfg):
     if is_caqr:
         roof, caqr_launches = caqr_roofline(A, cfg, args)
     if leaf_ev:
+        # the timed bracket: one factor_device call (or the graph replay of the
+        # step, which for explicit-Q configs also forms Q: 2x the flops)
         t_leaf = float(np.mean([a.elapsed_time(b) for a, b in leaf_ev])) * 1e-3
-        F_leaf = flops(hi - lo, n)
-        ach = F_leaf / t_leaf / 1e12
-        # DRAM traffic of the chain kernel from the committed ncu capture
-        # (profiles/r01/chain_kernel_ncu_summary.txt: 1.2417e9 B read + 3.5e6 B
-        # written for 148 leaves of 8192 x 128 = 1.0030x the 8mn algorithmic
-        # bytes), scaled to this launch's rows; None for other widths.
-        traffic = 8.0 * (hi - lo) * n * 1.0030 if (n == 128 and cfg["q"] == "none") else None
-        roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "traffic_source": "ncu --set full, profiles/r01 (scaled per launch)",
-                "kernel": "k_leaf_factor + k_tree_factor (one factor_device call)",
-                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
-                               "entry in MEASURED_PEAKS.json)",
-                "algorithmic_flops_per_launch": F_leaf}
-        if cfg["q"] == "none" and not is_caqr:
-            hbm = 6526.5
-            try:
-                hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-            except Exception:
-                pass
-            t_roof = max(F_leaf / (FP64_PEAK_TFLOPS * 1e12), 8.0 * (hi - lo) * n / (hbm * 1e9))
+        qmul = 2 if cfg["q"] == "explicit" else 1
+        F_leaf = qmul * flops(hi - lo, n)
+        hbm = 6526.5
+        try:
+            hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            pass
+        t_flop = F_leaf / (FP64_PEAK_TFLOPS * 1e12)
+        t_byte = 8.0 * (hi - lo) * n / (hbm * 1e9)
+        narrow = n <= 8 and cfg["q"] == "none"
+        if cfg["q"] == "none" and t_byte > t_flop:
+            # HBM-bound (C4, AI = n/4 flop/B < the 5.7 ridge): bytes of A per launch
+            ach = 8.0 * (hi - lo) * n / t_leaf / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "traffic": 8.0 * (hi - lo) * n * 1.0011 if narrow else None,
+                    "traffic_source": "ncu --set full of k_leaf_narrow (profiles/r01/"
+                                      "narrow_kernel_ncu_summary.txt): 1.0011 x 8mn, scaled per launch",
+                    "kernel": "k_leaf_narrow (cp.async stages) + fused ticket tree (one factor_device call)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "algorithmic_bytes_per_launch": 8.0 * (hi - lo) * n}
+        else:
+            ach = F_leaf / t_leaf / 1e12
+            # DRAM traffic of the chain kernel from the committed ncu capture
+            # (profiles/r01/chain_kernel_ncu_summary.txt: 1.2418e9 B read + 3.9e6 B
+            # written for 148 leaves of 8192 x 128 = 1.0030x the 8mn algorithmic
+            # bytes), scaled to this launch's rows; None for other widths.
+            traffic = 8.0 * (hi - lo) * n * 1.0030 if (n == 128 and cfg["q"] == "none") else None
+            kern = ("k_leaf_chain (R = 0 start) + k_tree_ring (one factor_device call)"
+                    if cfg["q"] == "none" else
+                    "k_leaf_dense + k_leaf_chain + k_tree_factor, then Q: k_tree_apply + k_leaf_apply "
+                    "(graph replay of the step; credited with the factor and Q-formation flops)")
+            roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "traffic_source": "ncu --set full, profiles/r01 (scaled per launch)",
+                    "kernel": kern,
+                    "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
+                                   "entry in MEASURED_PEAKS.json)",
+                    "algorithmic_flops_per_launch": F_leaf}
+        if cfg["q"] == "none":
+            t_roof = max(t_flop, t_byte)
             roof["t_roof_ms"] = t_roof * 1e3
             roof["roofline_frac_time"] = t_roof / t_leaf
 
