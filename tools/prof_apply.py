@@ -5,7 +5,6 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_0809_2407_b200 import _lib
 from paper_0809_2407_b200.tsqr import _leaf_apply, factor_device
 
 m, n, P, k = 16384, 128, 8, 16384 - 128

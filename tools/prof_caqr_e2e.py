@@ -1,4 +1,4 @@
-import time, torch, numpy as np, sys
+import time, torch, sys
 sys.path.insert(0, '.')
 from paper_0809_2407_b200.caqr import caqr_factor
 n = 16384
