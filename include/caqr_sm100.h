@@ -144,6 +144,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 /* CAQR_TUNE_ZSTART: 1 (default) = R-only leaves (no Y stored) run the chain from
  * R = 0 over all their rows instead of a dense first tile + chain. */
 #define CAQR_TUNE_ZSTART 6
+/* CAQR_TUNE_BLOCKED: 1 = R-only leaves with n in (64, 128] run the tall-tile kernel (128-row
+ * tiles in shared memory, 16-column panels, compact-WY trailing update on the FP64 tensor
+ * cores); 0 (default) = the warp-ring chain. */
+#define CAQR_TUNE_BLOCKED 8
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

@@ -121,6 +121,7 @@ def check(rc: int, what: str) -> None:
 TUNE_CHAIN_HT = {32: 1, 64: 2, 128: 3}
 TUNE_NARROW = 4
 TUNE_ZSTART = 6
+TUNE_BLOCKED = 8
 
 
 def tune(key: int, value: int) -> None:

@@ -50,6 +50,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
+static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -158,6 +159,8 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
   if (bad && flag) atomicOr(flag, 1);
 }
 
+
+#include "blocked_leaf.cuh"
 
 // ---------------------------------------------------------------------------
 // Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
@@ -1115,7 +1118,12 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                              \
+    if (NPV == 128 && zs && g_blocked) {                                                        \
+      rc = prep(k_leaf_blocked, BlockedSmem::bytes);                                         \
+      if (rc) return rc;                                                                        \
+      k_leaf_blocked<<<grid, 256, BlockedSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
+                                                               R, flag);                        \
+    } else if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                       \
       if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA)                                      \
       else if (NPV == 64 && g_ht[1] == 24) CHAIN_LAUNCH(64, 24)                                 \
       else CHAIN_LAUNCH(NPV, HB)                                                                \
@@ -1397,6 +1405,10 @@ int caqr_tune(int key, int value) {
   if (key == CAQR_TUNE_NARROW) {
     if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW takes 0, 1 or 2");
     g_narrow = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_BLOCKED) {
+    g_blocked = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_ZSTART) {
