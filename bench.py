@@ -633,7 +633,7 @@ def main():
                     help="replay each TSQR step as one captured CUDA graph (1 GPU, not CAQR)")
     ap.add_argument("--grid", action="store_true",
                     help="c5: run the Pr x Pc grid driver even on one GPU (1 x 1 grid)")
-    ap.add_argument("--panel-chains", type=int, default=2,
+    ap.add_argument("--panel-chains", type=int, default=4,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

@@ -76,7 +76,7 @@ def _panel_leaves(mj: int, w: int, leaf_rows: int) -> int:
 
 def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_rows: int = 2048,
                 device=None, counter=None, lookahead: bool = True,
-                panel_chains: int = 2) -> CaqrResult:
+                panel_chains: int = 4) -> CaqrResult:
     """CAQR of A (m x n, m >= n) with panel width b <= 128.
 
     With ``lookahead`` (default) the panels run on a high-priority stream:
