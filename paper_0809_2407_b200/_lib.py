@@ -122,6 +122,7 @@ TUNE_CHAIN_HT = {32: 1, 64: 2, 128: 3}
 TUNE_NARROW = 4
 TUNE_ZSTART = 6
 TUNE_BLOCKED = 8
+TUNE_DMMA = 9
 
 
 def tune(key: int, value: int) -> None:

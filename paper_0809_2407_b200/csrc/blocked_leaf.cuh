@@ -24,10 +24,6 @@ struct BlockedSmem {
 
 __device__ __forceinline__ int bl_pk(int j, int c) { return j * 128 - (j * (j - 1)) / 2 + (c - j); }
 
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll

@@ -93,6 +93,27 @@ __device__ __forceinline__ void ring_signal(int* ver, int value, int lane) {
   }
 }
 
+// cp.async granules (8 or 16 bytes, zero fill when bytes < G)
+template <int G>
+__device__ __forceinline__ void cp_async(unsigned dst, const void* src, unsigned bytes) {
+  if constexpr (G == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// FP64 tensor-core MMA, D = A B + D (m8n8k4, A row-major 8x4, B col-major 4x8):
+// lane (g = lane/4, q = lane%4) supplies A[g][q], B[q][g] and holds D[g][2q], D[g][2q+1]
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------------------------------
 // Tile load / store (row-major global, leading dimension ld, zero padding)
 // ---------------------------------------------------------------------------

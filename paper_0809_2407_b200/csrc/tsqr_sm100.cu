@@ -51,6 +51,7 @@ static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
+static int g_dmma = 0;     // CAQR_TUNE_DMMA: R-only n in (64,128] leaves on the DMMA warp ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -190,19 +191,6 @@ struct NarrowPipe {
   static constexpr int STAGE_B = 32 * K * ROW_B;
   static constexpr size_t SMEM = (size_t)W * STAGES * STAGE_B;
 };
-
-template <int G>
-__device__ __forceinline__ void cp_async(unsigned dst, const void* src, unsigned bytes) {
-  if constexpr (G == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(bytes)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 // Packed upper-triangular 8x8 R in registers: element (i, c), c >= i.
 __host__ __device__ constexpr int pk8(int i, int c) { return i * 8 - (i * (i - 1)) / 2 + (c - i); }
@@ -1006,6 +994,8 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+#include "dmma_ring.cuh"
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -1118,7 +1108,20 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if (NPV == 128 && zs && g_blocked) {                                                        \
+    if (NPV == 128 && zs && g_dmma) {                                                           \
+      const bool v16 = (n % 2 == 0) && (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);            \
+      if (v16) {                                                                                \
+        rc = prep(k_leaf_dmma<true>, DmmaRingSmem::bytes);                                      \
+        if (rc) return rc;                                                                      \
+        k_leaf_dmma<true><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n,  \
+                                                                          (int)P, base, R, flag); \
+      } else {                                                                                  \
+        rc = prep(k_leaf_dmma<false>, DmmaRingSmem::bytes);                                     \
+        if (rc) return rc;                                                                      \
+        k_leaf_dmma<false><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n, \
+                                                                           (int)P, base, R, flag); \
+      }                                                                                         \
+    } else if (NPV == 128 && zs && g_blocked) {                                                 \
       rc = prep(k_leaf_blocked, BlockedSmem::bytes);                                         \
       if (rc) return rc;                                                                        \
       k_leaf_blocked<<<grid, 256, BlockedSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
@@ -1409,6 +1412,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_BLOCKED) {
     g_blocked = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DMMA) {
+    g_dmma = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_ZSTART) {

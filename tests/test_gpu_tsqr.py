@@ -342,3 +342,38 @@ def test_blocked_tall_tile_leaf_parity():
             factor_device(torch.from_numpy(A).cuda(), 2)
     finally:
         _lib.tune(_lib.TUNE_BLOCKED, 0)
+
+
+@pytest.mark.parametrize("v16", [True, False])
+def test_dmma_ring_leaf_parity(v16):
+    """CAQR_TUNE_DMMA = 1: R-only leaves with n in (64, 128] on the DMMA warp
+    ring (16-row register tiles, 8-column Level-2 panels, compact-WY updates on
+    the FP64 tensor cores).  R against LAPACK, sign-normalised; odd n / lda take
+    the 8-byte cp.async staging path."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    shapes = [(4096, 128, 2), (20000, 100, 4), (3000, 72, 1), (9001, 128, 3), (1 << 16, 128, 4)]
+    if not v16:
+        shapes = [(5000, 99, 2), (4099, 127, 3)]
+    try:
+        _lib.tune(_lib.TUNE_DMMA, 1)
+        for (m, n, P) in shapes:
+            A = philox(m + n).standard_normal((m, n))
+            R = factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy()
+            assert np.array_equal(R, np.triu(R))
+            d = oracle.r_diff(R, np.linalg.qr(A, mode="r"), np.linalg.norm(A, 2))
+            assert d <= 1000 * EPS, (m, n, P, d / EPS)
+        # rank-deficient and zero columns (sigma = 0 / tau = 0 reflectors inside a
+        # panel): R is no longer unique, so check R^T R = A^T A instead
+        A = philox(3).standard_normal((4096, 96))
+        A[:, 10] = 0.0
+        A[:, 40] = A[:, 41]
+        R = factor_device(torch.from_numpy(A).cuda(), 2).R.cpu().numpy()
+        assert np.linalg.norm(R.T @ R - A.T @ A) <= 1000 * EPS * np.linalg.norm(A, 2) ** 2
+        A = philox(7).standard_normal((5000, 96))
+        A[4321, 50] = np.nan
+        with pytest.raises(ValueError):
+            factor_device(torch.from_numpy(A).cuda(), 2)
+    finally:
+        _lib.tune(_lib.TUNE_DMMA, 0)

@@ -15,9 +15,13 @@ ap.add_argument("--leaf-rows", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--q", default="none")
 ap.add_argument("--ht", type=int, default=0)
+ap.add_argument("--tune", action="append", default=[], help="KEY=VALUE (caqr_tune)")
 a = ap.parse_args()
 from paper_0809_2407_b200 import _lib
 np_ = 32 if a.n <= 32 else (64 if a.n <= 64 else 128)
+for kv in a.tune:
+    k, v = kv.split("=")
+    _lib.tune(int(k), int(v))
 if a.ht:
     _lib.tune(_lib.TUNE_CHAIN_HT[np_], a.ht)
 A = torch.randn(a.leaves * a.leaf_rows, a.n, dtype=torch.float64, device="cuda")
