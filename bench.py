@@ -513,12 +513,12 @@ def run_ours(args, cfg):
                     "algorithmic_bytes_per_launch": 8.0 * (hi - lo) * n}
         else:
             ach = F_leaf / t_leaf / 1e12
-            # DRAM traffic of the chain kernel from the committed ncu capture
-            # (profiles/r01/chain_kernel_ncu_summary.txt: 1.2418e9 B read + 3.9e6 B
-            # written for 148 leaves of 8192 x 128 = 1.0030x the 8mn algorithmic
+            # DRAM traffic of the leaf kernel from the committed ncu capture
+            # (profiles/r01/dmma_kernel_ncu_summary.txt: 1.2433e9 B read + 4.2e6 B
+            # written for 148 leaves of 8192 x 128 = 1.0048x the 8mn algorithmic
             # bytes), scaled to this launch's rows; None for other widths.
-            traffic = 8.0 * (hi - lo) * n * 1.0030 if (n == 128 and cfg["q"] == "none") else None
-            kern = ("k_leaf_chain (R = 0 start) + k_tree_ring (one factor_device call)"
+            traffic = 8.0 * (hi - lo) * n * 1.0048 if (n == 128 and cfg["q"] == "none") else None
+            kern = ("k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)"
                     if cfg["q"] == "none" else
                     "k_leaf_dense + k_leaf_chain + k_tree_factor, then Q: k_tree_apply + k_leaf_apply "
                     "(graph replay of the step; credited with the factor and Q-formation flops)")

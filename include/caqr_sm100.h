@@ -148,9 +148,9 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * tiles in shared memory, 16-column panels, compact-WY trailing update on the FP64 tensor
  * cores); 0 (default) = the warp-ring chain. */
 #define CAQR_TUNE_BLOCKED 8
-/* CAQR_TUNE_DMMA: 1 = R-only leaves with n in (64, 128] run the DMMA warp ring (16-row
- * tiles per warp in registers, 8-column Level-2 panels, compact-WY trailing updates on
- * the FP64 tensor cores); 0 = the rank-1 warp ring. */
+/* CAQR_TUNE_DMMA: 1 (default) = R-only leaves with n in (64, 128] run the DMMA warp ring
+ * (16-row tiles per warp in registers, 8-column Level-2 panels with look-ahead,
+ * compact-WY trailing updates on the FP64 tensor cores); 0 = the rank-1 warp ring. */
 #define CAQR_TUNE_DMMA 9
 int caqr_tune(int key, int value);
 

@@ -1,27 +1,32 @@
-// DMMA warp ring leaf (R only, 64 < n <= 128).
+// DMMA warp-ring leaf (R only, 64 < n <= 128): the C3 hot kernel.
 //
 // The flat chain of triangle-on-rectangle steps of a leaf (Alg. 2,
 // PAPER.md:840-866; one step = qr_triangle_on_rect, householder.py:297-332)
-// run as a warp ring like k_leaf_chain -- warp w owns 16-row tiles
-// t = w, w+8, ..., the pivot rows R live in shared memory -- but each tile step
-// is BLOCKED: 8-column panels are factored Level-2 inside the warp and the
-// trailing update of each panel is the compact-WY product (householder.py:
-// 175-186 with V = [I; Y])
+// runs as a warp ring like k_leaf_chain -- warp w owns the 16-row tiles
+// t = w, w+8, ..., the pivot rows R live in shared memory -- but every tile
+// step is BLOCKED: 8-column panels are factored Level-2 inside the warp and
+// the trailing update of each panel is the compact-WY product
+// (householder.py:175-186 with V = [I; Y])
 //
 //     W  = R_p,trail + Y^T C          (4 DMMA per 8-column block)
 //     W' = T^T W                      (2 DMMA)
 //     R_p,trail -= W',  C -= Y W'     (4 DMMA)
 //
-// on the FP64 tensor cores (mma.m8n8k4.f64).  One DMMA issues 256 FMAs, so the
-// issue slots the rank-1 ring spent on DFMA go to the panel reflectors.
+// on the FP64 tensor cores (mma.m8n8k4.f64); T itself is a Neumann product
+// on the tensor cores (dr_form_t).
 //
-// Register layout: the tile (16 x 128) is held as 2 x 16 blocks of 8 x 8 in
+// Register layout: the tile (16 x 128) is held as 16 x 2 blocks of 8 x 8 in
 // the DMMA accumulator layout of C^T: lane (g = lane/4, q = lane%4) holds
 // C[8 b + 2 q + e][8 cb + g], e = 0, 1.  With the rows of every k-step
 // permuted to {2 q + s}, that same register is the A operand of C^T Y and the
 // accumulator of C^T -= W'^T Y^T, so the tile never leaves registers.  The
 // panel being factored is always register block 0: after each panel the
 // blocks shift down by one.
+//
+// Look-ahead: the Level-2 of panel p+1 (block 1, once panel p has updated
+// it) is interleaved generation by generation with panel p's updates of the
+// other blocks, so the warp's latency-bound reflector chain and its DMMA work
+// overlap.
 //
 // Pivot rows: R is stored panel-packed in shared memory (panel p = rows
 // 8p..8p+7, columns 8p..127, row stride 130 - 8p).  Tile t may factor panel p
@@ -34,7 +39,7 @@ constexpr int DR_H = 16;            // tile rows per warp
 constexpr int DR_NP = 128;          // padded width
 constexpr int DR_NCB = DR_NP / 8;   // 8-column blocks
 constexpr int DR_SLD = DR_NP + 2;   // staging row stride (doubles): conflict-free fragment loads
-constexpr int DR_SCR = 336;         // per-warp scratch (V^T staging 16 x 12, G, T, tau)
+constexpr int DR_SCR = 264;         // per-warp scratch: Y^T staging 16 x 12, G 8 x 8, tau 8
 __host__ __device__ constexpr int dr_ldr(int p) { return DR_NP - 8 * p + 2; }
 __host__ __device__ constexpr int dr_pbase(int p) { return 8 * (p * (DR_NP + 2) - 4 * p * (p - 1)); }
 struct DmmaRingSmem {
@@ -75,77 +80,6 @@ __device__ __forceinline__ void dr_issue(double* stage, const double* __restrict
   cp_async_commit();
 }
 
-// Level-2 factorisation of the panel held in x[4] (= C[b][0][e]: rows
-// 8b + 2q + e, column pc + g) against the pivot rows Rpan (row stride ldr).
-// On return x holds the panel's Y (tile part of V), Rpan the updated R_pp,
-// gs[s][i] = Y_s^T Y_i (s < i) and taus[i] = tau_i.  Every lane evaluates the
-// reflector scalars (house_gen, householder.py:97-113) redundantly from the
-// broadcast column, so only two 4-lane reductions sit on the critical path.
-__device__ __forceinline__ void dr_panel(double (&x)[4], double* Rpan, int ldr, double* gs,
-                                         double* taus) {
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
-#ifdef DR_ROLLED
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-  for (int i = 0; i < 8; ++i) {
-    const int src = 4 * i + q;
-    double xi[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) xi[k] = __shfl_sync(FULL, x[k], src);
-    const double rgi = Rpan[i * ldr + g];  // row i of R_pp changes only at reflector i
-    const double x0 = __shfl_sync(FULL, rgi, 4 * i);
-    double s = xi[0] * xi[0], s2 = xi[2] * xi[2];
-    s = fma(xi[1], xi[1], s);
-    s2 = fma(xi[3], xi[3], s2);
-    double pd = xi[0] * x[0], pd2 = xi[2] * x[2];
-    pd = fma(xi[1], x[1], pd);
-    pd2 = fma(xi[3], x[3], pd2);
-    s += s2;
-    pd += pd2;
-    s += __shfl_xor_sync(FULL, s, 1);
-    pd += __shfl_xor_sync(FULL, pd, 1);
-    s += __shfl_xor_sync(FULL, s, 2);
-    pd += __shfl_xor_sync(FULL, pd, 2);
-    double beta, tau, scale;
-    house_lean(x0, s, beta, tau, scale);
-    const double wv = tau * fma(scale, pd, rgi);
-    const bool upd = g > i;
-    const double f = upd ? -scale * wv : 0.0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) x[k] = (g == i) ? xi[k] * scale : fma(f, xi[k], x[k]);
-    if (q == 0) {
-      if (upd) Rpan[i * ldr + g] = rgi - wv;
-      else if (g == i) Rpan[i * ldr + i] = beta;
-      else gs[g * 8 + i] = scale * pd;
-    }
-    if (lane == 0) taus[i] = tau;
-  }
-}
-
-// T of the panel (dlarft forward/columnwise, householder.py:148-164, with
-// V^T V = I + G): lane l < 8 runs the recurrence for row l of T.
-__device__ __forceinline__ void dr_form_t(const double* gs, const double* taus, double* ts) {
-  const int lane = threadIdx.x & 31;
-  if (lane < 8) {
-    const int l = lane;
-    double Tl[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) Tl[c] = (c == l) ? taus[l] : 0.0;
-#pragma unroll
-    for (int i = 1; i < 8; ++i) {
-      double z = 0.0;
-#pragma unroll
-      for (int s = 0; s < i; ++s) z = fma(Tl[s], gs[s * 8 + i], z);  // Tl[s] = 0 for s < l
-      if (l < i) Tl[i] = -taus[i] * z;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) ts[l * 8 + c] = Tl[c];
-  }
-}
-
 #ifdef DR_PROBE
 __device__ unsigned long long g_dr_cycles[8];
 #define DR_TICK(v) const long long v = clock64()
@@ -158,25 +92,152 @@ __device__ unsigned long long g_dr_cycles[8];
 
 // Ring wait, warp-uniform: lane 0 polls and broadcasts, so the warp never
 // diverges around the spin (a diverged warp runs every later shuffle through
-// the slow collective path).
-#ifndef DR_SLEEP
-#define DR_SLEEP 0
-#endif
+// the slow collective path -- measured 2.2x slower).
 __device__ __forceinline__ void dr_wait(const int* ver, int target, int lane) {
   for (;;) {
     int v = 0;
     if (lane == 0) v = ld_acquire(ver);
     v = __shfl_sync(FULL, v, 0);
     if (v == target) break;
-    if (DR_SLEEP) __nanosleep(DR_SLEEP);
   }
   __threadfence_block();
+}
+
+// house_gen scalars (householder.py:97-113) for the panel generations, with
+// the reciprocal seeded from the rsqrt seed so its MUFU latency overlaps the
+// rsqrt Newton steps (two Newton steps from a ~2^-19 seed: full precision),
+// plus invb = 1/beta (= -sign(x0) y; 0 when sigma = 0) so that the column
+// update factor -scale * tau * t = t / beta needs no product with tau.
+__device__ __forceinline__ void house_fast(double x0, double sigma, double& beta, double& tau,
+                                           double& scale, double& invb) {
+  const double a = fma(x0, x0, sigma);
+  const double ax = fabs(x0);
+  double y, r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double d0 = fma(a, y, ax);
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d0));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  const double nrm = a * y;
+  const double d = ax + nrm;
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  const bool pos = (x0 >= 0.0);
+  const bool z = (sigma == 0.0);
+  beta = z ? ax : (pos ? -nrm : nrm);
+  tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
+  scale = z ? 0.0 : (pos ? r : -r);
+  invb = z ? 0.0 : (pos ? -y : y);
+}
+
+// One generation (reflector I of the panel) of the register Level-2, with
+// branch-free stores: every lane stores (the four lanes of a column group
+// write the same value to the same address), so the look-ahead block stays
+// one basic block.  rgi = R[pc+I][pc+g] (preloaded); Rrow = &R[pc+I][pc].
+template <int I>
+__device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow, double* gs,
+                                       double* taus) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int src = 4 * I + q;
+  double xi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) xi[k] = __shfl_sync(FULL, x[k], src);
+  const double x0 = __shfl_sync(FULL, rgi, 4 * I);
+  double s = xi[0] * xi[0], s2 = xi[2] * xi[2];
+  s = fma(xi[1], xi[1], s);
+  s2 = fma(xi[3], xi[3], s2);
+  double pd = xi[0] * x[0], pd2 = xi[2] * x[2];
+  pd = fma(xi[1], x[1], pd);
+  pd2 = fma(xi[3], x[3], pd2);
+  s += s2;
+  pd += pd2;
+  s += __shfl_xor_sync(FULL, s, 1);
+  pd += __shfl_xor_sync(FULL, pd, 1);
+  s += __shfl_xor_sync(FULL, s, 2);
+  pd += __shfl_xor_sync(FULL, pd, 2);
+  double beta, tau, scale, invb;
+  house_fast(x0, s, beta, tau, scale, invb);
+  const double tw = fma(scale, pd, rgi);  // R[i][g] + v^T x_g
+  const double wv = tau * tw;
+  const bool upd = g > I;
+  const double f = upd ? tw * invb : 0.0;  // = -scale * wv
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[k] = (g == I) ? xi[k] * scale : fma(f, xi[k], x[k]);
+  double* dst = upd ? Rrow + g : ((g == I) ? Rrow + I : gs + g * 8 + I);
+  *dst = upd ? rgi - wv : ((g == I) ? beta : scale * pd);
+  taus[I] = tau;
+}
+
+// T^T of the panel on the FP64 tensor cores: with S = striu(G), D = diag(tau)
+// and N = D S (nilpotent), T = (I + N)^-1 D (T^-1 = D^-1 + S; equals dlarft's
+// recurrence, householder.py:148-164, also when some tau = 0), so
+// T^T = D P(M), M = N^T, P(M) = (I - M)(I + M^2)(I + M^4): five m8n8k4 pairs
+// instead of the sequential recurrence.  Returns tb[s] = T[2q+s][g], the B
+// operand of W'^T = W^T T.  Accumulator layout A: lane (g,q) holds X[g][2q+e];
+// B form: X[2q+s][g] (= the accumulator layout of X^T).
+__device__ __forceinline__ void dr_form_t(const double* gs, const double* taus, double& tb0,
+                                           double& tb1) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const double tg = taus[g];
+  double MA[2], MB[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int c = 2 * q + e;
+    MA[e] = (c < g) ? taus[c] * gs[c * 8 + g] : 0.0;  // M[g][c] = tau_c G[c][g]
+    MB[e] = (g < c) ? tg * gs[g * 8 + c] : 0.0;       // M[c][g] = tau_g G[g][c]
+  }
+  double M2A[2] = {0.0, 0.0}, M2B[2] = {0.0, 0.0};
+  dmma(M2A[0], M2A[1], MA[0], MB[0]);
+  dmma(M2B[0], M2B[1], MB[0], MA[0]);
+  dmma(M2A[0], M2A[1], MA[1], MB[1]);
+  dmma(M2B[0], M2B[1], MB[1], MA[1]);
+  double M4B[2] = {0.0, 0.0}, M3A[2] = {0.0, 0.0};
+  dmma(M4B[0], M4B[1], M2B[0], M2A[0]);
+  dmma(M3A[0], M3A[1], MA[0], M2B[0]);
+  dmma(M4B[0], M4B[1], M2B[1], M2A[1]);
+  dmma(M3A[0], M3A[1], MA[1], M2B[1]);
+  double P1[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) P1[e] = ((2 * q + e == g) ? 1.0 : 0.0) - MA[e] + M2A[e] - M3A[e];
+  double PA[2] = {P1[0], P1[1]};
+  dmma(PA[0], PA[1], P1[0], M4B[0]);
+  dmma(PA[0], PA[1], P1[1], M4B[1]);
+  tb0 = tg * PA[0];
+  tb1 = tg * PA[1];
+}
+
+// Compact-WY update (householder.py:175-186, V = [I; Y]) of one 8-column
+// block (registers Cb = C[cb][.][.]) by the panel: x = Y as the B operand of
+// C^T Y, vb = Y in the B layout of Y^T, tb = T in the B layout of W^T T; the
+// block's pivot rows R_p,trail at rp (row stride ldr).
+__device__ __forceinline__ void dr_upd(double (&Cb)[2][2], const double (&x)[4],
+                                       const double (&vb)[2][2], double tb0, double tb1,
+                                       double* rp, int ldr) {
+  const double ro0 = rp[0], ro1 = rp[ldr];
+  double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0;
+  dmma(wa0, wa1, Cb[0][0], x[0]);
+  dmma(wb0, wb1, Cb[1][0], x[2]);
+  dmma(wa0, wa1, Cb[0][1], x[1]);
+  dmma(wb0, wb1, Cb[1][1], x[3]);
+  const double w0 = ro0 + (wa0 + wb0), w1 = ro1 + (wa1 + wb1);
+  double u0 = 0.0, u1 = 0.0;
+  dmma(u0, u1, w0, tb0);
+  dmma(u0, u1, w1, tb1);
+  rp[0] = ro0 - u0;
+  rp[ldr] = ro1 - u1;
+  dmma(Cb[0][0], Cb[0][1], -u0, vb[0][0]);
+  dmma(Cb[1][0], Cb[1][1], -u0, vb[1][0]);
+  dmma(Cb[0][0], Cb[0][1], -u1, vb[0][1]);
+  dmma(Cb[1][0], Cb[1][1], -u1, vb[1][1]);
 }
 
 template <bool V16>
 __global__ void __launch_bounds__(DR_WARPS * 32, 1)
 k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-            double* Rio, int* flag) {
+             double* Rio, int* flag) {
   extern __shared__ __align__(16) double sm[];
   double* Rp = sm;
   double* stage_all = Rp + DmmaRingSmem::RP;
@@ -191,12 +252,11 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   const int npan = (n + 7) >> 3;
   for (int i = threadIdx.x; i < DmmaRingSmem::RP; i += DR_WARPS * 32) Rp[i] = 0.0;
   if (threadIdx.x < 2 * DR_NCB) ver[threadIdx.x] = 0;
-  __syncthreads();
   double* stage = stage_all + w * DR_H * DR_SLD;
   double* vs = scr_all + w * DR_SCR;  // 16 x 12
   double* gs = vs + 192;
-  double* ts = gs + 64;
-  double* taus = ts + 64;
+  double* taus = gs + 64;
+  __syncthreads();
   bool bad = false;
   if (w < T) {
     const int64_t row = r0 + (int64_t)w * DR_H;
@@ -206,88 +266,103 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   for (int t = w; t < T; t += DR_WARPS) {
     cp_async_wait<0>();
     __syncwarp();
-    double C[2][DR_NCB][2];
+    double C[DR_NCB][2][2];  // [column block][row block][e]
 #pragma unroll
-    for (int bb = 0; bb < 2; ++bb)
+    for (int cb = 0; cb < DR_NCB; ++cb)
 #pragma unroll
-      for (int cb = 0; cb < DR_NCB; ++cb)
+      for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 8 * cb + g;
           double v = stage[(8 * bb + 2 * q + e) * DR_SLD + c];
           v = (c < n) ? v : 0.0;
           bad |= !isfinite(v);
-          C[bb][cb][e] = v;
+          C[cb][bb][e] = v;
         }
     __syncwarp();
     if (t + DR_WARPS < T) {
       const int64_t row = r0 + (int64_t)(t + DR_WARPS) * DR_H;
       dr_issue<V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
     }
+    // ---- prologue: L2 of panel 0 ----
+    double x[4], rg[8];
+    DR_TICK(c0_);
+    dr_wait(ver, t, lane);
+    {
+      const int l0 = dr_ldr(0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rg[i] = Rp[i * l0 + g];
+      x[0] = C[0][0][0]; x[1] = C[0][0][1]; x[2] = C[0][1][0]; x[3] = C[0][1][1];
+      dr_gen<0>(x, rg[0], Rp, gs, taus);
+      dr_gen<1>(x, rg[1], Rp + l0, gs, taus);
+      dr_gen<2>(x, rg[2], Rp + 2 * l0, gs, taus);
+      dr_gen<3>(x, rg[3], Rp + 3 * l0, gs, taus);
+      dr_gen<4>(x, rg[4], Rp + 4 * l0, gs, taus);
+      dr_gen<5>(x, rg[5], Rp + 5 * l0, gs, taus);
+      dr_gen<6>(x, rg[6], Rp + 6 * l0, gs, taus);
+      dr_gen<7>(x, rg[7], Rp + 7 * l0, gs, taus);
+    }
+    DR_TICK(c1_);
+    DR_ADD(0, c0_, c1_);
     for (int p = 0; p < npan; ++p) {
       const int ldr = dr_ldr(p);
       double* Rpan = Rp + dr_pbase(p);
-      // ---- panel p: Level-2 against R_pp ----
-      DR_TICK(c0_);
-      dr_wait(ver + p, t, lane);
-      DR_TICK(c1_);
-      double x[4] = {C[0][0][0], C[0][0][1], C[1][0][0], C[1][0][1]};
-      dr_panel(x, Rpan, ldr, gs, taus);
-      ring_signal(ver + p, t + 1, lane);
       DR_TICK(c2_);
-      DR_ADD(0, c0_, c1_);
-      DR_ADD(1, c1_, c2_);
-      const int nlive = npan - p;  // register blocks 0 .. nlive-1 are live
-      if (nlive <= 1) dr_wait(ver + DR_NCB + p, t, lane);  // keep the versions monotone
-      else {
-        // V^T in the B layout of C^T -= W'^T Y^T: vb[b][s] = Y[8b + g][2q + s]
+      // L2(p) stored R_pp, G and tau as it went; publish R_pp
+      ring_signal(ver + p, t + 1, lane);  // (__syncwarp first: gs / taus visible)
+      const int nl = npan - p;            // live register blocks 0 .. nl-1
+      if (nl > 1) {
+        double vb[2][2], tb0, tb1;
+        // Y^T in the B layout of C^T -= W'^T Y^T, and T
 #pragma unroll
         for (int k = 0; k < 4; ++k) vs[(8 * (k >> 1) + 2 * q + (k & 1)) * 12 + g] = x[k];
         __syncwarp();
-        dr_form_t(gs, taus, ts);
-        double vb[2][2];
+        dr_form_t(gs, taus, tb0, tb1);
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
           for (int s = 0; s < 2; ++s) vb[bb][s] = vs[(8 * bb + g) * 12 + 2 * q + s];
-        __syncwarp();
-        const double tb0 = ts[(2 * q) * 8 + g], tb1 = ts[(2 * q + 1) * 8 + g];
         DR_TICK(c3_);
-        DR_ADD(2, c2_, c3_);
-        // ---- trailing update of panel p ----
+        DR_ADD(1, c2_, c3_);
         dr_wait(ver + DR_NCB + p, t, lane);
-        DR_TICK(c4_);
-        DR_ADD(3, c3_, c4_);
         double* rrow = Rpan + (2 * q) * ldr + g;
+        // block 1 (the next panel's columns) first: it feeds L2(p+1)
+        dr_upd(C[1], x, vb, tb0, tb1, rrow + 8, ldr);
+        dr_wait(ver + p + 1, t, lane);
+        __syncwarp();  // vb reads done before the next panel's vs writes
+        DR_TICK(c4_);
+        DR_ADD(2, c3_, c4_);
+        // ---- look-ahead block: L2(p+1) || blocks 2 .. nl-1 by panel p ----
+        // (interleaved in the source: ptxas keeps this order at this register
+        // pressure, so the update DMMAs run in the shadow of the reflector chain)
+        const int ldr1 = dr_ldr(p + 1);
+        double* Rpan1 = Rp + dr_pbase(p + 1);
 #pragma unroll
-        for (int cb = 1; cb < DR_NCB; ++cb) {
-#ifdef DR_NO_UPDATE
-          if (cb < 0) {
-#else
-          if (cb < nlive) {
-#endif
-            double* rp0 = rrow + 8 * cb;
-            const double ro0 = rp0[0], ro1 = rp0[ldr];
-            double wa0 = ro0, wa1 = ro1, wb0 = 0.0, wb1 = 0.0;
-            dmma(wa0, wa1, C[0][cb][0], x[0]);
-            dmma(wb0, wb1, C[1][cb][0], x[2]);
-            dmma(wa0, wa1, C[0][cb][1], x[1]);
-            dmma(wb0, wb1, C[1][cb][1], x[3]);
-            wa0 += wb0;
-            wa1 += wb1;
-            double u0 = 0.0, u1 = 0.0;
-            dmma(u0, u1, wa0, tb0);
-            dmma(u0, u1, wa1, tb1);
-            rp0[0] = ro0 - u0;
-            rp0[ldr] = ro1 - u1;
-            dmma(C[0][cb][0], C[0][cb][1], -u0, vb[0][0]);
-            dmma(C[1][cb][0], C[1][cb][1], -u0, vb[1][0]);
-            dmma(C[0][cb][0], C[0][cb][1], -u1, vb[0][1]);
-            dmma(C[1][cb][0], C[1][cb][1], -u1, vb[1][1]);
-          }
-        }
+        for (int i = 0; i < 8; ++i) rg[i] = Rpan1[i * ldr1 + g];
+        double xn[4] = {C[1][0][0], C[1][0][1], C[1][1][0], C[1][1][1]};
+#define DR_UPD(CB) if ((CB) < nl) dr_upd(C[CB], x, vb, tb0, tb1, rrow + 8 * (CB), ldr)
+        dr_gen<0>(xn, rg[0], Rpan1, gs, taus);
+        DR_UPD(2); DR_UPD(3);
+        dr_gen<1>(xn, rg[1], Rpan1 + ldr1, gs, taus);
+        DR_UPD(4); DR_UPD(5);
+        dr_gen<2>(xn, rg[2], Rpan1 + 2 * ldr1, gs, taus);
+        DR_UPD(6); DR_UPD(7);
+        dr_gen<3>(xn, rg[3], Rpan1 + 3 * ldr1, gs, taus);
+        DR_UPD(8); DR_UPD(9);
+        dr_gen<4>(xn, rg[4], Rpan1 + 4 * ldr1, gs, taus);
+        DR_UPD(10); DR_UPD(11);
+        dr_gen<5>(xn, rg[5], Rpan1 + 5 * ldr1, gs, taus);
+        DR_UPD(12); DR_UPD(13);
+        dr_gen<6>(xn, rg[6], Rpan1 + 6 * ldr1, gs, taus);
+        DR_UPD(14); DR_UPD(15);
+        dr_gen<7>(xn, rg[7], Rpan1 + 7 * ldr1, gs, taus);
+#undef DR_UPD
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = xn[k];
         DR_TICK(c5_);
-        DR_ADD(4, c4_, c5_);
+        DR_ADD(3, c4_, c5_);
+      } else {
+        dr_wait(ver + DR_NCB + p, t, lane);  // keep the versions monotone
       }
       ring_signal(ver + DR_NCB + p, t + 1, lane);
       // shift the register blocks: the next panel becomes block 0
@@ -295,8 +370,8 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
       for (int cb = 0; cb + 1 < DR_NCB; ++cb)
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb) {
-          C[bb][cb][0] = C[bb][cb + 1][0];
-          C[bb][cb][1] = C[bb][cb + 1][1];
+          C[cb][bb][0] = C[cb + 1][bb][0];
+          C[cb][bb][1] = C[cb + 1][bb][1];
         }
     }
   }

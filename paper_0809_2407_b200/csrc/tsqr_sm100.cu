@@ -51,7 +51,7 @@ static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
-static int g_dmma = 0;     // CAQR_TUNE_DMMA: R-only n in (64,128] leaves on the DMMA warp ring
+static int g_dmma = 1;     // CAQR_TUNE_DMMA: R-only n in (64,128] leaves on the DMMA warp ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>

@@ -346,10 +346,10 @@ def test_blocked_tall_tile_leaf_parity():
 
 @pytest.mark.parametrize("v16", [True, False])
 def test_dmma_ring_leaf_parity(v16):
-    """CAQR_TUNE_DMMA = 1: R-only leaves with n in (64, 128] on the DMMA warp
-    ring (16-row register tiles, 8-column Level-2 panels, compact-WY updates on
-    the FP64 tensor cores).  R against LAPACK, sign-normalised; odd n / lda take
-    the 8-byte cp.async staging path."""
+    """CAQR_TUNE_DMMA = 1 (default): R-only leaves with n in (64, 128] on the
+    DMMA warp ring (16-row register tiles, 8-column Level-2 panels with
+    look-ahead, compact-WY updates and T on the FP64 tensor cores).  R against
+    LAPACK, sign-normalised; odd n / lda take the 8-byte cp.async staging path."""
     from paper_0809_2407_b200 import _lib
     from paper_0809_2407_b200.tsqr import factor_device
 
@@ -376,4 +376,21 @@ def test_dmma_ring_leaf_parity(v16):
         with pytest.raises(ValueError):
             factor_device(torch.from_numpy(A).cuda(), 2)
     finally:
+        _lib.tune(_lib.TUNE_DMMA, 1)
+
+
+def test_dmma_ring_matches_rank1_ring():
+    """The DMMA ring and the rank-1 ring (CAQR_TUNE_DMMA = 0) give the same R up
+    to row signs on a C3-shaped slice (32 leaves of 8192 x 128)."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = torch.from_numpy(philox(11).standard_normal((32 * 8192, 128))).cuda()
+    Rd = factor_device(A, 32).R.cpu().numpy()
+    try:
         _lib.tune(_lib.TUNE_DMMA, 0)
+        Rr = factor_device(A, 32).R.cpu().numpy()
+    finally:
+        _lib.tune(_lib.TUNE_DMMA, 1)
+    nA = np.linalg.norm(Rr, 2)
+    assert oracle.r_diff(Rd, Rr, nA) <= 1000 * EPS

@@ -1,4 +1,4 @@
-// Compile-only unit for iterating on the DMMA ring kernel (ptxas -v, SASS).
+// Compile-only unit for iterating on the DMMA ring kernels (ptxas -v, SASS).
 #include "../paper_0809_2407_b200/csrc/tsqr_device.cuh"
 namespace tsqr {
 #include "../paper_0809_2407_b200/csrc/dmma_ring.cuh"

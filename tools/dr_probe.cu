@@ -9,6 +9,9 @@ namespace tsqr {
 #include "../paper_0809_2407_b200/csrc/dmma_ring.cuh"
 }
 using namespace tsqr;
+#ifndef DR_KERNEL
+#define DR_KERNEL k_leaf_dmma
+#endif
 int main(int argc, char** argv) {
   const int P = argc > 1 ? atoi(argv[1]) : 148;
   const int64_t b = 8192, n = 128, m = b * P;
@@ -22,7 +25,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&R, P * n * n * 8);
   cudaMalloc(&flag, 4);
   cudaMemcpy(A, h.data(), m * n * 8, cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(k_leaf_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem::bytes);
+  cudaFuncSetAttribute(DR_KERNEL<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem::bytes);
   for (int it = 0; it < 2; ++it) {
     unsigned long long z[8] = {};
     cudaMemcpyToSymbol(g_dr_cycles, z, sizeof(z));
@@ -30,14 +33,14 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_leaf_dmma<true><<<P, 256, DmmaRingSmem::bytes>>>(A, n, m, n, P, b, R, flag);
+    DR_KERNEL<true><<<P, 256, DmmaRingSmem::bytes>>>(A, n, m, n, P, b, R, flag);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaMemcpyFromSymbol(z, g_dr_cycles, sizeof(z));
     const double tiles = b / 16.0;  // per CTA
-    printf("%s  %.3f ms  per tile (cycles, summed over warps / tiles): wait1 %.0f panel %.0f formT %.0f wait2 %.0f update %.0f | total/warp %.0f\n",
+    printf("%s  %.3f ms  per tile (cycles, summed over warps / tiles): c0 %.0f c1 %.0f c2 %.0f c3 %.0f c4 %.0f | total/warp %.0f\n",
            cudaGetErrorString(e), ms, z[0] / tiles, z[1] / tiles, z[2] / tiles, z[3] / tiles, z[4] / tiles,
            z[5] / 8.0);
   }
