@@ -234,10 +234,16 @@ __device__ __forceinline__ void dr_upd(double (&Cb)[2][2], const double (&x)[4],
   dmma(Cb[1][0], Cb[1][1], -u1, vb[1][1]);
 }
 
-template <bool V16>
+template <bool V16, bool Q>
 __global__ void __launch_bounds__(DR_WARPS * 32, 1)
 k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-             double* Rio, int* flag) {
+            double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag,
+            int h0) {
+  // h0 = 0: R only, the chain starts from R = 0 at the leaf's first row.
+  // h0 > 0: the chain continues from the leaf's R slot after a dense first tile of h0 rows
+  // (k_leaf_dense); Y / tau (nullable) receive each chain tile's TRI_ON_RECT factor in the
+  // layout of k_leaf_chain<128, 16> (tile t: Y rows h0 + 16t.., tau at (t + 1) * n).
+  // Y may alias A (tile rows are staged before they are overwritten).
   extern __shared__ __align__(16) double sm[];
   double* Rp = sm;
   double* stage_all = Rp + DmmaRingSmem::RP;
@@ -248,9 +254,23 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   const int leaf = blockIdx.x;
   const int64_t r0 = (int64_t)leaf * base;
   const int64_t b = (leaf == P - 1) ? m - r0 : base;
-  const int T = (int)((b + DR_H - 1) / DR_H);
+  const int64_t rest = b - h0;
+  if (rest <= 0) return;  // the dense tile was the whole leaf: R is already in its slot
+  const int T = (int)((rest + DR_H - 1) / DR_H);
   const int npan = (n + 7) >> 3;
-  for (int i = threadIdx.x; i < DmmaRingSmem::RP; i += DR_WARPS * 32) Rp[i] = 0.0;
+  double* Rl = Rio + (int64_t)leaf * n * n;
+  for (int i = threadIdx.x; i < DmmaRingSmem::RP; i += DR_WARPS * 32) {
+    double v = 0.0;
+    if (Q || h0) {  // panel-packed index -> (r, c)
+      int pp = 0;
+      while (pp + 1 < DR_NCB && dr_pbase(pp + 1) <= i) ++pp;
+      const int off = i - dr_pbase(pp), ld = dr_ldr(pp);
+      const int r = 8 * pp + off / ld, c = 8 * pp + off % ld;
+      if (r < n && c < n && c >= r) v = Rl[r * n + c];
+    }
+    Rp[i] = v;
+  }
+  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
   if (threadIdx.x < 2 * DR_NCB) ver[threadIdx.x] = 0;
   double* stage = stage_all + w * DR_H * DR_SLD;
   double* vs = scr_all + w * DR_SCR;  // 16 x 12
@@ -259,7 +279,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   __syncthreads();
   bool bad = false;
   if (w < T) {
-    const int64_t row = r0 + (int64_t)w * DR_H;
+    const int64_t row = r0 + h0 + (int64_t)w * DR_H;
     dr_issue<V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
   }
   DR_TICK(k0_);
@@ -281,9 +301,11 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         }
     __syncwarp();
     if (t + DR_WARPS < T) {
-      const int64_t row = r0 + (int64_t)(t + DR_WARPS) * DR_H;
+      const int64_t row = r0 + h0 + (int64_t)(t + DR_WARPS) * DR_H;
       dr_issue<V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
     }
+    const int64_t trow = r0 + h0 + (int64_t)t * DR_H;  // this tile's first row
+    const int tvalid = (int)min64(DR_H, r0 + b - trow);
     // ---- prologue: L2 of panel 0 ----
     double x[4], rg[8];
     DR_TICK(c0_);
@@ -310,6 +332,15 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
       DR_TICK(c2_);
       // L2(p) stored R_pp, G and tau as it went; publish R_pp
       ring_signal(ver + p, t + 1, lane);  // (__syncwarp first: gs / taus visible)
+      if (Q) {  // the tile's factor for panel p: Y (= x, rows 8b+2q+e, column 8p+g) and tau
+        const int c = 8 * p + g;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int tr = 8 * (k >> 1) + 2 * q + (k & 1);
+          if (tr < tvalid && c < n) Y[(trow + tr) * ldy + c] = x[k];
+        }
+        if (lane < 8 && 8 * p + lane < n) tl[(int64_t)(t + 1) * n + 8 * p + lane] = taus[lane];
+      }
       const int nl = npan - p;            // live register blocks 0 .. nl-1
       if (nl > 1) {
         double vb[2][2], tb0, tb1;
@@ -378,7 +409,6 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   DR_TICK(k1_);
   DR_ADD(5, k0_, k1_);
   __syncthreads();
-  double* Rl = Rio + (int64_t)leaf * n * n;
   for (int idx = threadIdx.x; idx < n * n; idx += DR_WARPS * 32) {
     const int r = idx / n, c = idx - r * n;
     const int p = r >> 3;

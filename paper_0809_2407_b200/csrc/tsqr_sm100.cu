@@ -1098,6 +1098,13 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
                              st>>>(A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R,  \
                                    flag, zs ? 1 : 0);                                            \
   }
+#define DMMA_LAUNCH(V16, Q)                                                                     \
+  {                                                                                             \
+    rc = prep(k_leaf_dmma<V16, Q>, DmmaRingSmem::bytes);                                        \
+    if (rc) return rc;                                                                          \
+    k_leaf_dmma<V16, Q><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n,    \
+        (int)P, base, Y, ldy, tau, tau_stride, R, flag, h0d);                                   \
+  }
 #define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
     const bool zs = !Y && g_zstart;                                                             \
@@ -1108,19 +1115,13 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if (NPV == 128 && zs && g_dmma) {                                                           \
+    if (NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) {                                      \
+      const int h0d = zs ? 0 : WARPS * Geo<NPV>::HD;                                            \
       const bool v16 = (n % 2 == 0) && (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);            \
-      if (v16) {                                                                                \
-        rc = prep(k_leaf_dmma<true>, DmmaRingSmem::bytes);                                      \
-        if (rc) return rc;                                                                      \
-        k_leaf_dmma<true><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n,  \
-                                                                          (int)P, base, R, flag); \
-      } else {                                                                                  \
-        rc = prep(k_leaf_dmma<false>, DmmaRingSmem::bytes);                                     \
-        if (rc) return rc;                                                                      \
-        k_leaf_dmma<false><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n, \
-                                                                           (int)P, base, R, flag); \
-      }                                                                                         \
+      if (v16 && Y) DMMA_LAUNCH(true, true)                                                     \
+      else if (v16) DMMA_LAUNCH(true, false)                                                    \
+      else if (Y) DMMA_LAUNCH(false, true)                                                      \
+      else DMMA_LAUNCH(false, false)                                                            \
     } else if (NPV == 128 && zs && g_blocked) {                                                 \
       rc = prep(k_leaf_blocked, BlockedSmem::bytes);                                         \
       if (rc) return rc;                                                                        \
@@ -1136,6 +1137,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   switch (p) { LEAF_CASE(32, 16, 32) LEAF_CASE(64, 16, 32) LEAF_CASE(128, 16, 24) }
 #undef LEAF_CASE
 #undef CHAIN_LAUNCH
+#undef DMMA_LAUNCH
   return check_launch("k_leaf_dense/k_leaf_chain");
 }
 

@@ -25,7 +25,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&R, P * n * n * 8);
   cudaMalloc(&flag, 4);
   cudaMemcpy(A, h.data(), m * n * 8, cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(DR_KERNEL<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem::bytes);
+  cudaFuncSetAttribute(DR_KERNEL<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem::bytes);
   for (int it = 0; it < 2; ++it) {
     unsigned long long z[8] = {};
     cudaMemcpyToSymbol(g_dr_cycles, z, sizeof(z));
@@ -33,7 +33,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    DR_KERNEL<true><<<P, 256, DmmaRingSmem::bytes>>>(A, n, m, n, P, b, R, flag);
+    DR_KERNEL<true, false><<<P, 256, DmmaRingSmem::bytes>>>(A, n, m, n, P, b, nullptr, 0, nullptr, 0, R, flag, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms;
