@@ -566,11 +566,16 @@ k_tree_factor(double* Rslots, int n, const int* __restrict__ ev, double* Ynode, 
 // reflector vector is broadcast (shuffles).  Same STACKED semantics as
 // k_tree_factor / k_tree_apply (householder.py:263-294, 377-396).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, double* Ynode,
                   double* taunode, int bin_level) {
+  // One warp per event, a rolled loop over the reflectors (the short-lived tree
+  // kernels are instruction-fetch bound when fully unrolled).  Lane c holds
+  // column c of R_b in registers (rows > c stay exactly zero until reflector
+  // c, so sums over all 32 rows need no masking); R_a's rows -- the pivot
+  // rows, row j touched only by reflector j -- live in shared memory.
   const int lane = threadIdx.x & 31;
-  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int e = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (e >= nev) return;
   int a, b, id;
   if (ev) {
@@ -578,65 +583,68 @@ k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, do
   } else {
     a = e << bin_level; b = a + (1 << (bin_level - 1)); id = 0;
   }
-  __shared__ double vsm[8][32];
+  __shared__ double rsm[4][32][33];
+  __shared__ double vsm[4][32];
+  double (*Ras)[33] = rsm[threadIdx.x >> 5];
   double* vs = vsm[threadIdx.x >> 5];
   double* Ra = Rslots + (int64_t)a * n * n;
   const double* Rb = Rslots + (int64_t)b * n * n;
-  double ca[32], cb[32];  // column `lane` of R_a and R_b
+  double cb[32];
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     const bool ok = (r < n && lane < n && lane >= r);
-    ca[r] = ok ? Ra[r * n + lane] : 0.0;
+    Ras[r][lane] = ok ? Ra[r * n + lane] : 0.0;
     cb[r] = ok ? Rb[r * n + lane] : 0.0;
   }
+  __syncwarp();
+  const double diag = Ras[lane][lane];  // R_a[c][c]: unchanged until reflector c
+#pragma unroll 1
+  for (int j = 0; j < n; ++j) {
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (j >= n) break;
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: latency j/4 instead of j
-#pragma unroll
-    for (int r = 0; r <= j; ++r) s4[r & 3] = fma(cb[r], cb[r], s4[r & 3]);
-    double sg = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    sg = __shfl_sync(FULL, sg, j);
-    const double x0 = __shfl_sync(FULL, ca[j], j);
+    for (int r = 0; r < 32; ++r) s4[r & 3] = fma(cb[r], cb[r], s4[r & 3]);
+    const double sg = __shfl_sync(FULL, (s4[0] + s4[1]) + (s4[2] + s4[3]), j);
+    const double x0 = __shfl_sync(FULL, diag, j);
     double beta, tau, scale;
     house_lean(x0, sg, beta, tau, scale);
-    __syncwarp();
     if (lane == j) {
 #pragma unroll
-      for (int r = 0; r <= j; ++r) vs[r] = cb[r] * scale;
+      for (int r = 0; r < 32; ++r) vs[r] = cb[r] * scale;  // zero below row j
     }
     __syncwarp();
-    double d4[4] = {ca[j], 0.0, 0.0, 0.0};
+    const double raj = Ras[j][lane];
+    double d4[4] = {raj, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int r = 0; r <= j; ++r) d4[r & 3] = fma(vs[r], cb[r], d4[r & 3]);
+    for (int r = 0; r < 32; ++r) d4[r & 3] = fma(vs[r], cb[r], d4[r & 3]);
     const double d = (d4[0] + d4[1]) + (d4[2] + d4[3]);
     const double w = (lane > j) ? tau * d : 0.0;
-    ca[j] -= w;
 #pragma unroll
-    for (int r = 0; r <= j; ++r) cb[r] = fma(-vs[r], w, cb[r]);
+    for (int r = 0; r < 32; ++r) cb[r] = fma(-vs[r], w, cb[r]);
+    if (lane > j) Ras[j][lane] = raj - w;
     if (lane == j) {
-      ca[j] = beta;
+      Ras[j][j] = beta;
 #pragma unroll
-      for (int r = 0; r <= j; ++r) cb[r] = vs[r];
+      for (int r = 0; r < 32; ++r) cb[r] = vs[r];
     }
     if (lane == 0 && taunode) taunode[(int64_t)id * n + j] = tau;
+    __syncwarp();
   }
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     if (r < n && lane < n) {
-      Ra[r * n + lane] = (lane >= r) ? ca[r] : 0.0;
+      Ra[r * n + lane] = (lane >= r) ? Ras[r][lane] : 0.0;
       if (Ynode) Ynode[(int64_t)id * n * n + r * n + lane] = (lane >= r) ? cb[r] : 0.0;
     }
   }
 }
 
 template <bool TRANS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 k_tree_apply_w32(const double* __restrict__ Ynode, const double* __restrict__ taunode, int n,
                  const int* __restrict__ ev, int nev, double* C, int64_t ldc, int64_t slot_rows,
                  int64_t ncols, int zero_partner) {
   const int lane = threadIdx.x & 31;
-  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int e = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (e >= nev) return;
   const int a = ev[3 * e], b = ev[3 * e + 1], id = ev[3 * e + 2];
   const int64_t col = (int64_t)blockIdx.y * 32 + lane;
@@ -645,30 +653,34 @@ k_tree_apply_w32(const double* __restrict__ Ynode, const double* __restrict__ ta
   double* Cb = C + (int64_t)b * slot_rows * ldc + col;
   const double* Yn = Ynode + (int64_t)id * n * n;
   const double* tn = taunode + (int64_t)id * n;
-  __shared__ double vsm[8][32];
-  double* vs = vsm[threadIdx.x >> 5];
+  // the node's Y (n x n upper triangular) and tau staged once in shared memory:
+  // a global load per reflector would put an L2 round trip on the chain
+  __shared__ double ysm[4][32][33];
+  __shared__ double tsm[4][32];
+  double (*Ys)[33] = ysm[threadIdx.x >> 5];
+  double* ts = tsm[threadIdx.x >> 5];
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) Ys[r][lane] = (r < n && lane < n) ? __ldg(Yn + (int64_t)r * n + lane) : 0.0;
+  ts[lane] = lane < n ? __ldg(tn + lane) : 0.0;
   double ca[32], cb[32];
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     ca[r] = (okc && r < n) ? Ca[(int64_t)r * ldc] : 0.0;
     cb[r] = (okc && r < n && !zero_partner) ? Cb[(int64_t)r * ldc] : 0.0;
   }
-  // lane r holds column j of Ybot for the broadcast: ycol = Ybot[lane][j]
+  __syncwarp();
 #pragma unroll
   for (int jx = 0; jx < 32; ++jx) {
     const int j = TRANS ? jx : 31 - jx;
     if (j >= n) continue;
-    const double tj = __ldg(tn + j);
-    __syncwarp();
-    vs[lane] = (lane <= j) ? __ldg(Yn + (int64_t)lane * n + j) : 0.0;
-    __syncwarp();
+    const double tj = ts[j];
     double d = ca[j];
 #pragma unroll
-    for (int r = 0; r <= j; ++r) d = fma(vs[r], cb[r], d);
+    for (int r = 0; r <= j; ++r) d = fma(Ys[r][j], cb[r], d);
     const double w = tj * d;
     ca[j] -= w;
 #pragma unroll
-    for (int r = 0; r <= j; ++r) cb[r] = fma(-vs[r], w, cb[r]);
+    for (int r = 0; r <= j; ++r) cb[r] = fma(-Ys[r][j], w, cb[r]);
   }
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
@@ -1176,7 +1188,7 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
     break;                                                                               \
   }
     if (p == 32) {
-      k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, nullptr, (int)nev,
+      k_tree_factor_w32<<<(int)((nev + 3) / 4), 128, 0, st>>>(Rslots, (int)n, nullptr, (int)nev,
                                                              nullptr, nullptr, k);
     } else {
       switch (p) { TB_CASE(64) TB_CASE(128) }
@@ -1211,7 +1223,7 @@ int tsqr_f64_r_combine_level(double* Rslots, int64_t n, const int32_t* events, i
     return check_launch("k_narrow_combine");
   }
   if (p == 32) {
-    k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, events, (int)nev,
+    k_tree_factor_w32<<<(int)((nev + 3) / 4), 128, 0, st>>>(Rslots, (int)n, events, (int)nev,
                                                            nullptr, nullptr, 0);
     return check_launch("k_tree_factor_w32");
   }
@@ -1244,7 +1256,7 @@ int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events,
     break;                                                                               \
   }
   if (p == 32) {
-    k_tree_factor_w32<<<(int)((nev + 7) / 8), 256, 0, st>>>(Rslots, (int)n, events, (int)nev, Ynode,
+    k_tree_factor_w32<<<(int)((nev + 3) / 4), 128, 0, st>>>(Rslots, (int)n, events, (int)nev, Ynode,
                                                            taunode, 0);
     return check_launch("k_tree_factor_w32");
   }
@@ -1279,12 +1291,12 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
     break;                                                                                      \
   }
   if (p == 32) {
-    dim3 g32((unsigned)((nev + 7) / 8), (unsigned)((ncols + 31) / 32));
+    dim3 g32((unsigned)((nev + 3) / 4), (unsigned)((ncols + 31) / 32));
     if (transpose)
-      k_tree_apply_w32<true><<<g32, 256, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+      k_tree_apply_w32<true><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
                                                   slot_rows, ncols, zero_partner);
     else
-      k_tree_apply_w32<false><<<g32, 256, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+      k_tree_apply_w32<false><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
                                                    slot_rows, ncols, zero_partner);
     return check_launch("k_tree_apply_w32");
   }
