@@ -152,6 +152,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * (16-row tiles per warp in registers, 8-column Level-2 panels with look-ahead,
  * compact-WY trailing updates on the FP64 tensor cores); 0 = the rank-1 warp ring. */
 #define CAQR_TUNE_DMMA 9
+/* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with n in (64, 128] and 16-row chain
+ * tiles (the CAQR trailing update) runs the DMMA ring (compact-WY per 8-reflector panel on the
+ * FP64 tensor cores); 0 = the reflector-by-reflector warp ring. */
+#define CAQR_TUNE_DMMA_APPLY 10
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

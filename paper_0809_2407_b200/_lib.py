@@ -123,6 +123,7 @@ TUNE_NARROW = 4
 TUNE_ZSTART = 6
 TUNE_BLOCKED = 8
 TUNE_DMMA = 9
+TUNE_DMMA_APPLY = 10
 
 
 def tune(key: int, value: int) -> None:

@@ -1,0 +1,178 @@
+// DMMA leaf apply: C[leaf rows] <- Q_leaf^T C for the chain leaves of n in
+// (64, 128] (Y / tau in the layout of k_leaf_chain<128, 16> / k_leaf_dmma) --
+// the CAQR trailing update, _apply_yt with transpose (householder.py:175-186,
+// :209), one (leaf, 128-column block) per CTA.
+//
+// The dense first tile is applied CTA-cooperatively exactly as in
+// k_leaf_apply; its top n rows become the pivot rows Cs (shared memory, row
+// stride 130).  The chain tiles then run as the DMMA warp ring: warp w owns
+// tiles w, w+8, ..., holds its 16 x 128 tile of C in registers in the DMMA
+// accumulator layout of k_leaf_dmma, and applies each 8-reflector panel of
+// the tile's TRI_ON_RECT factor in compact-WY form on the tensor cores:
+//
+//   G = Y_p^T Y_p (4 DMMA), T from G and tau by the Neumann product (10 DMMA)
+//   per 8-column block: W = Cs_p + Y_p^T C (4), W' = T^T W (2), Cs_p -= W',
+//   C -= Y_p W' (4)
+//
+// Tile t may update the pivot rows of panel p once tile t-1 has (ver[p] == t).
+// Included by tsqr_sm100.cu (namespace tsqr) after dmma_ring.cuh.
+
+constexpr int DA_KB = 128;          // columns per CTA
+constexpr int DA_LDC = DA_KB + 2;   // pivot-row stride (doubles)
+struct DmmaApplySmem {
+  static constexpr int STAGE = ApplyStage<16>::DOUBLES;  // dense-tile V staging per warp
+  static constexpr size_t doubles =
+      (size_t)DR_NP * DA_LDC + 2 * WARPS * DA_KB + (size_t)WARPS * STAGE;
+  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * DR_NCB;
+};
+
+// Panel p of a chain tile: Y fragments (x: B operand of C^T Y; vb: B operand
+// of Y^T) and the tau values the T build needs (tau_g, tau_{2q}, tau_{2q+1}).
+struct DaPanel {
+  double x[4], vb[2][2], tg, tq0, tq1;
+};
+__device__ __forceinline__ void da_load_panel(DaPanel& P, const double* __restrict__ Yt,
+                                              int64_t ldy, const double* __restrict__ tt, int valid,
+                                              int n, int pc) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = 8 * (k >> 1) + 2 * q + (k & 1), c = pc + g;
+    P.x[k] = (r < valid && c < n) ? __ldg(Yt + (int64_t)r * ldy + c) : 0.0;
+  }
+#pragma unroll
+  for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int r = 8 * bb + g, c = pc + 2 * q + s;
+      P.vb[bb][s] = (r < valid && c < n) ? __ldg(Yt + (int64_t)r * ldy + c) : 0.0;
+    }
+  P.tg = (pc + g < n) ? __ldg(tt + pc + g) : 0.0;
+  P.tq0 = (pc + 2 * q < n) ? __ldg(tt + pc + 2 * q) : 0.0;
+  P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tt + pc + 2 * q + 1) : 0.0;
+}
+
+// tb[s] = T[2q+s][g] of the panel from Y and tau, all in registers: G = Y^T Y
+// is symmetric, so both the accumulator and the B layout of M come from the
+// same G fragment (same Neumann product as dr_form_t).
+__device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double& tb1) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  double G[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) dmma(G[0], G[1], P.x[k], P.x[k]);
+  const double tq[2] = {P.tq0, P.tq1};
+  double MA[2], MB[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int c = 2 * q + e;
+    MA[e] = (c < g) ? tq[e] * G[e] : 0.0;  // M[g][c] = tau_c G[c][g]
+    MB[e] = (g < c) ? P.tg * G[e] : 0.0;   // M[c][g] = tau_g G[g][c]
+  }
+  double M2A[2] = {0.0, 0.0}, M2B[2] = {0.0, 0.0};
+  dmma(M2A[0], M2A[1], MA[0], MB[0]);
+  dmma(M2B[0], M2B[1], MB[0], MA[0]);
+  dmma(M2A[0], M2A[1], MA[1], MB[1]);
+  dmma(M2B[0], M2B[1], MB[1], MA[1]);
+  double M4B[2] = {0.0, 0.0}, M3A[2] = {0.0, 0.0};
+  dmma(M4B[0], M4B[1], M2B[0], M2A[0]);
+  dmma(M3A[0], M3A[1], MA[0], M2B[0]);
+  dmma(M4B[0], M4B[1], M2B[1], M2A[1]);
+  dmma(M3A[0], M3A[1], MA[1], M2B[1]);
+  double P1[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) P1[e] = ((2 * q + e == g) ? 1.0 : 0.0) - MA[e] + M2A[e] - M3A[e];
+  double PA[2] = {P1[0], P1[1]};
+  dmma(PA[0], PA[1], P1[0], M4B[0]);
+  dmma(PA[0], PA[1], P1[1], M4B[1]);
+  tb0 = P.tg * PA[0];
+  tb1 = P.tg * PA[1];
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
+                  int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
+                  int64_t ncols) {
+  constexpr int HD = Geo<128>::HD, H0 = WARPS * HD, KBS = DA_KB / 32;
+  extern __shared__ __align__(16) double sm[];
+  double* Cs = sm;
+  double* part = Cs + DR_NP * DA_LDC;
+  double* vstage = part + 2 * WARPS * DA_KB + (threadIdx.x >> 5) * DmmaApplySmem::STAGE;
+  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * DA_KB + WARPS * DmmaApplySmem::STAGE);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int leaf = blockIdx.x;
+  const int col0 = blockIdx.y * DA_KB;
+  const int ncb = (int)min64(ncols - col0, DA_KB);
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const double* tl = tau + (int64_t)leaf * tau_stride;
+  const double* Yl = Y + r0 * ldy;
+  double* Cl = C + r0 * ldc + col0;
+  const int64_t rest = b - H0;
+  const int T = rest > 0 ? (int)((rest + DR_H - 1) / DR_H) : 0;
+  const int npan = (n + 7) >> 3;
+  bool bad = false;
+  auto ycol = [&](int r, int j) { return (r < b) ? __ldg(Yl + (int64_t)r * ldy + j) : 0.0; };
+  {  // dense first tile (LAPACK layout), CTA-cooperative; its top n rows -> Cs
+    const int v0 = (int)max64(0, min64((int64_t)HD, b - (int64_t)w * HD));
+    double X[HD][KBS];
+    load_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, bad);
+    cta_apply<HD, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false, vstage);
+#pragma unroll
+    for (int k = 0; k < HD; ++k) {
+      const int r = w * HD + k;
+#pragma unroll
+      for (int s = 0; s < KBS; ++s) Cs[r * DA_LDC + 32 * s + lane] = (r < n) ? X[k][s] : 0.0;
+    }
+    const int lo = max(0, n - w * HD);
+    store_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, lo);
+  }
+  if (threadIdx.x < DR_NCB) ver[threadIdx.x] = 0;
+  __syncthreads();
+  for (int t = w; t < T; t += WARPS) {
+    const int64_t row = H0 + (int64_t)t * DR_H;
+    const int valid = (int)min64(DR_H, b - row);
+    double Ct[DR_NCB][2][2];
+#pragma unroll
+    for (int cb = 0; cb < DR_NCB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * bb + 2 * q + e, c = 8 * cb + g;
+          Ct[cb][bb][e] = (r < valid && c < ncb) ? Cl[(row + r) * ldc + c] : 0.0;
+        }
+    const double* Yt = Yl + row * ldy;
+    const double* tt = tl + (int64_t)(t + 1) * n;
+    DaPanel cur, nxt;
+    da_load_panel(cur, Yt, ldy, tt, valid, n, 0);
+    for (int p = 0; p < npan; ++p) {
+      if (p + 1 < npan) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p + 1));
+      double tb0, tb1;
+      da_form_t(cur, tb0, tb1);
+      dr_wait(ver + p, t, lane);
+      double* rrow = Cs + (8 * p + 2 * q) * DA_LDC + g;
+#pragma unroll
+      for (int cb = 0; cb < DR_NCB; ++cb)
+        if (8 * cb < ncb) dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
+      ring_signal(ver + p, t + 1, lane);
+      cur = nxt;
+    }
+#pragma unroll
+    for (int cb = 0; cb < DR_NCB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * bb + 2 * q + e, c = 8 * cb + g;
+          if (r < valid && c < ncb) Cl[(row + r) * ldc + c] = Ct[cb][bb][e];
+        }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * DA_KB; idx += THREADS) {
+    const int r = idx / DA_KB, c = idx - r * DA_KB;
+    if (c < ncb) Cl[(int64_t)r * ldc + c] = Cs[r * DA_LDC + c];
+  }
+}

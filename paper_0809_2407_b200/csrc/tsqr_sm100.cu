@@ -51,7 +51,8 @@ static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
-static int g_dmma = 1;     // CAQR_TUNE_DMMA: R-only n in (64,128] leaves on the DMMA warp ring
+static int g_dmma = 1;     // CAQR_TUNE_DMMA: n in (64,128] leaves on the DMMA warp ring
+static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (64,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -1007,6 +1008,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 }
 
 #include "dmma_ring.cuh"
+#include "dmma_apply.cuh"
 
 // ===========================================================================
 // C-ABI
@@ -1346,7 +1348,14 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     }
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
-      else LA_LAUNCH(128, 4, 16)
+      else if (transpose && g_dmma_apply) {
+        const size_t sm = DmmaApplySmem::bytes;
+        int rc = prep(k_leaf_apply_dmma, sm);
+        if (rc) return rc;
+        dim3 gd((unsigned)P, (unsigned)((ncols + DA_KB - 1) / DA_KB));
+        k_leaf_apply_dmma<<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P, base,
+                                                   C, ldc, ncols);
+      } else LA_LAUNCH(128, 4, 16)
       break;
     }
   }
@@ -1426,6 +1435,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_BLOCKED) {
     g_blocked = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DMMA_APPLY) {
+    g_dmma_apply = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA) {

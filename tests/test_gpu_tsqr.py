@@ -394,3 +394,30 @@ def test_dmma_ring_matches_rank1_ring():
         _lib.tune(_lib.TUNE_DMMA, 1)
     nA = np.linalg.norm(Rr, 2)
     assert oracle.r_diff(Rd, Rr, nA) <= 1000 * EPS
+
+
+@pytest.mark.parametrize("shape", [(8 * 2048, 128, 8, 300), (3 * 1500 + 77, 100, 3, 129),
+                                   (4096, 128, 2, 64)])
+def test_dmma_leaf_apply_matches_ring(shape):
+    """CAQR_TUNE_DMMA_APPLY = 1 (default): Q^T C of n in (64, 128] chain leaves
+    on the DMMA ring (compact WY per 8-reflector panel, T from the Neumann
+    product) equals the reflector-by-reflector ring (= 0), and Q^T A = [R; 0]
+    leaf by leaf."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, factor_device
+
+    m, n, P, k = shape
+    A = torch.from_numpy(philox(m + k).standard_normal((m, n))).cuda()
+    C = torch.from_numpy(philox(m - k).standard_normal((m, k))).cuda()
+    f = factor_device(A, P, want_q=True)
+    Qd = apply_q_device(f, C, transpose=True)
+    try:
+        _lib.tune(_lib.TUNE_DMMA_APPLY, 0)
+        Qr = apply_q_device(f, C, transpose=True)
+    finally:
+        _lib.tune(_lib.TUNE_DMMA_APPLY, 1)
+    scale = torch.linalg.norm(C).item()
+    assert torch.linalg.norm(Qd - Qr).item() <= 100 * n * EPS * scale
+    # round trip: Q (Q^T C) = C
+    back = apply_q_device(f, Qd, transpose=False)
+    assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * scale
