@@ -154,9 +154,11 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
       da_form_t(cur, tb0, tb1);
       dr_wait(ver + p, t, lane);
       double* rrow = Cs + (8 * p + 2 * q) * DA_LDC + g;
+      // all 16 blocks, unguarded (columns >= ncb are zero in Ct and Cs and never
+      // stored): one basic block, so ptxas interleaves the blocks' DMMA chains
 #pragma unroll
       for (int cb = 0; cb < DR_NCB; ++cb)
-        if (8 * cb < ncb) dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
+        dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
       ring_signal(ver + p, t + 1, lane);
       cur = nxt;
     }
