@@ -599,34 +599,49 @@ k_tree_factor_w32(double* Rslots, int n, const int* __restrict__ ev, int nev, do
   }
   __syncwarp();
   const double diag = Ras[lane][lane];  // R_a[c][c]: unchanged until reflector c
-#pragma unroll 1
-  for (int j = 0; j < n; ++j) {
+  // every lane keeps the squared norm of its own column of R_b, refreshed in the
+  // update pass, so reflector j's sigma is ready when step j starts
+  double sig;
+  {
     double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int r = 0; r < 32; ++r) s4[r & 3] = fma(cb[r], cb[r], s4[r & 3]);
-    const double sg = __shfl_sync(FULL, (s4[0] + s4[1]) + (s4[2] + s4[3]), j);
+    sig = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
+  double2* vs2 = reinterpret_cast<double2*>(vs);
+#pragma unroll 1
+  for (int j = 0; j < n; ++j) {
+    const double sg = __shfl_sync(FULL, sig, j);
     const double x0 = __shfl_sync(FULL, diag, j);
     double beta, tau, scale;
     house_lean(x0, sg, beta, tau, scale);
-    if (lane == j) {
+    if (lane == j) {  // v = column j of R_b, scaled (zero below row j)
 #pragma unroll
-      for (int r = 0; r < 32; ++r) vs[r] = cb[r] * scale;  // zero below row j
+      for (int r = 0; r < 32; r += 2) vs2[r >> 1] = make_double2(cb[r] * scale, cb[r + 1] * scale);
     }
     __syncwarp();
+    double v[32];
+#pragma unroll
+    for (int r = 0; r < 32; r += 2) {
+      const double2 t = vs2[r >> 1];
+      v[r] = t.x;
+      v[r + 1] = t.y;
+    }
     const double raj = Ras[j][lane];
     double d4[4] = {raj, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int r = 0; r < 32; ++r) d4[r & 3] = fma(vs[r], cb[r], d4[r & 3]);
+    for (int r = 0; r < 32; ++r) d4[r & 3] = fma(v[r], cb[r], d4[r & 3]);
     const double d = (d4[0] + d4[1]) + (d4[2] + d4[3]);
     const double w = (lane > j) ? tau * d : 0.0;
+    const bool own = (lane == j);
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int r = 0; r < 32; ++r) cb[r] = fma(-vs[r], w, cb[r]);
-    if (lane > j) Ras[j][lane] = raj - w;
-    if (lane == j) {
-      Ras[j][j] = beta;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) cb[r] = vs[r];
+    for (int r = 0; r < 32; ++r) {
+      cb[r] = own ? v[r] : fma(-v[r], w, cb[r]);
+      s4[r & 3] = fma(cb[r], cb[r], s4[r & 3]);
     }
+    sig = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    Ras[j][lane] = own ? beta : raj - w;  // lanes < j: w = 0, unchanged
     if (lane == 0 && taunode) taunode[(int64_t)id * n + j] = tau;
     __syncwarp();
   }
