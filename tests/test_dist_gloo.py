@@ -42,6 +42,7 @@ def _worker(rank, world, port, A, leaf_rows, all_reduce, out):
         R, nodes = cross_tree(R_loc, combine, all_reduce=all_reduce, recorder=rec)
         out[rank] = (None if R is None else R.numpy(), len(nodes), rec.messages_received,
                      rec.words_received, rec.messages_sent)
+        out[("rec", rank)] = (dict(rec.stages), rec.messages_received, rec.words_received)
     finally:
         dist.destroy_process_group()
 
@@ -158,3 +159,58 @@ def test_cross_tree_q_gloo(world):
     assert np.linalg.norm(back - Cfull) <= 10 * n * eps * np.linalg.norm(Cfull)
     # down the tree: every non-root rank receives exactly one n x n block
     assert out[0][3] == 0 and all(out[r][3] == 1 for r in range(1, world))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_par_runtime_model_check_gloo(world):
+    """the cross-GPU tree's recorded critical path matches
+    Eq. (4.1): log2 P messages exactly, packed-triangle words (n+1)/n x n^2/2."""
+    from paper_0809_2407_b200.counters import CommRecorder, par_runtime_model_check
+
+    rng = np.random.Generator(np.random.Philox(world + 10))
+    m, n = 4096, 16
+    A = rng.standard_normal((m, n))
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, A, 256, False, out), nprocs=world, join=True)
+    recs = []
+    for r in range(world):
+        stages, mr, wr = out[("rec", r)]
+        rec = CommRecorder(messages_received=mr, words_received=wr)
+        rec.stages = stages
+        recs.append(rec)
+    rep = par_runtime_model_check(m, n, world, recs)
+    assert rep["messages_ok"] and rep["messages"] == (world - 1).bit_length()
+    assert rep["words_ok"] and rep["words_ratio"] == pytest.approx((n + 1) / n)
+
+
+def test_par_runtime_model_check_examples():
+    """SPEC examples: P = 1 -> 0 messages / 0 words; P = 4, n = 10 -> 55 words per
+    stage vs the model's 50 (ratio 1.1); P = 16, n = 32 -> 4 messages."""
+    from paper_0809_2407_b200.counters import CommRecorder, par_runtime_model_check
+
+    rep = par_runtime_model_check(100, 8, 1, [CommRecorder()])
+    assert rep["messages"] == 0 and rep["words"] == 0 and rep["messages_ok"] and rep["words_ok"]
+
+    def tree_recorders(P, n):
+        recs = [CommRecorder() for _ in range(P)]
+        k = 1
+        while (1 << (k - 1)) < P:
+            for f in range(0, P, 1 << k):
+                s = f + (1 << (k - 1))
+                if s < P:
+                    recs[s].record_send(n * (n + 1) // 2)
+                    recs[f].record_recv(n * (n + 1) // 2, stage=(k, "R"))
+            k += 1
+        return recs
+
+    rep = par_runtime_model_check(400, 10, 4, tree_recorders(4, 10))
+    assert rep["messages"] == 2 and rep["words"] == 2 * 55
+    assert rep["words_ratio"] == pytest.approx(1.1)
+    rep = par_runtime_model_check(16 * 64, 32, 16, tree_recorders(16, 32))
+    assert rep["messages"] == 4 and rep["messages_ok"] and rep["words_ok"]
+    # a wrong census is flagged
+    recs = tree_recorders(4, 10)
+    recs[0].record_recv(55, stage=(9, "R"))
+    assert not par_runtime_model_check(400, 10, 4, recs)["messages_ok"]
