@@ -56,12 +56,10 @@ __device__ __forceinline__ void da_load_panel(DaPanel& P, const double* __restri
 // tb[s] = T[2q+s][g] of the panel from Y and tau, all in registers: G = Y^T Y
 // is symmetric, so both the accumulator and the B layout of M come from the
 // same G fragment (same Neumann product as dr_form_t).
-__device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double& tb1) {
+__device__ __forceinline__ void da_form_t_g(const DaPanel& P, const double (&G)[2], double& tb0,
+                                            double& tb1) {
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
-  double G[2] = {0.0, 0.0};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) dmma(G[0], G[1], P.x[k], P.x[k]);
   const double tq[2] = {P.tq0, P.tq1};
   double MA[2], MB[2];
 #pragma unroll
@@ -88,6 +86,12 @@ __device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double&
   dmma(PA[0], PA[1], P1[1], M4B[1]);
   tb0 = P.tg * PA[0];
   tb1 = P.tg * PA[1];
+}
+__device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double& tb1) {
+  double G[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) dmma(G[0], G[1], P.x[k], P.x[k]);
+  da_form_t_g(P, G, tb0, tb1);
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -176,5 +180,152 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
   for (int idx = threadIdx.x; idx < n * DA_KB; idx += THREADS) {
     const int r = idx / DA_KB, c = idx - r * DA_KB;
     if (c < ncb) Cl[(int64_t)r * ldc + c] = Cs[r * DA_LDC + c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA tree apply: [C_a; C_b] <- Q_node^T [C_a; C_b] for a STACKED node
+// (qr_stacked_triangles, q = 2: reflector j = [e_j; Y[0..j][j]], householder.py:
+// 263-294, 335-374 with the identity top) -- the CAQR tree-level update.
+// One (event, 64-column block) per CTA; warp w holds rows 16w.. of C_b in
+// registers, C_a (the pivot rows) lives in shared memory.  Per 8-reflector
+// panel p (Y's rows > 8p+7 are zero, so warps below them sit out):
+//   partial G_w = Y_w^T Y_w and W_w = Y_w^T C_b,w (active warps)  | barrier
+//   every warp: T from sum G; warp w forms W' = T^T (C_a,p + sum W_w) for its
+//   column block, C_a,p -= W'                                       | barrier
+//   active warps: C_b,w -= Y_w W'
+// Two barriers per 8 reflectors instead of one per reflector.
+// ---------------------------------------------------------------------------
+constexpr int TA_KB = 64;
+constexpr int TA_LDC = TA_KB + 2;
+struct TreeApplyDmmaSmem {
+  static constexpr size_t doubles = (size_t)DR_NP * TA_LDC + WARPS * 8 * TA_KB + WARPS * 64 + 8 * TA_KB;
+  static constexpr size_t bytes = sizeof(double) * doubles;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ taunode, int n,
+                  const int* __restrict__ ev, double* C, int64_t ldc, int64_t slot_rows,
+                  int64_t ncols) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ca = sm;                           // 128 x 66
+  double* wpart = Ca + DR_NP * TA_LDC;       // [warp][refl 8][col 64]
+  double* gpart = wpart + WARPS * 8 * TA_KB; // [warp][8 x 8]
+  double* wfin = gpart + WARPS * 64;         // [refl 8][col 64]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int a = ev[3 * blockIdx.x], b = ev[3 * blockIdx.x + 1], id = ev[3 * blockIdx.x + 2];
+  const int col0 = blockIdx.y * TA_KB;
+  const int ncb = (int)min64(ncols - col0, TA_KB);
+  double* Cag = C + (int64_t)a * slot_rows * ldc + col0;
+  double* Cbg = C + (int64_t)b * slot_rows * ldc + col0;
+  const double* Yn = Ynode + (int64_t)id * n * n;
+  const double* tn = taunode + (int64_t)id * n;
+  for (int idx = threadIdx.x; idx < DR_NP * TA_KB; idx += THREADS) {
+    const int r = idx / TA_KB, c = idx - r * TA_KB;
+    Ca[r * TA_LDC + c] = (r < n && c < ncb) ? Cag[(int64_t)r * ldc + c] : 0.0;
+  }
+  double Cb[TA_KB / 8][2][2];
+#pragma unroll
+  for (int cb = 0; cb < TA_KB / 8; ++cb)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
+        Cb[cb][bb][e] = (r < n && c < ncb) ? Cbg[(int64_t)r * ldc + c] : 0.0;
+      }
+  __syncthreads();
+  const int npan = (n + 7) >> 3;
+  for (int p = 0; p < npan; ++p) {
+    const int pc = 8 * p;
+    const int wmax = min(WARPS - 1, (pc + 7) >> 4);  // warps holding nonzero rows of Y_p
+    const bool active = w <= wmax;
+    double x[4], vb[2][2];
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = 16 * w + 8 * (k >> 1) + 2 * q + (k & 1), c = pc + g;
+        x[k] = (r < n && c < n) ? __ldg(Yn + (int64_t)r * n + c) : 0.0;
+      }
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int r = 16 * w + 8 * bb + g, c = pc + 2 * q + s;
+          vb[bb][s] = (r < n && c < n) ? __ldg(Yn + (int64_t)r * n + c) : 0.0;
+        }
+      double G[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dmma(G[0], G[1], x[k], x[k]);
+      gpart[w * 64 + g * 8 + 2 * q] = G[0];
+      gpart[w * 64 + g * 8 + 2 * q + 1] = G[1];
+#pragma unroll
+      for (int cb = 0; cb < TA_KB / 8; ++cb) {
+        double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0;
+        dmma(wa0, wa1, Cb[cb][0][0], x[0]);
+        dmma(wb0, wb1, Cb[cb][1][0], x[2]);
+        dmma(wa0, wa1, Cb[cb][0][1], x[1]);
+        dmma(wb0, wb1, Cb[cb][1][1], x[3]);
+        double* wp = wpart + w * 8 * TA_KB + 8 * cb + g;
+        wp[(2 * q) * TA_KB] = wa0 + wb0;
+        wp[(2 * q + 1) * TA_KB] = wa1 + wb1;
+      }
+    }
+    __syncthreads();
+    {  // T (every warp) and W' of column block w
+      double G[2] = {0.0, 0.0};
+      for (int w2 = 0; w2 <= wmax; ++w2) {
+        G[0] += gpart[w2 * 64 + g * 8 + 2 * q];
+        G[1] += gpart[w2 * 64 + g * 8 + 2 * q + 1];
+      }
+      DaPanel P;
+      P.x[0] = P.x[1] = P.x[2] = P.x[3] = 0.0;
+      P.tg = (pc + g < n) ? __ldg(tn + pc + g) : 0.0;
+      P.tq0 = (pc + 2 * q < n) ? __ldg(tn + pc + 2 * q) : 0.0;
+      P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tn + pc + 2 * q + 1) : 0.0;
+      double tb0, tb1;
+      da_form_t_g(P, G, tb0, tb1);
+      double* ca = Ca + (pc + 2 * q) * TA_LDC + 8 * w + g;
+      double w0 = ca[0], w1 = ca[TA_LDC];
+      for (int w2 = 0; w2 <= wmax; ++w2) {
+        const double* wp = wpart + w2 * 8 * TA_KB + 8 * w + g;
+        w0 += wp[(2 * q) * TA_KB];
+        w1 += wp[(2 * q + 1) * TA_KB];
+      }
+      double u0 = 0.0, u1 = 0.0;
+      dmma(u0, u1, w0, tb0);
+      dmma(u0, u1, w1, tb1);
+      ca[0] -= u0;
+      ca[TA_LDC] -= u1;
+      wfin[(2 * q) * TA_KB + 8 * w + g] = u0;
+      wfin[(2 * q + 1) * TA_KB + 8 * w + g] = u1;
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int cb = 0; cb < TA_KB / 8; ++cb) {
+        const double u0 = wfin[(2 * q) * TA_KB + 8 * cb + g];
+        const double u1 = wfin[(2 * q + 1) * TA_KB + 8 * cb + g];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma(Cb[cb][bb][0], Cb[cb][bb][1], -u0, vb[bb][0]);
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma(Cb[cb][bb][0], Cb[cb][bb][1], -u1, vb[bb][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int cb = 0; cb < TA_KB / 8; ++cb)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
+        if (r < n && c < ncb) Cbg[(int64_t)r * ldc + c] = Cb[cb][bb][e];
+      }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * TA_KB; idx += THREADS) {
+    const int r = idx / TA_KB, c = idx - r * TA_KB;
+    if (c < ncb) Cag[(int64_t)r * ldc + c] = Ca[r * TA_LDC + c];
   }
 }

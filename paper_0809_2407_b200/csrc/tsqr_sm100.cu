@@ -1317,6 +1317,15 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
                                                    slot_rows, ncols, zero_partner);
     return check_launch("k_tree_apply_w32");
   }
+  if (p == 128 && transpose && !zero_partner && g_dmma_apply) {
+    const size_t sm = TreeApplyDmmaSmem::bytes;
+    int rc = prep(k_tree_apply_dmma, sm);
+    if (rc) return rc;
+    dim3 gd((unsigned)nev, (unsigned)((ncols + TA_KB - 1) / TA_KB));
+    k_tree_apply_dmma<<<gd, THREADS, sm, st>>>(Ynode, taunode, (int)n, events, C, ldc, slot_rows,
+                                               ncols);
+    return check_launch("k_tree_apply_dmma");
+  }
   switch (p) { TA_CASE(32) TA_CASE(64) TA_CASE(128) }
 #undef TA_CASE
   return check_launch("k_tree_apply");
