@@ -17,12 +17,14 @@
 // Tile t may update the pivot rows of panel p once tile t-1 has (ver[p] == t).
 // Included by tsqr_sm100.cu (namespace tsqr) after dmma_ring.cuh.
 
-constexpr int DA_KB = 128;          // columns per CTA
-constexpr int DA_LDC = DA_KB + 2;   // pivot-row stride (doubles)
+// KB = columns per CTA: 128 for full-width trailing updates, 32 when the
+// launch has few CTAs (the look-ahead update of the next panel's 128 columns:
+// 4x the CTAs, each a quarter of the column work).
+template <int KB>
 struct DmmaApplySmem {
+  static constexpr int LDC = KB + 2;                       // pivot-row stride (doubles)
   static constexpr int STAGE = ApplyStage<16>::DOUBLES;  // dense-tile V staging per warp
-  static constexpr size_t doubles =
-      (size_t)DR_NP * DA_LDC + 2 * WARPS * DA_KB + (size_t)WARPS * STAGE;
+  static constexpr size_t doubles = (size_t)DR_NP * LDC + 2 * WARPS * KB + (size_t)WARPS * STAGE;
   static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * DR_NCB;
 };
 
@@ -94,16 +96,18 @@ __device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double&
   da_form_t_g(P, G, tb0, tb1);
 }
 
+template <int KB>
 __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
                   int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
                   int64_t ncols) {
-  constexpr int HD = Geo<128>::HD, H0 = WARPS * HD, KBS = DA_KB / 32;
+  constexpr int HD = Geo<128>::HD, H0 = WARPS * HD, KBS = KB / 32, CB = KB / 8;
+  constexpr int DA_KB = KB, DA_LDC = DmmaApplySmem<KB>::LDC;
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
   double* part = Cs + DR_NP * DA_LDC;
-  double* vstage = part + 2 * WARPS * DA_KB + (threadIdx.x >> 5) * DmmaApplySmem::STAGE;
-  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * DA_KB + WARPS * DmmaApplySmem::STAGE);
+  double* vstage = part + 2 * WARPS * DA_KB + (threadIdx.x >> 5) * DmmaApplySmem<KB>::STAGE;
+  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * DA_KB + WARPS * DmmaApplySmem<KB>::STAGE);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
@@ -138,9 +142,9 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
   for (int t = w; t < T; t += WARPS) {
     const int64_t row = H0 + (int64_t)t * DR_H;
     const int valid = (int)min64(DR_H, b - row);
-    double Ct[DR_NCB][2][2];
+    double Ct[CB][2][2];
 #pragma unroll
-    for (int cb = 0; cb < DR_NCB; ++cb)
+    for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
@@ -161,13 +165,13 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
       // all 16 blocks, unguarded (columns >= ncb are zero in Ct and Cs and never
       // stored): one basic block, so ptxas interleaves the blocks' DMMA chains
 #pragma unroll
-      for (int cb = 0; cb < DR_NCB; ++cb)
+      for (int cb = 0; cb < CB; ++cb)
         dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
       ring_signal(ver + p, t + 1, lane);
       cur = nxt;
     }
 #pragma unroll
-    for (int cb = 0; cb < DR_NCB; ++cb)
+    for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll

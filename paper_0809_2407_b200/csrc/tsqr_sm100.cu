@@ -1373,12 +1373,23 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
       else if (transpose && g_dmma_apply) {
-        const size_t sm = DmmaApplySmem::bytes;
-        int rc = prep(k_leaf_apply_dmma, sm);
-        if (rc) return rc;
-        dim3 gd((unsigned)P, (unsigned)((ncols + DA_KB - 1) / DA_KB));
-        k_leaf_apply_dmma<<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P, base,
-                                                   C, ldc, ncols);
+        // few CTAs at full width (e.g. the look-ahead update of one panel): 32-column blocks
+        const bool narrow = P * ((ncols + 127) / 128) < 2 * 148;
+        if (narrow) {
+          const size_t sm = DmmaApplySmem<32>::bytes;
+          int rc = prep(k_leaf_apply_dmma<32>, sm);
+          if (rc) return rc;
+          dim3 gd((unsigned)P, (unsigned)((ncols + 31) / 32));
+          k_leaf_apply_dmma<32><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
+                                                         base, C, ldc, ncols);
+        } else {
+          const size_t sm = DmmaApplySmem<128>::bytes;
+          int rc = prep(k_leaf_apply_dmma<128>, sm);
+          if (rc) return rc;
+          dim3 gd((unsigned)P, (unsigned)((ncols + 127) / 128));
+          k_leaf_apply_dmma<128><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
+                                                          base, C, ldc, ncols);
+        }
       } else LA_LAUNCH(128, 4, 16)
       break;
     }

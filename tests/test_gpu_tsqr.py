@@ -397,12 +397,13 @@ def test_dmma_ring_matches_rank1_ring():
 
 
 @pytest.mark.parametrize("shape", [(8 * 2048, 128, 8, 300), (3 * 1500 + 77, 100, 3, 129),
-                                   (4096, 128, 2, 64)])
+                                   (4096, 128, 2, 64), (8 * 2048, 128, 8, 37 * 128 + 5)])
 def test_dmma_leaf_apply_matches_ring(shape):
     """CAQR_TUNE_DMMA_APPLY = 1 (default): Q^T C of n in (64, 128] chain leaves
     on the DMMA ring (compact WY per 8-reflector panel, T from the Neumann
-    product) equals the reflector-by-reflector ring (= 0), and Q^T A = [R; 0]
-    leaf by leaf."""
+    product; 32-column CTAs when the launch is small, 128-column CTAs for the
+    last shape) and the DMMA tree apply equal the reflector rings (= 0), and
+    Q (Q^T C) = C."""
     from paper_0809_2407_b200 import _lib
     from paper_0809_2407_b200.tsqr import apply_q_device, factor_device
 

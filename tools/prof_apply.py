@@ -7,7 +7,7 @@ import torch
 
 from paper_0809_2407_b200.tsqr import _leaf_apply, factor_device
 
-m, n, P, k = 16384, 128, 8, 16384 - 128
+m, n, P, k = 16384, 128, 8, int(sys.argv[1]) if len(sys.argv) > 1 else 16384 - 128
 A = torch.randn(m, n, dtype=torch.float64, device="cuda")
 f = factor_device(A, P, want_q=True)
 C = torch.randn(m, k, dtype=torch.float64, device="cuda")
