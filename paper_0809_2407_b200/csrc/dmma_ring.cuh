@@ -108,6 +108,9 @@ __device__ __forceinline__ void dr_wait(const int* ver, int target, int lane) {
 // rsqrt Newton steps (two Newton steps from a ~2^-19 seed: full precision),
 // plus invb = 1/beta (= -sign(x0) y; 0 when sigma = 0) so that the column
 // update factor -scale * tau * t = t / beta needs no product with tau.
+__device__ __forceinline__ double dr_neg(double x) {  // sign flip on the ALU, not the FP64 pipe
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
 __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta, double& tau,
                                            double& scale, double& invb) {
   const double a = fma(x0, x0, sigma);
@@ -125,10 +128,10 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
   r = r * fma(-d, r, 2.0);
   const bool pos = (x0 >= 0.0);
   const bool z = (sigma == 0.0);
-  beta = z ? ax : (pos ? -nrm : nrm);
+  beta = z ? ax : (pos ? dr_neg(nrm) : nrm);
   tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
-  scale = z ? 0.0 : (pos ? r : -r);
-  invb = z ? 0.0 : (pos ? -y : y);
+  scale = z ? 0.0 : (pos ? r : dr_neg(r));
+  invb = z ? 0.0 : (pos ? dr_neg(y) : y);
 }
 
 // One generation (reflector I of the panel) of the register Level-2, with
@@ -162,9 +165,11 @@ __device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow,
   const double tw = fma(scale, pd, rgi);  // R[i][g] + v^T x_g
   const double wv = tau * tw;
   const bool upd = g > I;
-  const double f = upd ? tw * invb : 0.0;  // = -scale * wv
+  // x_g -= scale * wv * x_I for g > I (f = t / beta = -scale tau t); the owner
+  // column becomes v = scale * x_I, written as x + (scale - 1) x: one FMA form
+  const double f = upd ? tw * invb : ((g == I) ? scale - 1.0 : 0.0);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) x[k] = (g == I) ? xi[k] * scale : fma(f, xi[k], x[k]);
+  for (int k = 0; k < 4; ++k) x[k] = fma(f, xi[k], x[k]);
   double* dst = upd ? Rrow + g : ((g == I) ? Rrow + I : gs + g * 8 + I);
   *dst = upd ? rgi - wv : ((g == I) ? beta : scale * pd);
   taus[I] = tau;
