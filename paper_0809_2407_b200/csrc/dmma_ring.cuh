@@ -222,12 +222,12 @@ __device__ __forceinline__ void dr_upd(double (&Cb)[2][2], const double (&x)[4],
                                        const double (&vb)[2][2], double tb0, double tb1,
                                        double* rp, int ldr) {
   const double ro0 = rp[0], ro1 = rp[ldr];
-  double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0;
-  dmma(wa0, wa1, Cb[0][0], x[0]);
-  dmma(wb0, wb1, Cb[1][0], x[2]);
-  dmma(wa0, wa1, Cb[0][1], x[1]);
-  dmma(wb0, wb1, Cb[1][1], x[3]);
-  const double w0 = ro0 + (wa0 + wb0), w1 = ro1 + (wa1 + wb1);
+  // one accumulation chain seeded with R_p,trail: no FP64 adds on the pipe
+  double w0 = ro0, w1 = ro1;
+  dmma(w0, w1, Cb[0][0], x[0]);
+  dmma(w0, w1, Cb[1][0], x[2]);
+  dmma(w0, w1, Cb[0][1], x[1]);
+  dmma(w0, w1, Cb[1][1], x[3]);
   double u0 = 0.0, u1 = 0.0;
   dmma(u0, u1, w0, tb0);
   dmma(u0, u1, w1, tb1);
