@@ -108,9 +108,6 @@ __device__ __forceinline__ void dr_wait(const int* ver, int target, int lane) {
 // rsqrt Newton steps (two Newton steps from a ~2^-19 seed: full precision),
 // plus invb = 1/beta (= -sign(x0) y; 0 when sigma = 0) so that the column
 // update factor -scale * tau * t = t / beta needs no product with tau.
-__device__ __forceinline__ double dr_neg(double x) {  // sign flip on the ALU, not the FP64 pipe
-  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
-}
 __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta, double& tau,
                                            double& scale, double& invb) {
   const double a = fma(x0, x0, sigma);
@@ -134,10 +131,10 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
   }
   const bool pos = (x0 >= 0.0);
   const bool z = (sigma == 0.0);
-  beta = z ? ax : (pos ? dr_neg(nrm) : nrm);
+  beta = z ? ax : (pos ? neg_alu(nrm) : nrm);
   tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
-  scale = z ? 0.0 : (pos ? r : dr_neg(r));
-  invb = z ? 0.0 : (pos ? dr_neg(y) : y);
+  scale = z ? 0.0 : (pos ? r : neg_alu(r));
+  invb = z ? 0.0 : (pos ? neg_alu(y) : y);
 }
 
 // One generation (reflector I of the panel) of the register Level-2, with

@@ -150,13 +150,15 @@ __device__ __forceinline__ void store_rows(const double (&X)[RW][S], double* dst
   }
 }
 
-// Leaner reflector scalars for the pipelined ring: y = rsqrt(a) after two
-// Newton steps (MUFU seeds are ~2^-20) is accurate to a few ulp, so
+// Leaner reflector scalars for the pipelined ring: y = rsqrt(a) refined from
+// the MUFU seed (~2^-20) is accurate to a few ulp, so
 // nrm = a*y needs no correction and tau = 1 + |x0|/nrm = 1 + |x0|*y needs no
 // division; scale = 1/(x0 - beta) = sign(x0)/(|x0| + nrm).  Conventions of
 // house_gen (householder.py:101-111), branch-free.
-__device__ __forceinline__ void house_lean(double x0, double sigma, double& beta, double& tau,
-                                           double& scale) {
+// Two-Newton-step variant (the narrow n <= 8 kernel keeps it: its lane-private
+// chains schedule better with it -- measured, C4 2.10 vs 2.20 ms).
+__device__ __forceinline__ void house_newton(double x0, double sigma, double& beta, double& tau,
+                                             double& scale) {
   const double a = fma(x0, x0, sigma);
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
@@ -175,6 +177,37 @@ __device__ __forceinline__ void house_lean(double x0, double sigma, double& beta
   beta = z ? ax : (pos ? -nrm : nrm);
   tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
   scale = z ? 0.0 : (pos ? r : -r);
+}
+__device__ __forceinline__ double neg_alu(double x) {  // sign flip on the ALU, off the FP64 pipe
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+__device__ __forceinline__ void house_lean(double x0, double sigma, double& beta, double& tau,
+                                           double& scale) {
+  // MUFU seeds (~2^-20) refined by one third-order step each (error ~2^-60, within
+  // 2.3 / 3.5 ulp: tools/house_acc.cu): y (1 + e/2 + 3e^2/8) with e = 1 - a y^2,
+  // and r (1 + e + e^2) with e = 1 - d r; the reciprocal is seeded from the rsqrt
+  // seed so the two MUFU latencies overlap
+  const double a = fma(x0, x0, sigma);
+  const double ax = fabs(x0);
+  double y, r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double d0 = fma(a, y, ax);
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d0));
+  {
+    const double e = fma(-a * y, y, 1.0);
+    y = fma(y, e * fma(e, 0.375, 0.5), y);
+  }
+  const double nrm = a * y;
+  const double d = ax + nrm;
+  {
+    const double e = fma(-d, r, 1.0);
+    r = fma(r, fma(e, e, e), r);
+  }
+  const bool pos = (x0 >= 0.0);
+  const bool z = (sigma == 0.0);
+  beta = z ? ax : (pos ? neg_alu(nrm) : nrm);
+  tau = z ? (pos ? 0.0 : 2.0) : fma(ax, y, 1.0);
+  scale = z ? 0.0 : (pos ? r : neg_alu(r));
 }
 
 // ---------------------------------------------------------------------------

@@ -208,7 +208,7 @@ __device__ __forceinline__ void narrow_step(double (&R)[36], double (&B)[K][8], 
 #pragma unroll
     for (int k = 0; k < K; ++k) sg = fma(B[k][j], B[k][j], sg);
     double beta, tau, scale;
-    house_lean(R[pk8(j, j)], sg, beta, tau, scale);
+    house_newton(R[pk8(j, j)], sg, beta, tau, scale);
 #pragma unroll
     for (int c = j + 1; c < 8; ++c) {
       double d = 0.0;
