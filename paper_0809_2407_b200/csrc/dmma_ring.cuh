@@ -304,7 +304,6 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
           const int c = 8 * cb + g;
           double v = stage[(8 * bb + 2 * q + e) * DR_SLD + c];
           v = (c < n) ? v : 0.0;
-          bad |= !isfinite(v);
           C[cb][bb][e] = v;
         }
     __syncwarp();
@@ -417,10 +416,15 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   DR_TICK(k1_);
   DR_ADD(5, k0_, k1_);
   __syncthreads();
+  // NaN / Inf anywhere in the leaf reaches R (every entry enters a column norm
+  // or a dot product, and non-finite values never become finite again), so R is
+  // checked once instead of every input element on the FP64 pipe
   for (int idx = threadIdx.x; idx < n * n; idx += DR_WARPS * 32) {
     const int r = idx / n, c = idx - r * n;
     const int p = r >> 3;
-    Rl[idx] = (c >= r) ? Rp[dr_pbase(p) + (r & 7) * dr_ldr(p) + (c - 8 * p)] : 0.0;
+    const double v = (c >= r) ? Rp[dr_pbase(p) + (r & 7) * dr_ldr(p) + (c - 8 * p)] : 0.0;
+    bad |= !isfinite(v);
+    Rl[idx] = v;
   }
   if (bad && flag) atomicOr(flag, 1);
 }
