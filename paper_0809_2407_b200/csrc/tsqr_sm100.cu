@@ -1373,8 +1373,10 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     case 128: {
       if (g_ht[2] == 24) LA_LAUNCH(128, 2, 24)
       else if (transpose && g_dmma_apply) {
-        // few CTAs at full width (e.g. the look-ahead update of one panel): 32-column blocks
-        const bool narrow = P * ((ncols + 127) / 128) < 2 * 148;
+        // fewer than one wave of 128-column CTAs (e.g. the look-ahead update of one
+        // panel): 32-column blocks, 4x the CTAs at ~3x the T overhead per column
+        // (C5: threshold 148 -> 466.6 ms, 296 -> 469.6, 592 -> 504.5)
+        const bool narrow = P * ((ncols + 127) / 128) < 148;
         if (narrow) {
           const size_t sm = DmmaApplySmem<32>::bytes;
           int rc = prep(k_leaf_apply_dmma<32>, sm);
