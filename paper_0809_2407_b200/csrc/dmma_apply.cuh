@@ -167,7 +167,7 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb)
         dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
-      ring_signal(ver + p, t + 1, lane);
+      dr_signal(ver + p, t + 1, lane);
       cur = nxt;
     }
 #pragma unroll

@@ -100,7 +100,14 @@ __device__ __forceinline__ void dr_wait(const int* ver, int target, int lane) {
     v = __shfl_sync(FULL, v, 0);
     if (v == target) break;
   }
-  __threadfence_block();
+  __syncwarp();  // lane 0's acquire, then the warp barrier orders the other lanes' reads
+}
+// Publish: the warp barrier orders every lane's prior shared-memory writes before
+// lane 0's release store (PTX memory model: bar.warp.sync orders memory among
+// its threads, st.release makes what happens-before it visible to the acquirer).
+__device__ __forceinline__ void dr_signal(int* ver, int value, int lane) {
+  __syncwarp();
+  if (lane == 0) st_release(ver, value);
 }
 
 // house_gen scalars (householder.py:97-113) for the panel generations, with
@@ -338,7 +345,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
       double* Rpan = Rp + dr_pbase(p);
       DR_TICK(c2_);
       // L2(p) stored R_pp, G and tau as it went; publish R_pp
-      ring_signal(ver + p, t + 1, lane);  // (__syncwarp first: gs / taus visible)
+      dr_signal(ver + p, t + 1, lane);  // (__syncwarp first: gs / taus visible)
       if (Q) {  // the tile's factor for panel p: Y (= x, rows 8b+2q+e, column 8p+g) and tau
         const int c = 8 * p + g;
 #pragma unroll
@@ -402,7 +409,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
       } else {
         dr_wait(ver + DR_NCB + p, t, lane);  // keep the versions monotone
       }
-      ring_signal(ver + DR_NCB + p, t + 1, lane);
+      dr_signal(ver + DR_NCB + p, t + 1, lane);
       // shift the register blocks: the next panel becomes block 0
 #pragma unroll
       for (int cb = 0; cb + 1 < DR_NCB; ++cb)
