@@ -30,8 +30,9 @@
 //
 // Pivot rows: R is stored panel-packed in shared memory (panel p = rows
 // 8p..8p+7, columns 8p..127, row stride 130 - 8p).  Tile t may factor panel p
-// once tile t-1 has (ver1[p] == t) and may update R_p,trail once tile t-1 has
-// (ver2[p] == t) -- the ring of k_leaf_chain at panel granularity.
+// once tile t-1 has (ver[p] == t); tile t-1 publishes ver[p+1] only after its
+// update of R_p,trail, so the same counter also releases R_p,trail -- the ring
+// of k_leaf_chain at panel granularity.
 // Included by tsqr_sm100.cu (namespace tsqr).
 
 constexpr int DR_WARPS = 8;
@@ -263,7 +264,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   double* Rp = sm;
   double* stage_all = Rp + DmmaRingSmem::RP;
   double* scr_all = stage_all + DR_WARPS * DR_H * DR_SLD;
-  int* ver = reinterpret_cast<int*>(scr_all + DR_WARPS * DR_SCR);  // ver1[16], ver2[16]
+  int* ver = reinterpret_cast<int*>(scr_all + DR_WARPS * DR_SCR);  // one counter per panel
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
@@ -369,11 +370,13 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
           for (int s = 0; s < 2; ++s) vb[bb][s] = vs[(8 * bb + g) * 12 + 2 * q + s];
         DR_TICK(c3_);
         DR_ADD(1, c2_, c3_);
-        dr_wait(ver + DR_NCB + p, t, lane);
+        // one wait covers both R_{p+1,p+1} and R_p,trail: tile t-1 publishes
+        // ver[p+1] (after its L2(p+1)) only once its update of R_p,trail is done
+        // (program order + release), so no separate counter is needed for it
+        dr_wait(ver + p + 1, t, lane);
         double* rrow = Rpan + (2 * q) * ldr + g;
         // block 1 (the next panel's columns) first: it feeds L2(p+1)
         dr_upd(C[1], x, vb, tb0, tb1, rrow + 8, ldr);
-        dr_wait(ver + p + 1, t, lane);
         __syncwarp();  // vb reads done before the next panel's vs writes
         DR_TICK(c4_);
         DR_ADD(2, c3_, c4_);
@@ -406,10 +409,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         for (int k = 0; k < 4; ++k) x[k] = xn[k];
         DR_TICK(c5_);
         DR_ADD(3, c4_, c5_);
-      } else {
-        dr_wait(ver + DR_NCB + p, t, lane);  // keep the versions monotone
       }
-      dr_signal(ver + DR_NCB + p, t + 1, lane);
       // shift the register blocks: the next panel becomes block 0
 #pragma unroll
       for (int cb = 0; cb + 1 < DR_NCB; ++cb)
