@@ -422,3 +422,40 @@ def test_dmma_leaf_apply_matches_ring(shape):
     # round trip: Q (Q^T C) = C
     back = apply_q_device(f, Qd, transpose=False)
     assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * scale
+
+
+def test_dmma_kernels_random_shapes():
+    """Randomised cross-check (tools/stress_dmma.py, 10 shapes): DMMA leaf factor
+    (R only and Q-keeping), DMMA leaf apply and tree apply vs the rank-1 /
+    reflector rings, n in (64, 128], ragged leaves, narrow and wide column counts."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, factor_device
+
+    rng = np.random.default_rng(77)
+
+    def sgn(R):
+        return R * torch.sign(torch.diagonal(R)).unsqueeze(1)
+
+    for _ in range(10):
+        n = int(rng.integers(65, 129))
+        P = int(rng.integers(1, 9))
+        m = P * int(rng.integers(max(n, 300), 2500)) + int(rng.integers(0, 50))
+        k = int(rng.choice([int(rng.integers(1, 200)), int(rng.integers(2000, 5000))]))
+        A = torch.from_numpy(rng.standard_normal((m, n))).cuda()
+        C = torch.from_numpy(rng.standard_normal((m, k))).cuda()
+        f = factor_device(A, P, want_q=True)
+        R1 = factor_device(A, P).R
+        Qd = apply_q_device(f, C, transpose=True)
+        try:
+            _lib.tune(_lib.TUNE_DMMA, 0)
+            _lib.tune(_lib.TUNE_DMMA_APPLY, 0)
+            f0 = factor_device(A, P, want_q=True)
+            R0 = factor_device(A, P).R
+            Qr = apply_q_device(f0, C, transpose=True)
+        finally:
+            _lib.tune(_lib.TUNE_DMMA, 1)
+            _lib.tune(_lib.TUNE_DMMA_APPLY, 1)
+        nA = torch.linalg.norm(A, 2).item()
+        assert (sgn(R1) - sgn(R0)).abs().max().item() <= 100 * EPS * nA, (m, n, P)
+        assert (f.R - f0.R).abs().max().item() <= 100 * EPS * nA, (m, n, P)
+        assert torch.linalg.norm(Qd - Qr).item() <= 100 * EPS * torch.linalg.norm(C).item(), (m, n, P, k)
