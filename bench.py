@@ -514,10 +514,10 @@ def run_ours(args, cfg):
         else:
             ach = F_leaf / t_leaf / 1e12
             # DRAM traffic of the leaf kernel from the committed ncu capture
-            # (profiles/r01/dmma_kernel_ncu_summary.txt: 1.2417e9 B read + 3.8e6 B
-            # written for 148 leaves of 8192 x 128 = 1.0032x the 8mn algorithmic
+            # (profiles/r01/dmma_kernel_ncu_summary.txt: 1.2432e9 B read + 4.1e6 B
+            # written for 148 leaves of 8192 x 128 = 1.0047x the 8mn algorithmic
             # bytes), scaled to this launch's rows; None for other widths.
-            traffic = 8.0 * (hi - lo) * n * 1.0032 if (n == 128 and cfg["q"] == "none") else None
+            traffic = 8.0 * (hi - lo) * n * 1.0047 if (n == 128 and cfg["q"] == "none") else None
             kern = ("k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)"
                     if cfg["q"] == "none" else
                     "k_leaf_dense + k_leaf_chain + k_tree_factor, then Q: k_tree_apply + k_leaf_apply "
