@@ -3,9 +3,10 @@
 // the CAQR trailing update, _apply_yt with transpose (householder.py:175-186,
 // :209), one (leaf, 128-column block) per CTA.
 //
-// The dense first tile is applied CTA-cooperatively exactly as in
-// k_leaf_apply; its top n rows become the pivot rows Cs (shared memory, row
-// stride 130).  The chain tiles then run as the DMMA warp ring: warp w owns
+// The dense first tile (V unit lower trapezoidal, LAPACK layout) is applied
+// in compact WY too, 8 reflectors per panel with the tile's rows spread over
+// the warps (partial G / W in shared memory, two barriers per panel); its top
+// n rows then become the pivot rows Cs (shared memory, row stride KB + 2).  The chain tiles then run as the DMMA warp ring: warp w owns
 // tiles w, w+8, ..., holds its 16 x 128 tile of C in registers in the DMMA
 // accumulator layout of k_leaf_dmma, and applies each 8-reflector panel of
 // the tile's TRI_ON_RECT factor in compact-WY form on the tensor cores:
@@ -22,10 +23,10 @@
 // 4x the CTAs, each a quarter of the column work).
 template <int KB>
 struct DmmaApplySmem {
-  static constexpr int LDC = KB + 2;                       // pivot-row stride (doubles)
-  static constexpr int STAGE = ApplyStage<16>::DOUBLES;  // dense-tile V staging per warp
-  static constexpr size_t doubles = (size_t)DR_NP * LDC + 2 * WARPS * KB + (size_t)WARPS * STAGE;
+  static constexpr int LDC = KB + 2;  // pivot-row stride (doubles)
+  static constexpr size_t doubles = (size_t)DR_NP * LDC;  // pivot rows (also the dense phase's W / G)
   static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * DR_NCB;
+  static_assert(WARPS * 8 * KB + WARPS * 64 + 8 * KB <= DR_NP * LDC, "dense-phase scratch fits in Cs");
 };
 
 // Panel p of a chain tile: Y fragments (x: B operand of C^T Y; vb: B operand
@@ -101,13 +102,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
                   int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
                   int64_t ncols) {
-  constexpr int HD = Geo<128>::HD, H0 = WARPS * HD, KBS = KB / 32, CB = KB / 8;
+  constexpr int H0 = WARPS * Geo<128>::HD, CB = KB / 8;  // dense first tile: 128 rows
   constexpr int DA_KB = KB, DA_LDC = DmmaApplySmem<KB>::LDC;
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
-  double* part = Cs + DR_NP * DA_LDC;
-  double* vstage = part + 2 * WARPS * DA_KB + (threadIdx.x >> 5) * DmmaApplySmem<KB>::STAGE;
-  int* ver = reinterpret_cast<int*>(part + 2 * WARPS * DA_KB + WARPS * DmmaApplySmem<KB>::STAGE);
+  int* ver = reinterpret_cast<int*>(Cs + DR_NP * DA_LDC);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
@@ -121,21 +120,107 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
   const int64_t rest = b - H0;
   const int T = rest > 0 ? (int)((rest + DR_H - 1) / DR_H) : 0;
   const int npan = (n + 7) >> 3;
-  bool bad = false;
-  auto ycol = [&](int r, int j) { return (r < b) ? __ldg(Yl + (int64_t)r * ldy + j) : 0.0; };
-  {  // dense first tile (LAPACK layout), CTA-cooperative; its top n rows -> Cs
-    const int v0 = (int)max64(0, min64((int64_t)HD, b - (int64_t)w * HD));
-    double X[HD][KBS];
-    load_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, bad);
-    cta_apply<HD, KBS, DENSE, true>(X, nullptr, n, ycol, tl, part, col0, false, vstage);
+  {  // dense first tile (LAPACK layout: V unit lower trapezoidal) in compact WY on the
+     // tensor cores, 8 reflectors per panel: warp w holds rows 16w.. of the tile;
+     // per panel partial G = V^T V and W = V^T C per warp (shared memory), then T
+     // and W' = T^T W per column block, then C -= V W'.  Two barriers per panel.
+    double* wpart = Cs;                       // [warp][refl 8][KB]  (Cs is free until the end)
+    double* gpart = wpart + WARPS * 8 * KB;   // [warp][8 x 8]
+    double* wfin = gpart + WARPS * 64;        // [refl 8][KB]
+    double Cd[CB][2][2];
 #pragma unroll
-    for (int k = 0; k < HD; ++k) {
-      const int r = w * HD + k;
+    for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
-      for (int s = 0; s < KBS; ++s) Cs[r * DA_LDC + 32 * s + lane] = (r < n) ? X[k][s] : 0.0;
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
+          Cd[cb][bb][e] = (r < b && c < ncb) ? Cl[(int64_t)r * ldc + c] : 0.0;
+        }
+    auto vdense = [&](int r, int c) {  // V[r][c] of the dense tile
+      return (r >= b || c >= n) ? 0.0 : (r > c ? __ldg(Yl + (int64_t)r * ldy + c) : (r == c ? 1.0 : 0.0));
+    };
+    for (int p = 0; p < npan; ++p) {
+      const int pc = 8 * p;
+      const int wmin = pc >> 4;  // warps holding rows >= pc
+      const bool active = w >= wmin;
+      double x[4], vb[2][2];
+      if (active) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = vdense(16 * w + 8 * (k >> 1) + 2 * q + (k & 1), pc + g);
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int sx = 0; sx < 2; ++sx) vb[bb][sx] = vdense(16 * w + 8 * bb + g, pc + 2 * q + sx);
+        double G[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dmma(G[0], G[1], x[k], x[k]);
+        gpart[w * 64 + g * 8 + 2 * q] = G[0];
+        gpart[w * 64 + g * 8 + 2 * q + 1] = G[1];
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+          double w0 = 0.0, w1 = 0.0;
+          dmma(w0, w1, Cd[cb][0][0], x[0]);
+          dmma(w0, w1, Cd[cb][1][0], x[2]);
+          dmma(w0, w1, Cd[cb][0][1], x[1]);
+          dmma(w0, w1, Cd[cb][1][1], x[3]);
+          double* wp = wpart + (w * 8 + 2 * q) * KB + 8 * cb + g;
+          wp[0] = w0;
+          wp[KB] = w1;
+        }
+      }
+      __syncthreads();
+      {
+        double G[2] = {0.0, 0.0};
+        for (int w2 = wmin; w2 < WARPS; ++w2) {
+          G[0] += gpart[w2 * 64 + g * 8 + 2 * q];
+          G[1] += gpart[w2 * 64 + g * 8 + 2 * q + 1];
+        }
+        DaPanel Pn;
+        Pn.x[0] = Pn.x[1] = Pn.x[2] = Pn.x[3] = 0.0;
+        Pn.tg = (pc + g < n) ? __ldg(tl + pc + g) : 0.0;
+        Pn.tq0 = (pc + 2 * q < n) ? __ldg(tl + pc + 2 * q) : 0.0;
+        Pn.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tl + pc + 2 * q + 1) : 0.0;
+        double tb0, tb1;
+        da_form_t_g(Pn, G, tb0, tb1);
+        for (int cb = w; cb < CB; cb += WARPS) {
+          double w0 = 0.0, w1 = 0.0;
+          for (int w2 = wmin; w2 < WARPS; ++w2) {
+            const double* wp = wpart + (w2 * 8 + 2 * q) * KB + 8 * cb + g;
+            w0 += wp[0];
+            w1 += wp[KB];
+          }
+          double u0 = 0.0, u1 = 0.0;
+          dmma(u0, u1, w0, tb0);
+          dmma(u0, u1, w1, tb1);
+          wfin[(2 * q) * KB + 8 * cb + g] = u0;
+          wfin[(2 * q + 1) * KB + 8 * cb + g] = u1;
+        }
+      }
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+          const double u0 = wfin[(2 * q) * KB + 8 * cb + g];
+          const double u1 = wfin[(2 * q + 1) * KB + 8 * cb + g];
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma(Cd[cb][bb][0], Cd[cb][bb][1], -u0, vb[bb][0]);
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma(Cd[cb][bb][0], Cd[cb][bb][1], -u1, vb[bb][1]);
+        }
+      }
     }
-    const int lo = max(0, n - w * HD);
-    store_rows<HD, KBS>(X, Cl + (int64_t)w * HD * ldc, ldc, v0, ncb, 0, lo);
+    __syncthreads();  // wpart / wfin (in Cs) consumed before Cs is filled
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
+          Cs[r * DA_LDC + c] = (r < n) ? Cd[cb][bb][e] : 0.0;
+          if (r >= n && r < b && c < ncb) Cl[(int64_t)r * ldc + c] = Cd[cb][bb][e];  // final rows
+        }
   }
   if (threadIdx.x < DR_NCB) ver[threadIdx.x] = 0;
   __syncthreads();
