@@ -241,19 +241,27 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
     const double* tt = tl + (int64_t)(t + 1) * n;
     DaPanel cur, nxt;
     da_load_panel(cur, Yt, ldy, tt, valid, n, 0);
+    // T of panel p+1 is formed in the same basic block as panel p's block
+    // updates (its DMMA chain runs under them); for the last panel it works on
+    // stale data and is discarded
+    nxt = cur;
+    double tb0, tb1;
+    da_form_t(cur, tb0, tb1);
     for (int p = 0; p < npan; ++p) {
       if (p + 1 < npan) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p + 1));
-      double tb0, tb1;
-      da_form_t(cur, tb0, tb1);
       dr_wait(ver + p, t, lane);
       double* rrow = Cs + (8 * p + 2 * q) * DA_LDC + g;
-      // all 16 blocks, unguarded (columns >= ncb are zero in Ct and Cs and never
+      double tn0, tn1;
+      da_form_t(nxt, tn0, tn1);
+      // all blocks, unguarded (columns >= ncb are zero in Ct and Cs and never
       // stored): one basic block, so ptxas interleaves the blocks' DMMA chains
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb)
         dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, DA_LDC);
       dr_signal(ver + p, t + 1, lane);
       cur = nxt;
+      tb0 = tn0;
+      tb1 = tn1;
     }
 #pragma unroll
     for (int cb = 0; cb < CB; ++cb)
