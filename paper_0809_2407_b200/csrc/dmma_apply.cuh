@@ -296,7 +296,9 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
 constexpr int TA_KB = 64;
 constexpr int TA_LDC = TA_KB + 2;
 struct TreeApplyDmmaSmem {
-  static constexpr size_t doubles = (size_t)DR_NP * TA_LDC + WARPS * 8 * TA_KB + WARPS * 64 + 8 * TA_KB;
+  // C_a, partial W, final W', then per-panel partial G (16 x 8 warps) and T (16 x 64)
+  static constexpr size_t doubles = (size_t)DR_NP * TA_LDC + WARPS * 8 * TA_KB + WARPS * 64 + 8 * TA_KB +
+                                    (size_t)DR_NCB * WARPS * 64 + DR_NCB * 64;
   static constexpr size_t bytes = sizeof(double) * doubles;
 };
 
@@ -332,8 +334,46 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
         const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
         Cb[cb][bb][e] = (r < n && c < ncb) ? Cbg[(int64_t)r * ldc + c] : 0.0;
       }
-  __syncthreads();
   const int npan = (n + 7) >> 3;
+  // T of every panel depends on the node factor only: build them all up front
+  // (partial G per warp and panel, then warp w forms T of panels w, w+8)
+  double* gall = wfin + 8 * TA_KB;            // [panel][warp][8 x 8]
+  double* tball = gall + DR_NCB * WARPS * 64;  // [panel][lane][2]
+  for (int p = 0; p < npan; ++p) {
+    const int pc = 8 * p;
+    if (16 * w > pc + 7) continue;  // no nonzero rows of Y_p in this warp
+    double xg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = 16 * w + 8 * (k >> 1) + 2 * q + (k & 1), c = pc + g;
+      xg[k] = (r < n && c < n) ? __ldg(Yn + (int64_t)r * n + c) : 0.0;
+    }
+    double G[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dmma(G[0], G[1], xg[k], xg[k]);
+    gall[(p * WARPS + w) * 64 + g * 8 + 2 * q] = G[0];
+    gall[(p * WARPS + w) * 64 + g * 8 + 2 * q + 1] = G[1];
+  }
+  __syncthreads();
+  for (int p = w; p < npan; p += WARPS) {
+    const int pc = 8 * p;
+    const int wmax = min(WARPS - 1, (pc + 7) >> 4);
+    double G[2] = {0.0, 0.0};
+    for (int w2 = 0; w2 <= wmax; ++w2) {
+      G[0] += gall[(p * WARPS + w2) * 64 + g * 8 + 2 * q];
+      G[1] += gall[(p * WARPS + w2) * 64 + g * 8 + 2 * q + 1];
+    }
+    DaPanel P;
+    P.x[0] = P.x[1] = P.x[2] = P.x[3] = 0.0;
+    P.tg = (pc + g < n) ? __ldg(tn + pc + g) : 0.0;
+    P.tq0 = (pc + 2 * q < n) ? __ldg(tn + pc + 2 * q) : 0.0;
+    P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tn + pc + 2 * q + 1) : 0.0;
+    double tb0, tb1;
+    da_form_t_g(P, G, tb0, tb1);
+    tball[p * 64 + 2 * lane] = tb0;
+    tball[p * 64 + 2 * lane + 1] = tb1;
+  }
+  __syncthreads();
   for (int p = 0; p < npan; ++p) {
     const int pc = 8 * p;
     const int wmax = min(WARPS - 1, (pc + 7) >> 4);  // warps holding nonzero rows of Y_p
@@ -352,11 +392,6 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
           const int r = 16 * w + 8 * bb + g, c = pc + 2 * q + s;
           vb[bb][s] = (r < n && c < n) ? __ldg(Yn + (int64_t)r * n + c) : 0.0;
         }
-      double G[2] = {0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dmma(G[0], G[1], x[k], x[k]);
-      gpart[w * 64 + g * 8 + 2 * q] = G[0];
-      gpart[w * 64 + g * 8 + 2 * q + 1] = G[1];
 #pragma unroll
       for (int cb = 0; cb < TA_KB / 8; ++cb) {
         double wa0 = 0.0, wa1 = 0.0, wb0 = 0.0, wb1 = 0.0;
@@ -370,19 +405,8 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
       }
     }
     __syncthreads();
-    {  // T (every warp) and W' of column block w
-      double G[2] = {0.0, 0.0};
-      for (int w2 = 0; w2 <= wmax; ++w2) {
-        G[0] += gpart[w2 * 64 + g * 8 + 2 * q];
-        G[1] += gpart[w2 * 64 + g * 8 + 2 * q + 1];
-      }
-      DaPanel P;
-      P.x[0] = P.x[1] = P.x[2] = P.x[3] = 0.0;
-      P.tg = (pc + g < n) ? __ldg(tn + pc + g) : 0.0;
-      P.tq0 = (pc + 2 * q < n) ? __ldg(tn + pc + 2 * q) : 0.0;
-      P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tn + pc + 2 * q + 1) : 0.0;
-      double tb0, tb1;
-      da_form_t_g(P, G, tb0, tb1);
+    {  // W' of column block w
+      const double tb0 = tball[p * 64 + 2 * lane], tb1 = tball[p * 64 + 2 * lane + 1];
       double* ca = Ca + (pc + 2 * q) * TA_LDC + 8 * w + g;
       double w0 = ca[0], w1 = ca[TA_LDC];
       for (int w2 = 0; w2 <= wmax; ++w2) {
