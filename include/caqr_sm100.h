@@ -148,14 +148,20 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * tiles in shared memory, 16-column panels, compact-WY trailing update on the FP64 tensor
  * cores); 0 (default) = the warp-ring chain. */
 #define CAQR_TUNE_BLOCKED 8
-/* CAQR_TUNE_DMMA: 1 (default) = R-only leaves with n in (64, 128] run the DMMA warp ring
+/* CAQR_TUNE_DMMA: 1 (default) = leaves with n in (64, 128] run the DMMA warp ring
  * (16-row tiles per warp in registers, 8-column Level-2 panels with look-ahead,
- * compact-WY trailing updates on the FP64 tensor cores); 0 = the rank-1 warp ring. */
+ * compact-WY trailing updates on the FP64 tensor cores); 2 = also n in (32, 64] (the NP = 64
+ * ring, two CTAs per SM; implicit-Q leaves need CAQR_TUNE_CHAIN_HT_64 = 16); 0 = the rank-1
+ * warp ring. */
 #define CAQR_TUNE_DMMA 9
 /* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with n in (64, 128] and 16-row chain
  * tiles (the CAQR trailing update) runs the DMMA ring (compact-WY per 8-reflector panel on the
  * FP64 tensor cores); 0 = the reflector-by-reflector warp ring. */
 #define CAQR_TUNE_DMMA_APPLY 10
+/* CAQR_TUNE_DMMA_Q: 1 (default) = Q C (explicit Q, apply_q) for leaves with 16-row chain tiles
+ * and n in (32, 128] runs the DMMA ring backward (compact WY per 8-reflector panel, panels in
+ * reverse order); 0 = the reflector-by-reflector warp ring. */
+#define CAQR_TUNE_DMMA_Q 11
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

@@ -124,10 +124,23 @@ TUNE_ZSTART = 6
 TUNE_BLOCKED = 8
 TUNE_DMMA = 9
 TUNE_DMMA_APPLY = 10
+TUNE_DMMA_Q = 11
+
+
+# the library's defaults (csrc/tsqr_sm100.cu, g_ht / g_narrow / ... initialisers)
+TUNE_DEFAULTS = {TUNE_CHAIN_HT[32]: 16, TUNE_CHAIN_HT[64]: 16, TUNE_CHAIN_HT[128]: 16,
+                 TUNE_NARROW: 2, TUNE_ZSTART: 1, TUNE_BLOCKED: 0, TUNE_DMMA: 2,
+                 TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1}
 
 
 def tune(key: int, value: int) -> None:
     check(load().caqr_tune(key, value), "caqr_tune")
+
+
+def reset_tuning() -> None:
+    """Restore every tuning knob to the library default."""
+    for key, value in TUNE_DEFAULTS.items():
+        tune(key, value)
 
 
 def geometry(n: int):

@@ -56,9 +56,13 @@ __device__ __forceinline__ void da_load_panel(DaPanel& P, const double* __restri
   P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tt + pc + 2 * q + 1) : 0.0;
 }
 
-// tb[s] = T[2q+s][g] of the panel from Y and tau, all in registers: G = Y^T Y
-// is symmetric, so both the accumulator and the B layout of M come from the
-// same G fragment (same Neumann product as dr_form_t).
+// TR: tb[s] = T[2q+s][g] of the panel (the B operand of W'^T = W^T T, for Q^T)
+// from Y and tau, all in registers: G = Y^T Y is symmetric, so both the
+// accumulator and the B layout of M come from the same G fragment (same
+// Neumann product as dr_form_t).  !TR: tb[s] = T[g][2q+s] (W'^T = W^T T^T, for
+// Q): the polynomial of M^T = (the B layout of M read as the A layout) gives
+// P(M)^T, and T = P(M)^T D.
+template <bool TR = true>
 __device__ __forceinline__ void da_form_t_g(const DaPanel& P, const double (&G)[2], double& tb0,
                                             double& tb1) {
   const int lane = threadIdx.x & 31;
@@ -68,8 +72,10 @@ __device__ __forceinline__ void da_form_t_g(const DaPanel& P, const double (&G)[
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int c = 2 * q + e;
-    MA[e] = (c < g) ? tq[e] * G[e] : 0.0;  // M[g][c] = tau_c G[c][g]
-    MB[e] = (g < c) ? P.tg * G[e] : 0.0;   // M[c][g] = tau_g G[g][c]
+    const double ma = (c < g) ? tq[e] * G[e] : 0.0;  // M[g][c] = tau_c G[c][g]
+    const double mb = (g < c) ? P.tg * G[e] : 0.0;   // M[c][g] = tau_g G[g][c]
+    MA[e] = TR ? ma : mb;
+    MB[e] = TR ? mb : ma;
   }
   double M2A[2] = {0.0, 0.0}, M2B[2] = {0.0, 0.0};
   dmma(M2A[0], M2A[1], MA[0], MB[0]);
@@ -87,14 +93,15 @@ __device__ __forceinline__ void da_form_t_g(const DaPanel& P, const double (&G)[
   double PA[2] = {P1[0], P1[1]};
   dmma(PA[0], PA[1], P1[0], M4B[0]);
   dmma(PA[0], PA[1], P1[1], M4B[1]);
-  tb0 = P.tg * PA[0];
-  tb1 = P.tg * PA[1];
+  tb0 = (TR ? P.tg : P.tq0) * PA[0];
+  tb1 = (TR ? P.tg : P.tq1) * PA[1];
 }
+template <bool TR = true>
 __device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double& tb1) {
   double G[2] = {0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < 4; ++k) dmma(G[0], G[1], P.x[k], P.x[k]);
-  da_form_t_g(P, G, tb0, tb1);
+  da_form_t_g<TR>(P, G, tb0, tb1);
 }
 
 template <int KB>
@@ -278,6 +285,227 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
     const int r = idx / DA_KB, c = idx - r * DA_KB;
     if (c < ncb) Cl[(int64_t)r * ldc + c] = Cs[r * DA_LDC + c];
   }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA leaf Q: C[leaf rows] <- Q_leaf C for the chain leaves of n in (32, 64]
+// (NP = 64) or (64, 128] (NP = 128) with 16-row chain tiles -- explicit-Q
+// formation and apply_q (householder.py:377-404; the order of k_leaf_apply's
+// Q branch).  One (leaf, KB-column block) per CTA.  S (nullable): the leaf's
+// top n rows come from S + leaf * s_slot_rows * lds (the tree's Q block);
+// zero_init: the other rows start at zero.
+//
+// Q_leaf = Q_dense Q_1 ... Q_{T-1}, every tile factor a product of 8-reflector
+// panels I - V T V^T, so the chain tiles run as the DMMA warp ring BACKWARD
+// (tile T-1 first, warp w takes the w-th tile from the end) with the panels in
+// reverse order:
+//   W = Cs_p + Y_p^T C (4 DMMA per 8-column block), W' = T W (2),
+//   Cs_p -= W', C -= Y_p W' (4)
+// (dr_upd with T^T's B layout, da_form_t<false>), then the dense first tile
+// (H0 = 8 x HD rows, RG 16-row groups per warp) in compact WY with its panels
+// in reverse order.
+// ---------------------------------------------------------------------------
+template <int NP, int KB>
+struct DmmaQSmem {
+  static constexpr int LDC = KB + 2;
+  static constexpr int SCR = WARPS * 8 * KB + WARPS * 64 + 8 * KB;  // dense phase: W, G, W'
+  static constexpr size_t doubles = (size_t)NP * LDC + SCR;
+  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * (NP / 8);
+  static constexpr int MINB = NP == 128 ? 1 : 2;
+};
+
+template <int NP, int KB, int MB = DmmaQSmem<NP, KB>::MINB>
+__global__ void __launch_bounds__(THREADS, MB)
+k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
+              int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
+              int64_t ncols, const double* __restrict__ S, int64_t lds, int64_t s_slot_rows,
+              int zero_init) {
+  using SMQ = DmmaQSmem<NP, KB>;
+  constexpr int HD = Geo<NP>::HD, H0 = WARPS * HD, RG = HD / 16, CB = KB / 8, LDC = SMQ::LDC;
+  extern __shared__ __align__(16) double sm[];
+  double* Cs = sm;                       // pivot rows, NP x LDC
+  double* wpart = Cs + NP * LDC;         // [warp][refl 8][KB]
+  double* gpart = wpart + WARPS * 8 * KB;  // [warp][8 x 8]
+  double* wfin = gpart + WARPS * 64;       // [refl 8][KB]
+  int* ver = reinterpret_cast<int*>(sm + SMQ::doubles);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int leaf = blockIdx.x;
+  const int col0 = blockIdx.y * KB;
+  const int ncb = (int)min64(ncols - col0, KB);
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const double* tl = tau + (int64_t)leaf * tau_stride;
+  const double* Yl = Y + r0 * ldy;
+  double* Cl = C + r0 * ldc + col0;
+  const double* Sl = S ? S + (int64_t)leaf * s_slot_rows * lds + col0 : nullptr;
+  const int64_t rest = b - H0;
+  const int T = rest > 0 ? (int)((rest + DR_H - 1) / DR_H) : 0;
+  const int npan = (n + 7) >> 3;
+  for (int idx = threadIdx.x; idx < NP * KB; idx += THREADS) {
+    const int r = idx / KB, c = idx - r * KB;
+    double x = 0.0;
+    if (r < n && c < ncb) x = Sl ? Sl[(int64_t)r * lds + c] : Cl[(int64_t)r * ldc + c];
+    Cs[r * LDC + c] = x;
+  }
+  if (threadIdx.x < NP / 8) ver[threadIdx.x] = 0;
+  __syncthreads();
+  for (int o = w; o < T; o += WARPS) {
+    const int t = T - 1 - o;
+    const int64_t row = H0 + (int64_t)t * DR_H;
+    const int valid = (int)min64(DR_H, b - row);
+    double Ct[CB][2][2];
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * bb + 2 * q + e, c = 8 * cb + g;
+          Ct[cb][bb][e] = (!zero_init && r < valid && c < ncb) ? Cl[(row + r) * ldc + c] : 0.0;
+        }
+    const double* Yt = Yl + row * ldy;
+    const double* tt = tl + (int64_t)(t + 1) * n;
+    DaPanel cur, nxt;
+    da_load_panel(cur, Yt, ldy, tt, valid, n, 8 * (npan - 1));
+    nxt = cur;
+    double tb0, tb1;
+    da_form_t<false>(cur, tb0, tb1);
+    for (int p = npan - 1; p >= 0; --p) {
+      if (p > 0) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p - 1));
+      dr_wait(ver + p, o, lane);
+      double* rrow = Cs + (8 * p + 2 * q) * LDC + g;
+      double tn0, tn1;
+      da_form_t<false>(nxt, tn0, tn1);  // stale for p = 0, discarded
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb)
+        dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, LDC);
+      dr_signal(ver + p, o + 1, lane);
+      cur = nxt;
+      tb0 = tn0;
+      tb1 = tn1;
+    }
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * bb + 2 * q + e, c = 8 * cb + g;
+          if (r < valid && c < ncb) Cl[(row + r) * ldc + c] = Ct[cb][bb][e];
+        }
+  }
+  __syncthreads();
+  // dense first tile: warp w holds rows HD w + 16 j + .., j < RG
+  double Cd[RG][CB][2][2];
+#pragma unroll
+  for (int j = 0; j < RG; ++j)
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = HD * w + 16 * j + 8 * bb + 2 * q + e, c = 8 * cb + g;
+          double x = 0.0;
+          if (r < n) x = Cs[r * LDC + c];
+          else if (!zero_init && r < b && c < ncb) x = Cl[(int64_t)r * ldc + c];
+          Cd[j][cb][bb][e] = x;
+        }
+  auto vdense = [&](int r, int c) {  // V[r][c] of the dense tile (unit lower trapezoidal)
+    return (r >= b || c >= n) ? 0.0 : (r > c ? __ldg(Yl + (int64_t)r * ldy + c) : (r == c ? 1.0 : 0.0));
+  };
+  for (int p = npan - 1; p >= 0; --p) {
+    const int pc = 8 * p;
+    const int wmin = pc / HD;  // warps holding rows >= pc
+    const bool active = w >= wmin;
+    double x[RG][4], vb[RG][2][2];
+    if (active) {
+      double G[2] = {0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < RG; ++j) {
+        const int rb = HD * w + 16 * j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[j][k] = vdense(rb + 8 * (k >> 1) + 2 * q + (k & 1), pc + g);
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int sx = 0; sx < 2; ++sx) vb[j][bb][sx] = vdense(rb + 8 * bb + g, pc + 2 * q + sx);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dmma(G[0], G[1], x[j][k], x[j][k]);
+      }
+      gpart[w * 64 + g * 8 + 2 * q] = G[0];
+      gpart[w * 64 + g * 8 + 2 * q + 1] = G[1];
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < RG; ++j) {
+          dmma(w0, w1, Cd[j][cb][0][0], x[j][0]);
+          dmma(w0, w1, Cd[j][cb][1][0], x[j][2]);
+          dmma(w0, w1, Cd[j][cb][0][1], x[j][1]);
+          dmma(w0, w1, Cd[j][cb][1][1], x[j][3]);
+        }
+        double* wp = wpart + (w * 8 + 2 * q) * KB + 8 * cb + g;
+        wp[0] = w0;
+        wp[KB] = w1;
+      }
+    }
+    __syncthreads();
+    {
+      double G[2] = {0.0, 0.0};
+      for (int w2 = wmin; w2 < WARPS; ++w2) {
+        G[0] += gpart[w2 * 64 + g * 8 + 2 * q];
+        G[1] += gpart[w2 * 64 + g * 8 + 2 * q + 1];
+      }
+      DaPanel Pn;
+      Pn.x[0] = Pn.x[1] = Pn.x[2] = Pn.x[3] = 0.0;
+      Pn.tg = (pc + g < n) ? __ldg(tl + pc + g) : 0.0;
+      Pn.tq0 = (pc + 2 * q < n) ? __ldg(tl + pc + 2 * q) : 0.0;
+      Pn.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tl + pc + 2 * q + 1) : 0.0;
+      double tb0, tb1;
+      da_form_t_g<false>(Pn, G, tb0, tb1);
+      for (int cb = w; cb < CB; cb += WARPS) {
+        double w0 = 0.0, w1 = 0.0;
+        for (int w2 = wmin; w2 < WARPS; ++w2) {
+          const double* wp = wpart + (w2 * 8 + 2 * q) * KB + 8 * cb + g;
+          w0 += wp[0];
+          w1 += wp[KB];
+        }
+        double u0 = 0.0, u1 = 0.0;
+        dmma(u0, u1, w0, tb0);
+        dmma(u0, u1, w1, tb1);
+        wfin[(2 * q) * KB + 8 * cb + g] = u0;
+        wfin[(2 * q + 1) * KB + 8 * cb + g] = u1;
+      }
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        const double u0 = wfin[(2 * q) * KB + 8 * cb + g];
+        const double u1 = wfin[(2 * q + 1) * KB + 8 * cb + g];
+#pragma unroll
+        for (int j = 0; j < RG; ++j) {
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma(Cd[j][cb][bb][0], Cd[j][cb][bb][1], -u0, vb[j][bb][0]);
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) dmma(Cd[j][cb][bb][0], Cd[j][cb][bb][1], -u1, vb[j][bb][1]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RG; ++j)
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = HD * w + 16 * j + 8 * bb + 2 * q + e, c = 8 * cb + g;
+          if (r < b && c < ncb) Cl[(int64_t)r * ldc + c] = Cd[j][cb][bb][e];
+        }
 }
 
 // ---------------------------------------------------------------------------

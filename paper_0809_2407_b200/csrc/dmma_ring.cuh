@@ -41,17 +41,25 @@ constexpr int DR_NP = 128;          // padded width
 constexpr int DR_NCB = DR_NP / 8;   // 8-column blocks
 constexpr int DR_SLD = DR_NP + 2;   // staging row stride (doubles): conflict-free fragment loads
 constexpr int DR_SCR = 264;         // per-warp scratch: Y^T staging 16 x 12, G 8 x 8, tau 8
-__host__ __device__ constexpr int dr_ldr(int p) { return DR_NP - 8 * p + 2; }
-__host__ __device__ constexpr int dr_pbase(int p) { return 8 * (p * (DR_NP + 2) - 4 * p * (p - 1)); }
+// The ring kernel is built for NP = 128 (64 < n <= 128, one CTA per SM) and
+// NP = 64 (32 < n <= 64: half the registers and shared memory, two CTAs per SM).
+template <int NP = DR_NP>
+__host__ __device__ constexpr int dr_ldr(int p) { return NP - 8 * p + 2; }
+template <int NP = DR_NP>
+__host__ __device__ constexpr int dr_pbase(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
+template <int NP = DR_NP>
 struct DmmaRingSmem {
-  static constexpr int RP = dr_pbase(DR_NCB);
-  static constexpr size_t doubles = (size_t)RP + DR_WARPS * DR_H * DR_SLD + DR_WARPS * DR_SCR;
-  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * 2 * DR_NCB;
+  static constexpr int NCB = NP / 8;
+  static constexpr int SLD = NP + 2;  // conflict-free fragment loads (SLD = 2 mod 16)
+  static constexpr int RP = dr_pbase<NP>(NCB);
+  static constexpr int MINB = NP == 128 ? 1 : 2;  // CTAs per SM
+  static constexpr size_t doubles = (size_t)RP + DR_WARPS * DR_H * SLD + DR_WARPS * DR_SCR;
+  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * 2 * NCB;
 };
 
 // Stage tile rows [row0, row0 + valid) of A into the warp's staging buffer
 // (cp.async, zero fill below `valid`); V16: 16-byte granules (n, lda even).
-template <bool V16>
+template <int NP, bool V16>
 __device__ __forceinline__ void dr_issue(double* stage, const double* __restrict__ A, int64_t lda,
                                          int64_t row0, int valid, int n) {
   const int lane = threadIdx.x & 31;
@@ -59,22 +67,22 @@ __device__ __forceinline__ void dr_issue(double* stage, const double* __restrict
   if constexpr (V16) {
     const int cpr = n >> 1;
 #pragma unroll 4
-    for (int idx = lane; idx < DR_H * 64; idx += 32) {
-      const int r = idx >> 6, c2 = idx & 63;
+    for (int idx = lane; idx < DR_H * NP / 2; idx += 32) {
+      const int r = idx / (NP / 2), c2 = idx % (NP / 2);
       if (c2 < cpr) {
         const bool ok = r < valid;
         const double* src = ok ? A + (row0 + r) * lda + 2 * c2 : A;
-        cp_async<16>(sb + 8u * (unsigned)(r * DR_SLD + 2 * c2), src, ok ? 16u : 0u);
+        cp_async<16>(sb + 8u * (unsigned)(r * (NP + 2) + 2 * c2), src, ok ? 16u : 0u);
       }
     }
   } else {
 #pragma unroll 4
-    for (int idx = lane; idx < DR_H * DR_NP; idx += 32) {
-      const int r = idx >> 7, c = idx & 127;
+    for (int idx = lane; idx < DR_H * NP; idx += 32) {
+      const int r = idx / NP, c = idx % NP;
       if (c < n) {
         const bool ok = r < valid;
         const double* src = ok ? A + (row0 + r) * lda + c : A;
-        cp_async<8>(sb + 8u * (unsigned)(r * DR_SLD + c), src, ok ? 8u : 0u);
+        cp_async<8>(sb + 8u * (unsigned)(r * (NP + 2) + c), src, ok ? 8u : 0u);
       }
     }
   }
@@ -250,8 +258,8 @@ __device__ __forceinline__ void dr_upd(double (&Cb)[2][2], const double (&x)[4],
   dmma(Cb[1][0], Cb[1][1], -u1, vb[1][1]);
 }
 
-template <bool V16, bool Q>
-__global__ void __launch_bounds__(DR_WARPS * 32, 1)
+template <int NP, bool V16, bool Q>
+__global__ void __launch_bounds__(DR_WARPS * 32, DmmaRingSmem<NP>::MINB)
 k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag,
             int h0) {
@@ -260,10 +268,12 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   // (k_leaf_dense); Y / tau (nullable) receive each chain tile's TRI_ON_RECT factor in the
   // layout of k_leaf_chain<128, 16> (tile t: Y rows h0 + 16t.., tau at (t + 1) * n).
   // Y may alias A (tile rows are staged before they are overwritten).
+  using SM = DmmaRingSmem<NP>;
+  constexpr int NCB = SM::NCB, SLD = SM::SLD;
   extern __shared__ __align__(16) double sm[];
   double* Rp = sm;
-  double* stage_all = Rp + DmmaRingSmem::RP;
-  double* scr_all = stage_all + DR_WARPS * DR_H * DR_SLD;
+  double* stage_all = Rp + SM::RP;
+  double* scr_all = stage_all + DR_WARPS * DR_H * SLD;
   int* ver = reinterpret_cast<int*>(scr_all + DR_WARPS * DR_SCR);  // one counter per panel
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -275,20 +285,20 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   const int T = (int)((rest + DR_H - 1) / DR_H);
   const int npan = (n + 7) >> 3;
   double* Rl = Rio + (int64_t)leaf * n * n;
-  for (int i = threadIdx.x; i < DmmaRingSmem::RP; i += DR_WARPS * 32) {
+  for (int i = threadIdx.x; i < SM::RP; i += DR_WARPS * 32) {
     double v = 0.0;
     if (Q || h0) {  // panel-packed index -> (r, c)
       int pp = 0;
-      while (pp + 1 < DR_NCB && dr_pbase(pp + 1) <= i) ++pp;
-      const int off = i - dr_pbase(pp), ld = dr_ldr(pp);
+      while (pp + 1 < NCB && dr_pbase<NP>(pp + 1) <= i) ++pp;
+      const int off = i - dr_pbase<NP>(pp), ld = dr_ldr<NP>(pp);
       const int r = 8 * pp + off / ld, c = 8 * pp + off % ld;
       if (r < n && c < n && c >= r) v = Rl[r * n + c];
     }
     Rp[i] = v;
   }
   double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
-  if (threadIdx.x < 2 * DR_NCB) ver[threadIdx.x] = 0;
-  double* stage = stage_all + w * DR_H * DR_SLD;
+  if (threadIdx.x < 2 * NCB) ver[threadIdx.x] = 0;
+  double* stage = stage_all + w * DR_H * SLD;
   double* vs = scr_all + w * DR_SCR;  // 16 x 12
   double* gs = vs + 192;
   double* taus = gs + 64;
@@ -296,28 +306,28 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   bool bad = false;
   if (w < T) {
     const int64_t row = r0 + h0 + (int64_t)w * DR_H;
-    dr_issue<V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
+    dr_issue<NP, V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
   }
   DR_TICK(k0_);
   for (int t = w; t < T; t += DR_WARPS) {
     cp_async_wait<0>();
     __syncwarp();
-    double C[DR_NCB][2][2];  // [column block][row block][e]
+    double C[NCB][2][2];  // [column block][row block][e]
 #pragma unroll
-    for (int cb = 0; cb < DR_NCB; ++cb)
+    for (int cb = 0; cb < NCB; ++cb)
 #pragma unroll
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 8 * cb + g;
-          double v = stage[(8 * bb + 2 * q + e) * DR_SLD + c];
+          double v = stage[(8 * bb + 2 * q + e) * SLD + c];
           v = (c < n) ? v : 0.0;
           C[cb][bb][e] = v;
         }
     __syncwarp();
     if (t + DR_WARPS < T) {
       const int64_t row = r0 + h0 + (int64_t)(t + DR_WARPS) * DR_H;
-      dr_issue<V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
+      dr_issue<NP, V16>(stage, A, lda, row, (int)min64(DR_H, r0 + b - row), n);
     }
     const int64_t trow = r0 + h0 + (int64_t)t * DR_H;  // this tile's first row
     const int tvalid = (int)min64(DR_H, r0 + b - trow);
@@ -326,7 +336,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
     DR_TICK(c0_);
     dr_wait(ver, t, lane);
     {
-      const int l0 = dr_ldr(0);
+      const int l0 = dr_ldr<NP>(0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) rg[i] = Rp[i * l0 + g];
       x[0] = C[0][0][0]; x[1] = C[0][0][1]; x[2] = C[0][1][0]; x[3] = C[0][1][1];
@@ -342,8 +352,8 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
     DR_TICK(c1_);
     DR_ADD(0, c0_, c1_);
     for (int p = 0; p < npan; ++p) {
-      const int ldr = dr_ldr(p);
-      double* Rpan = Rp + dr_pbase(p);
+      const int ldr = dr_ldr<NP>(p);
+      double* Rpan = Rp + dr_pbase<NP>(p);
       DR_TICK(c2_);
       // L2(p) stored R_pp, G and tau as it went; publish R_pp
       dr_signal(ver + p, t + 1, lane);  // (__syncwarp first: gs / taus visible)
@@ -383,12 +393,13 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         // ---- look-ahead block: L2(p+1) || blocks 2 .. nl-1 by panel p ----
         // (interleaved in the source: ptxas keeps this order at this register
         // pressure, so the update DMMAs run in the shadow of the reflector chain)
-        const int ldr1 = dr_ldr(p + 1);
-        double* Rpan1 = Rp + dr_pbase(p + 1);
+        const int ldr1 = dr_ldr<NP>(p + 1);
+        double* Rpan1 = Rp + dr_pbase<NP>(p + 1);
 #pragma unroll
         for (int i = 0; i < 8; ++i) rg[i] = Rpan1[i * ldr1 + g];
         double xn[4] = {C[1][0][0], C[1][0][1], C[1][1][0], C[1][1][1]};
-#define DR_UPD(CB) if ((CB) < nl) dr_upd(C[CB], x, vb, tb0, tb1, rrow + 8 * (CB), ldr)
+#define DR_UPD(CB) \
+  if constexpr ((CB) < NCB) { if ((CB) < nl) dr_upd(C[CB], x, vb, tb0, tb1, rrow + 8 * (CB), ldr); }
         dr_gen<0>(xn, rg[0], Rpan1, gs, taus);
         DR_UPD(2); DR_UPD(3);
         dr_gen<1>(xn, rg[1], Rpan1 + ldr1, gs, taus);
@@ -412,7 +423,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
       }
       // shift the register blocks: the next panel becomes block 0
 #pragma unroll
-      for (int cb = 0; cb + 1 < DR_NCB; ++cb)
+      for (int cb = 0; cb + 1 < NCB; ++cb)
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb) {
           C[cb][bb][0] = C[cb + 1][bb][0];
@@ -429,7 +440,7 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
   for (int idx = threadIdx.x; idx < n * n; idx += DR_WARPS * 32) {
     const int r = idx / n, c = idx - r * n;
     const int p = r >> 3;
-    const double v = (c >= r) ? Rp[dr_pbase(p) + (r & 7) * dr_ldr(p) + (c - 8 * p)] : 0.0;
+    const double v = (c >= r) ? Rp[dr_pbase<NP>(p) + (r & 7) * dr_ldr<NP>(p) + (c - 8 * p)] : 0.0;
     bad |= !isfinite(v);
     Rl[idx] = v;
   }

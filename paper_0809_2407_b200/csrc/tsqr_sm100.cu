@@ -47,11 +47,12 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // ---------------------------------------------------------------------------
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
-static int g_ht[3] = {16, 24, 16};  // NP = 32, 64, 128 (measured best)
+static int g_ht[3] = {16, 16, 16};  // NP = 32, 64, 128 (16: the DMMA rings' tile)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
-static int g_dmma = 1;     // CAQR_TUNE_DMMA: n in (64,128] leaves on the DMMA warp ring
+static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
+static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves on the DMMA ring
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (64,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -1127,12 +1128,13 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
                              st>>>(A, lda, m, (int)n, (int)P, base, Y, ldy, tau, tau_stride, R,  \
                                    flag, zs ? 1 : 0);                                            \
   }
-#define DMMA_LAUNCH(V16, Q)                                                                     \
+#define DMMA_LAUNCH(NPX, V16, Q)                                                                 \
   {                                                                                             \
-    rc = prep(k_leaf_dmma<V16, Q>, DmmaRingSmem::bytes);                                        \
+    constexpr int NPD = NPX == 128 ? 128 : 64;                                                  \
+    rc = prep(k_leaf_dmma<NPD, V16, Q>, DmmaRingSmem<NPD>::bytes);                              \
     if (rc) return rc;                                                                          \
-    k_leaf_dmma<V16, Q><<<grid, DR_WARPS * 32, DmmaRingSmem::bytes, st>>>(A, lda, m, (int)n,    \
-        (int)P, base, Y, ldy, tau, tau_stride, R, flag, h0d);                                   \
+    k_leaf_dmma<NPD, V16, Q><<<grid, DR_WARPS * 32, DmmaRingSmem<NPD>::bytes, st>>>(A, lda, m,  \
+        (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag, h0d);                           \
   }
 #define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
@@ -1144,13 +1146,14 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if (NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) {                                      \
+    if ((NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) ||                                    \
+        (NPV == 64 && g_dmma >= 2 && (zs || g_ht[1] == 16))) {                                  \
       const int h0d = zs ? 0 : WARPS * Geo<NPV>::HD;                                            \
       const bool v16 = (n % 2 == 0) && (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);            \
-      if (v16 && Y) DMMA_LAUNCH(true, true)                                                     \
-      else if (v16) DMMA_LAUNCH(true, false)                                                    \
-      else if (Y) DMMA_LAUNCH(false, true)                                                      \
-      else DMMA_LAUNCH(false, false)                                                            \
+      if (v16 && Y) DMMA_LAUNCH(NPV, true, true)                                                     \
+      else if (v16) DMMA_LAUNCH(NPV, true, false)                                                    \
+      else if (Y) DMMA_LAUNCH(NPV, false, true)                                                      \
+      else DMMA_LAUNCH(NPV, false, false)                                                            \
     } else if (NPV == 128 && zs && g_blocked) {                                                 \
       rc = prep(k_leaf_blocked, BlockedSmem::bytes);                                         \
       if (rc) return rc;                                                                        \
@@ -1362,6 +1365,22 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
+  if (!transpose && g_dmma_q && ((p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16))) {
+#define LQ_LAUNCH(NPV, KBQ, MB)                                                                    \
+    {                                                                                             \
+      const size_t sm = DmmaQSmem<NPV, KBQ>::bytes;                                               \
+      dim3 gq((unsigned)P, (unsigned)((ncols + KBQ - 1) / KBQ));                                  \
+      int rc = prep(k_leaf_q_dmma<NPV, KBQ, MB>, sm); if (rc) return rc;                          \
+      k_leaf_q_dmma<NPV, KBQ, MB><<<gq, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,     \
+          (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init);                           \
+    }
+    if (p == 128) LQ_LAUNCH(128, 64, 1)
+    else if (g_dmma_q == 2) LQ_LAUNCH(64, 32, 2)
+    else if (g_dmma_q == 3) LQ_LAUNCH(64, 64, 1)
+    else LQ_LAUNCH(64, 64, 2)
+#undef LQ_LAUNCH
+    return check_launch("k_leaf_q_dmma");
+  }
   switch (p) {
     LA_CASE(32, 1, 16, 32)
     case 64: {
@@ -1474,12 +1493,18 @@ int caqr_tune(int key, int value) {
     g_blocked = value ? 1 : 0;
     return CAQR_OK;
   }
+  if (key == CAQR_TUNE_DMMA_Q) {
+    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_Q takes 0 .. 3");
+    g_dmma_q = value;
+    return CAQR_OK;
+  }
   if (key == CAQR_TUNE_DMMA_APPLY) {
     g_dmma_apply = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA) {
-    g_dmma = value ? 1 : 0;
+    if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0, 1 or 2");
+    g_dmma = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_ZSTART) {

@@ -294,13 +294,13 @@ def test_tuning_variants_keep_parity():
         assert oracle.orthogonality(Q) <= 10 * 100 * EPS
         assert oracle.residual(A, Q, R) <= 10 * 100 * EPS
     finally:
-        _lib.tune(_lib.TUNE_CHAIN_HT[128], 16)
+        _lib.reset_tuning()
     try:
         _lib.tune(_lib.TUNE_ZSTART, 0)
         R0 = tsqr(A, leaf_rows=5000)  # dense first tile, ring tree
         assert oracle.r_diff(R0, Rref, scale) <= 1000 * EPS
     finally:
-        _lib.tune(_lib.TUNE_ZSTART, 1)
+        _lib.reset_tuning()
     assert oracle.r_diff(tsqr(A, leaf_rows=5000), Rref, scale) <= 1000 * EPS
 
 
@@ -341,7 +341,7 @@ def test_blocked_tall_tile_leaf_parity():
         with pytest.raises(ValueError):
             factor_device(torch.from_numpy(A).cuda(), 2)
     finally:
-        _lib.tune(_lib.TUNE_BLOCKED, 0)
+        _lib.reset_tuning()
 
 
 @pytest.mark.parametrize("v16", [True, False])
@@ -376,7 +376,7 @@ def test_dmma_ring_leaf_parity(v16):
         with pytest.raises(ValueError):
             factor_device(torch.from_numpy(A).cuda(), 2)
     finally:
-        _lib.tune(_lib.TUNE_DMMA, 1)
+        _lib.reset_tuning()
 
 
 def test_dmma_ring_matches_rank1_ring():
@@ -391,7 +391,7 @@ def test_dmma_ring_matches_rank1_ring():
         _lib.tune(_lib.TUNE_DMMA, 0)
         Rr = factor_device(A, 32).R.cpu().numpy()
     finally:
-        _lib.tune(_lib.TUNE_DMMA, 1)
+        _lib.reset_tuning()
     nA = np.linalg.norm(Rr, 2)
     assert oracle.r_diff(Rd, Rr, nA) <= 1000 * EPS
 
@@ -416,7 +416,7 @@ def test_dmma_leaf_apply_matches_ring(shape):
         _lib.tune(_lib.TUNE_DMMA_APPLY, 0)
         Qr = apply_q_device(f, C, transpose=True)
     finally:
-        _lib.tune(_lib.TUNE_DMMA_APPLY, 1)
+        _lib.reset_tuning()
     scale = torch.linalg.norm(C).item()
     assert torch.linalg.norm(Qd - Qr).item() <= 100 * n * EPS * scale
     # round trip: Q (Q^T C) = C
@@ -453,9 +453,111 @@ def test_dmma_kernels_random_shapes():
             R0 = factor_device(A, P).R
             Qr = apply_q_device(f0, C, transpose=True)
         finally:
-            _lib.tune(_lib.TUNE_DMMA, 1)
-            _lib.tune(_lib.TUNE_DMMA_APPLY, 1)
+            _lib.reset_tuning()
         nA = torch.linalg.norm(A, 2).item()
         assert (sgn(R1) - sgn(R0)).abs().max().item() <= 100 * EPS * nA, (m, n, P)
         assert (f.R - f0.R).abs().max().item() <= 100 * EPS * nA, (m, n, P)
         assert torch.linalg.norm(Qd - Qr).item() <= 100 * EPS * torch.linalg.norm(C).item(), (m, n, P, k)
+
+
+@pytest.mark.parametrize("m,n,P", [(1500, 64, 2), (4096, 48, 5), (999, 33, 3), (20000, 64, 4)])
+def test_dmma_ring_np64_matches_oracle(m, n, P):
+    """CAQR_TUNE_DMMA = 2 with CAQR_TUNE_CHAIN_HT_64 = 16: leaves with n in (32, 64] on
+    the NP = 64 DMMA ring (two CTAs per SM).  Its chain-tile factors (Y, tau) and the
+    tree factors against the oracle's hybrid chain element-wise, explicit Q against the
+    oracle's Q, and the R-only (zero-start) leaves against LAPACK; odd n takes the 8-byte
+    staging path."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
+
+    A = philox(5 * m + n).standard_normal((m, n))
+    try:
+        _lib.tune(_lib.TUNE_DMMA, 2)
+        _lib.tune(_lib.TUNE_CHAIN_HT[64], 16)
+        _, h0, ht = geom(n)
+        assert ht == 16
+        f = factor(A, P)
+        Q = explicit_q_device(f).cpu().numpy()
+        Rz = factor(A, P, want_q=False).R.cpu().numpy()
+    finally:
+        _lib.reset_tuning()
+    ref = oracle.tsqr_hybrid(A, P, h0, ht)
+    scale = np.linalg.norm(A, 2)
+    R = f.R.cpu().numpy()
+    assert np.max(np.abs(R - ref["R"])) <= 200 * EPS * scale
+    Y, tau, offs = f.Y.cpu().numpy(), f.tau.cpu().numpy(), ref["offs"]
+    for i, tiles in enumerate(ref["leaves"]):
+        bnds = oracle.tsqr.chain_tiles(offs[i + 1] - offs[i], h0, ht)
+        for k, ((V, t), (s, e)) in enumerate(zip(tiles[1:], bnds[1:]), start=1):
+            Vg = Y[offs[i] + s: offs[i] + e]
+            assert np.max(np.abs(Vg - V)) <= 1e-9 * max(1.0, np.max(np.abs(V))), (i, k)
+            assert np.max(np.abs(tau[i, k] - t)) <= 1e-12, (i, k)
+    Qref = oracle.tsqr_hybrid_q(ref)
+    assert np.max(np.abs(Q - Qref)) <= 1e-11
+    assert oracle.residual(A, Q, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q) <= 10 * n * EPS
+    assert np.array_equal(Rz, np.triu(Rz))
+    assert oracle.r_diff(Rz, np.linalg.qr(A, mode="r"), scale) <= 1000 * EPS
+
+
+@pytest.mark.parametrize("n,variant", [(64, 1), (64, 2), (64, 3), (40, 1), (128, 1), (99, 1)])
+def test_dmma_leaf_q_matches_ring(n, variant):
+    """CAQR_TUNE_DMMA_Q (1 = NP 64 with 64-column CTAs, 2 = 32-column CTAs, 3 = one CTA per
+    SM): Q C on the backward DMMA ring + reverse-panel dense tile equals the
+    reflector-by-reflector ring (= 0) for explicit Q, thin Q C (S path, zero-initialised
+    rows) and full Q C (C's own rows), and Q^T (Q C) = C."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, explicit_q_device, factor_device
+
+    m, P, k = 3 * 2500 + 37, 3, 300
+    A = torch.from_numpy(philox(n + variant).standard_normal((m, n))).cuda()
+    Cf = torch.from_numpy(philox(2 * n).standard_normal((m, k))).cuda()
+    Ct = torch.from_numpy(philox(3 * n).standard_normal((n, k))).cuda()
+    try:
+        _lib.tune(_lib.TUNE_DMMA, 2)
+        _lib.tune(_lib.TUNE_CHAIN_HT[64], 16)
+        f = factor_device(A, P, want_q=True)
+        out = []
+        for qv in (variant, 0):
+            _lib.tune(_lib.TUNE_DMMA_Q, qv)
+            out.append((explicit_q_device(f), apply_q_device(f, Ct, transpose=False),
+                        apply_q_device(f, Cf, transpose=False)))
+        back = apply_q_device(f, out[0][2], transpose=True)  # same chain geometry as f
+    finally:
+        _lib.reset_tuning()
+    (Qd, Td, Fd), (Qr, Tr, Fr) = out
+    assert (Qd - Qr).abs().max().item() <= 1e-12
+    assert torch.linalg.norm(Td - Tr).item() <= 100 * n * EPS * torch.linalg.norm(Ct).item()
+    assert torch.linalg.norm(Fd - Fr).item() <= 100 * n * EPS * torch.linalg.norm(Cf).item()
+    assert torch.linalg.norm(back - Cf).item() <= 100 * n * EPS * torch.linalg.norm(Cf).item()
+
+
+@pytest.mark.parametrize("dmma,ht", [(1, 24), (1, 16), (0, 24)])
+def test_np64_chain_variants_keep_parity(dmma, ht):
+    """n in (32, 64] off the default DMMA path: the rank-1 chain with 24- or 16-row
+    tiles (CAQR_TUNE_DMMA = 1 / 0, CAQR_TUNE_CHAIN_HT_64) and the reflector-ring Q / Q^T
+    applies; R, explicit Q and Q^T C against LAPACK / the oracle's invariants."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, explicit_q_device, factor_device
+
+    m, n, P = 6000, 56, 3
+    A = philox(4 * ht + dmma).standard_normal((m, n))
+    C = torch.from_numpy(philox(9).standard_normal((m, 70))).cuda()
+    try:
+        _lib.tune(_lib.TUNE_DMMA, dmma)
+        _lib.tune(_lib.TUNE_CHAIN_HT[64], ht)
+        assert geom(n)[2] == ht
+        f = factor(A, P)
+        Q = explicit_q_device(f).cpu().numpy()
+        QtC = apply_q_device(f, C, transpose=True)
+        back = apply_q_device(f, QtC, transpose=False)
+        Rz = factor(A, P, want_q=False).R.cpu().numpy()
+    finally:
+        _lib.reset_tuning()
+    R = f.R.cpu().numpy()
+    scale = np.linalg.norm(A, 2)
+    assert oracle.r_diff(R, np.linalg.qr(A, mode="r"), scale) <= 1000 * EPS
+    assert oracle.r_diff(Rz, np.linalg.qr(A, mode="r"), scale) <= 1000 * EPS
+    assert oracle.residual(A, Q, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q) <= 10 * n * EPS
+    assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * torch.linalg.norm(C).item()

@@ -9,12 +9,15 @@ namespace tsqr {
 #include "../paper_0809_2407_b200/csrc/dmma_ring.cuh"
 }
 using namespace tsqr;
+#ifndef DR_NPX
+#define DR_NPX 128
+#endif
 #ifndef DR_KERNEL
 #define DR_KERNEL k_leaf_dmma
 #endif
 int main(int argc, char** argv) {
   const int P = argc > 1 ? atoi(argv[1]) : 148;
-  const int64_t b = 8192, n = 128, m = b * P;
+  const int64_t b = argc > 2 ? atoll(argv[2]) : 8192, n = DR_NPX, m = b * P;
   std::vector<double> h(m * n);
   std::mt19937_64 rng(1);
   std::normal_distribution<double> nd;
@@ -25,7 +28,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&R, P * n * n * 8);
   cudaMalloc(&flag, 4);
   cudaMemcpy(A, h.data(), m * n * 8, cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(DR_KERNEL<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem::bytes);
+  cudaFuncSetAttribute(DR_KERNEL<DR_NPX, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DmmaRingSmem<DR_NPX>::bytes);
   for (int it = 0; it < 2; ++it) {
     unsigned long long z[8] = {};
     cudaMemcpyToSymbol(g_dr_cycles, z, sizeof(z));
@@ -33,7 +36,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    DR_KERNEL<true, false><<<P, 256, DmmaRingSmem::bytes>>>(A, n, m, n, P, b, nullptr, 0, nullptr, 0, R, flag, 0);
+    DR_KERNEL<DR_NPX, true, false><<<P, 256, DmmaRingSmem<DR_NPX>::bytes>>>(A, n, m, n, P, b, nullptr, 0, nullptr, 0, R, flag, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms;
