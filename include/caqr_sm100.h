@@ -154,9 +154,11 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * ring, two CTAs per SM; implicit-Q leaves need CAQR_TUNE_CHAIN_HT_64 = 16); 0 = the rank-1
  * warp ring. */
 #define CAQR_TUNE_DMMA 9
-/* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with n in (64, 128] and 16-row chain
- * tiles (the CAQR trailing update) runs the DMMA ring (compact-WY per 8-reflector panel on the
- * FP64 tensor cores); 0 = the reflector-by-reflector warp ring. */
+/* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with 16-row chain tiles (the CAQR
+ * trailing update) runs on the DMMA ring (compact-WY per 8-reflector panel on the FP64 tensor
+ * cores): n in (64, 128] on k_leaf_apply_dmma, n in (32, 64] on k_leaf_q_dmma (64-column CTAs,
+ * two per SM; 2 = 32-column CTAs, 3 = one CTA per SM); 0 = the reflector-by-reflector warp
+ * ring. */
 #define CAQR_TUNE_DMMA_APPLY 10
 /* CAQR_TUNE_DMMA_Q: 1 (default) = Q C (explicit Q, apply_q) for leaves with 16-row chain tiles
  * and n in (32, 128] runs the DMMA ring backward (compact WY per 8-reflector panel, panels in

@@ -314,7 +314,7 @@ struct DmmaQSmem {
   static constexpr int MINB = NP == 128 ? 1 : 2;
 };
 
-template <int NP, int KB, int MB = DmmaQSmem<NP, KB>::MINB>
+template <int NP, int KB, int MB, bool TR>
 __global__ void __launch_bounds__(THREADS, MB)
 k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
               int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
@@ -350,8 +350,9 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
   }
   if (threadIdx.x < NP / 8) ver[threadIdx.x] = 0;
   __syncthreads();
+  auto chain = [&]() {
   for (int o = w; o < T; o += WARPS) {
-    const int t = T - 1 - o;
+    const int t = TR ? o : T - 1 - o;
     const int64_t row = H0 + (int64_t)t * DR_H;
     const int valid = (int)min64(DR_H, b - row);
     double Ct[CB][2][2];
@@ -367,16 +368,17 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
     const double* Yt = Yl + row * ldy;
     const double* tt = tl + (int64_t)(t + 1) * n;
     DaPanel cur, nxt;
-    da_load_panel(cur, Yt, ldy, tt, valid, n, 8 * (npan - 1));
+    da_load_panel(cur, Yt, ldy, tt, valid, n, TR ? 0 : 8 * (npan - 1));
     nxt = cur;
     double tb0, tb1;
-    da_form_t<false>(cur, tb0, tb1);
-    for (int p = npan - 1; p >= 0; --p) {
-      if (p > 0) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p - 1));
+    da_form_t<TR>(cur, tb0, tb1);
+    for (int i = 0; i < npan; ++i) {
+      const int p = TR ? i : npan - 1 - i;
+      if (i + 1 < npan) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (TR ? p + 1 : p - 1));
       dr_wait(ver + p, o, lane);
       double* rrow = Cs + (8 * p + 2 * q) * LDC + g;
       double tn0, tn1;
-      da_form_t<false>(nxt, tn0, tn1);  // stale for p = 0, discarded
+      da_form_t<TR>(nxt, tn0, tn1);  // stale for the last panel, discarded
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb)
         dr_upd(Ct[cb], cur.x, cur.vb, tb0, tb1, rrow + 8 * cb, LDC);
@@ -395,7 +397,11 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
           if (r < valid && c < ncb) Cl[(row + r) * ldc + c] = Ct[cb][bb][e];
         }
   }
-  __syncthreads();
+  };
+  if (!TR) {
+    chain();
+    __syncthreads();
+  }
   // dense first tile: warp w holds rows HD w + 16 j + .., j < RG
   double Cd[RG][CB][2][2];
 #pragma unroll
@@ -415,7 +421,8 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
   auto vdense = [&](int r, int c) {  // V[r][c] of the dense tile (unit lower trapezoidal)
     return (r >= b || c >= n) ? 0.0 : (r > c ? __ldg(Yl + (int64_t)r * ldy + c) : (r == c ? 1.0 : 0.0));
   };
-  for (int p = npan - 1; p >= 0; --p) {
+  for (int i = 0; i < npan; ++i) {
+    const int p = TR ? i : npan - 1 - i;
     const int pc = 8 * p;
     const int wmin = pc / HD;  // warps holding rows >= pc
     const bool active = w >= wmin;
@@ -464,7 +471,7 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
       Pn.tq0 = (pc + 2 * q < n) ? __ldg(tl + pc + 2 * q) : 0.0;
       Pn.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tl + pc + 2 * q + 1) : 0.0;
       double tb0, tb1;
-      da_form_t_g<false>(Pn, G, tb0, tb1);
+      da_form_t_g<TR>(Pn, G, tb0, tb1);
       for (int cb = w; cb < CB; cb += WARPS) {
         double w0 = 0.0, w1 = 0.0;
         for (int w2 = wmin; w2 < WARPS; ++w2) {
@@ -504,8 +511,18 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = HD * w + 16 * j + 8 * bb + 2 * q + e, c = 8 * cb + g;
-          if (r < b && c < ncb) Cl[(int64_t)r * ldc + c] = Cd[j][cb][bb][e];
+          if (TR && r < n) Cs[r * LDC + c] = Cd[j][cb][bb][e];  // the chain's pivot rows
+          else if (r < b && c < ncb) Cl[(int64_t)r * ldc + c] = Cd[j][cb][bb][e];
         }
+  if (TR) {
+    __syncthreads();
+    chain();
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * KB; idx += THREADS) {
+      const int r = idx / KB, c = idx - r * KB;
+      if (c < ncb) Cl[(int64_t)r * ldc + c] = Cs[r * LDC + c];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

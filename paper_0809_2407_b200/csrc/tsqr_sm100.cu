@@ -53,7 +53,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves on the DMMA ring
-static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (64,128] chain leaves on the DMMA ring
+static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -1365,19 +1365,25 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
-  if (!transpose && g_dmma_q && ((p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16))) {
-#define LQ_LAUNCH(NPV, KBQ, MB)                                                                    \
+  const bool q16 = (p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16);
+  if ((!transpose && g_dmma_q && q16) || (transpose && p == 64 && g_dmma_apply && q16)) {
+#define LQ_LAUNCH(NPV, KBQ, MB, TR)                                                               \
     {                                                                                             \
       const size_t sm = DmmaQSmem<NPV, KBQ>::bytes;                                               \
       dim3 gq((unsigned)P, (unsigned)((ncols + KBQ - 1) / KBQ));                                  \
-      int rc = prep(k_leaf_q_dmma<NPV, KBQ, MB>, sm); if (rc) return rc;                          \
-      k_leaf_q_dmma<NPV, KBQ, MB><<<gq, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,     \
-          (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init);                           \
+      int rc = prep(k_leaf_q_dmma<NPV, KBQ, MB, TR>, sm); if (rc) return rc;                      \
+      k_leaf_q_dmma<NPV, KBQ, MB, TR><<<gq, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,         \
+          (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init);                   \
     }
-    if (p == 128) LQ_LAUNCH(128, 64, 1)
-    else if (g_dmma_q == 2) LQ_LAUNCH(64, 32, 2)
-    else if (g_dmma_q == 3) LQ_LAUNCH(64, 64, 1)
-    else LQ_LAUNCH(64, 64, 2)
+    const int var = transpose ? g_dmma_apply : g_dmma_q;
+    if (transpose) {
+      if (var == 2) LQ_LAUNCH(64, 32, 2, true)
+      else if (var == 3) LQ_LAUNCH(64, 64, 1, true)
+      else LQ_LAUNCH(64, 64, 2, true)
+    } else if (p == 128) LQ_LAUNCH(128, 64, 1, false)
+    else if (var == 2) LQ_LAUNCH(64, 32, 2, false)
+    else if (var == 3) LQ_LAUNCH(64, 64, 1, false)
+    else LQ_LAUNCH(64, 64, 2, false)
 #undef LQ_LAUNCH
     return check_launch("k_leaf_q_dmma");
   }
@@ -1499,7 +1505,8 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_APPLY) {
-    g_dmma_apply = value ? 1 : 0;
+    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_APPLY takes 0 .. 3");
+    g_dmma_apply = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA) {

@@ -561,3 +561,28 @@ def test_np64_chain_variants_keep_parity(dmma, ht):
     assert oracle.residual(A, Q, R) <= 10 * n * EPS
     assert oracle.orthogonality(Q) <= 10 * n * EPS
     assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * torch.linalg.norm(C).item()
+
+
+@pytest.mark.parametrize("n,variant", [(64, 1), (64, 2), (64, 3), (37, 1)])
+def test_dmma_leaf_qt_np64_matches_ring(n, variant):
+    """CAQR_TUNE_DMMA_APPLY for n in (32, 64] (k_leaf_q_dmma with TR: dense tile forward,
+    then the chain ring forward, T^T): Q^T C equals the reflector ring (= 0), on ragged
+    leaves and a column count that is not a multiple of the CTA width, and Q (Q^T C) = C."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, factor_device
+
+    m, P, k = 4 * 1900 + 13, 4, 150
+    A = torch.from_numpy(philox(7 * n + variant).standard_normal((m, n))).cuda()
+    C = torch.from_numpy(philox(8 * n).standard_normal((m, k))).cuda()
+    f = factor_device(A, P, want_q=True)
+    try:
+        _lib.tune(_lib.TUNE_DMMA_APPLY, variant)
+        Qd = apply_q_device(f, C, transpose=True)
+        back = apply_q_device(f, Qd, transpose=False)
+        _lib.tune(_lib.TUNE_DMMA_APPLY, 0)
+        Qr = apply_q_device(f, C, transpose=True)
+    finally:
+        _lib.reset_tuning()
+    scale = torch.linalg.norm(C).item()
+    assert torch.linalg.norm(Qd - Qr).item() <= 100 * n * EPS * scale
+    assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * scale

@@ -45,11 +45,13 @@ for rnd in range(3):
 for k in cases:
     print(f"{k}: {min(res[k]):.3f} ms")
 
-for ht in (24, 16):
+for ht, av in ((24, 0), (16, 0), (16, 1), (16, 2), (16, 3)):
     _lib.tune(H, ht)
+    _lib.tune(_lib.TUNE_DMMA_APPLY, av)
     f = factor_device(A64, 512, want_q=True, check=False)
-    print(f"Q^T C 2^21x64 (k=64) ht64={ht}: {timeit(lambda: apply_q_device(f, C64, True)):.3f} ms")
-_lib.tune(H, 24)
+    print(f"Q^T C 2^21x64 (k=64) ht64={ht} dmma_apply={av}: "
+          f"{timeit(lambda: apply_q_device(f, C64, True)):.3f} ms")
+_lib.reset_tuning()
 f = factor_device(A128, 128, want_q=True, check=False)
 for qv in (0, 1):
     _lib.tune(Q, qv)
