@@ -40,7 +40,7 @@ enum Mode { DENSE = 0, STACKED = 1, TRIRECT = 2, STACKEDQ = 3 };
 // tunable template parameter of the chain / apply kernels.
 template <int NP> struct Geo;
 template <> struct Geo<32>  { static constexpr int S = 1, HD = 32; };
-template <> struct Geo<64>  { static constexpr int S = 2, HD = 32; };
+template <> struct Geo<64>  { static constexpr int S = 2, HD = 16; };
 template <> struct Geo<128> { static constexpr int S = 4, HD = 16; };
 // Warps of the factorization ring for a chain tile height (register budget:
 // 16 warps -> 128 regs, 8 warps -> 255 regs per thread).
