@@ -164,6 +164,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * and n in (32, 128] runs the DMMA ring backward (compact WY per 8-reflector panel, panels in
  * reverse order); 0 = the reflector-by-reflector warp ring. */
 #define CAQR_TUNE_DMMA_Q 11
+/* CAQR_TUNE_DMMA_TREE: 1 (default) = Q C / Q^T C of the tree nodes (STACKED factors) for
+ * n in (32, 128] runs k_tree_apply_dmma (compact WY per 8 reflectors, two CTA barriers per panel);
+ * 0 = the reflector-by-reflector k_tree_apply. */
+#define CAQR_TUNE_DMMA_TREE 12
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

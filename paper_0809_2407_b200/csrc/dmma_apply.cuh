@@ -547,10 +547,13 @@ struct TreeApplyDmmaSmem {
   static constexpr size_t bytes = sizeof(double) * doubles;
 };
 
+// TR = false: Q_node [C_a; C_b] (explicit Q / apply_q walking the tree down):
+// panels in reverse order with T instead of T^T; zero_partner: C_b starts at 0.
+template <bool TR>
 __global__ void __launch_bounds__(THREADS, 1)
 k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ taunode, int n,
                   const int* __restrict__ ev, double* C, int64_t ldc, int64_t slot_rows,
-                  int64_t ncols) {
+                  int64_t ncols, int zero_partner) {
   extern __shared__ __align__(16) double sm[];
   double* Ca = sm;                           // 128 x 66
   double* wpart = Ca + DR_NP * TA_LDC;       // [warp][refl 8][col 64]
@@ -577,7 +580,7 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int r = 16 * w + 8 * bb + 2 * q + e, c = 8 * cb + g;
-        Cb[cb][bb][e] = (r < n && c < ncb) ? Cbg[(int64_t)r * ldc + c] : 0.0;
+        Cb[cb][bb][e] = (!zero_partner && r < n && c < ncb) ? Cbg[(int64_t)r * ldc + c] : 0.0;
       }
   const int npan = (n + 7) >> 3;
   // T of every panel depends on the node factor only: build them all up front
@@ -614,12 +617,13 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
     P.tq0 = (pc + 2 * q < n) ? __ldg(tn + pc + 2 * q) : 0.0;
     P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tn + pc + 2 * q + 1) : 0.0;
     double tb0, tb1;
-    da_form_t_g(P, G, tb0, tb1);
+    da_form_t_g<TR>(P, G, tb0, tb1);
     tball[p * 64 + 2 * lane] = tb0;
     tball[p * 64 + 2 * lane + 1] = tb1;
   }
   __syncthreads();
-  for (int p = 0; p < npan; ++p) {
+  for (int i = 0; i < npan; ++i) {
+    const int p = TR ? i : npan - 1 - i;
     const int pc = 8 * p;
     const int wmax = min(WARPS - 1, (pc + 7) >> 4);  // warps holding nonzero rows of Y_p
     const bool active = w <= wmax;

@@ -53,6 +53,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves on the DMMA ring
+static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of n in (32,128] tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -1320,13 +1321,18 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
                                                    slot_rows, ncols, zero_partner);
     return check_launch("k_tree_apply_w32");
   }
-  if (p == 128 && transpose && !zero_partner && g_dmma_apply) {
+  if ((p == 128 || p == 64) && g_dmma_tree) {
     const size_t sm = TreeApplyDmmaSmem::bytes;
-    int rc = prep(k_tree_apply_dmma, sm);
-    if (rc) return rc;
     dim3 gd((unsigned)nev, (unsigned)((ncols + TA_KB - 1) / TA_KB));
-    k_tree_apply_dmma<<<gd, THREADS, sm, st>>>(Ynode, taunode, (int)n, events, C, ldc, slot_rows,
-                                               ncols);
+#define TAD_LAUNCH(TR)                                                                             \
+    {                                                                                              \
+      int rc = prep(k_tree_apply_dmma<TR>, sm);                                                    \
+      if (rc) return rc;                                                                           \
+      k_tree_apply_dmma<TR><<<gd, THREADS, sm, st>>>(Ynode, taunode, (int)n, events, C, ldc,      \
+                                                     slot_rows, ncols, zero_partner);             \
+    }
+    if (transpose) TAD_LAUNCH(true) else TAD_LAUNCH(false)
+#undef TAD_LAUNCH
     return check_launch("k_tree_apply_dmma");
   }
   switch (p) { TA_CASE(32) TA_CASE(64) TA_CASE(128) }
@@ -1497,6 +1503,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_BLOCKED) {
     g_blocked = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DMMA_TREE) {
+    g_dmma_tree = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_Q) {

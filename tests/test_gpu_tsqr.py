@@ -586,3 +586,29 @@ def test_dmma_leaf_qt_np64_matches_ring(n, variant):
     scale = torch.linalg.norm(C).item()
     assert torch.linalg.norm(Qd - Qr).item() <= 100 * n * EPS * scale
     assert torch.linalg.norm(back - C).item() <= 100 * n * EPS * scale
+
+
+@pytest.mark.parametrize("n", [64, 40, 128, 100])
+def test_dmma_tree_apply_matches_ring(n):
+    """CAQR_TUNE_DMMA_TREE = 1 (default): the tree-level Q / Q^T (STACKED node factors,
+    k_tree_apply_dmma, both directions, zero partner blocks for explicit Q / thin Q C) equals
+    the reflector-by-reflector k_tree_apply (= 0)."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, explicit_q_device, factor_device
+
+    m, P, k = 8 * 700 + 5, 8, 90
+    A = torch.from_numpy(philox(11 * n).standard_normal((m, n))).cuda()
+    Cf = torch.from_numpy(philox(12 * n).standard_normal((m, k))).cuda()
+    Ct = torch.from_numpy(philox(13 * n).standard_normal((n, k))).cuda()
+    f = factor_device(A, P, want_q=True)
+    out = []
+    try:
+        for tv in (1, 0):
+            _lib.tune(_lib.TUNE_DMMA_TREE, tv)
+            out.append((explicit_q_device(f), apply_q_device(f, Ct, transpose=False),
+                        apply_q_device(f, Cf, transpose=False), apply_q_device(f, Cf, transpose=True)))
+    finally:
+        _lib.reset_tuning()
+    for d, r, C in zip(out[0], out[1], (None, Ct, Cf, Cf)):
+        scale = 1.0 if C is None else torch.linalg.norm(C).item()
+        assert torch.linalg.norm(d - r).item() <= 100 * n * EPS * max(scale, np.sqrt(n))

@@ -11,7 +11,7 @@ from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
 
 m, n, P = 1048576, 64, 256
 A = torch.randn(m, n, dtype=torch.float64, device="cuda")
-settings = [(2, 16, 1), (2, 16, 2), (2, 16, 3)]
+settings = [(2, 16, 1, 1), (2, 16, 1, 0)]
 res = {s: [] for s in settings}
 
 
@@ -25,6 +25,7 @@ for rnd in range(5):
         _lib.tune(_lib.TUNE_DMMA, s[0])
         _lib.tune(_lib.TUNE_CHAIN_HT[64], s[1])
         _lib.tune(_lib.TUNE_DMMA_Q, s[2])
+        _lib.tune(_lib.TUNE_DMMA_TREE, s[3])
         for _ in range(3):
             step()
         torch.cuda.synchronize()
@@ -37,7 +38,5 @@ for rnd in range(5):
         res[s].append(e0.elapsed_time(e1) / 10)
 for s in settings:
     v = sorted(res[s])
-    print(f"dmma={s[0]} ht64={s[1]} dmma_q={s[2]}: median {v[len(v) // 2]:.3f} ms  min {v[0]:.3f}")
-_lib.tune(_lib.TUNE_DMMA, 1)
-_lib.tune(_lib.TUNE_CHAIN_HT[64], 24)
-_lib.tune(_lib.TUNE_DMMA_Q, 1)
+    print(f"dmma={s[0]} ht64={s[1]} dmma_q={s[2]} dmma_tree={s[3]}: median {v[len(v) // 2]:.3f} ms  min {v[0]:.3f}")
+_lib.reset_tuning()
