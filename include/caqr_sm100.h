@@ -156,17 +156,18 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 #define CAQR_TUNE_DMMA 9
 /* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with 16-row chain tiles (the CAQR
  * trailing update) runs on the DMMA ring (compact-WY per 8-reflector panel on the FP64 tensor
- * cores): n in (64, 128] on k_leaf_apply_dmma, n in (32, 64] on k_leaf_q_dmma (64-column CTAs,
- * two per SM; 2 = 32-column CTAs, 3 = one CTA per SM); 0 = the reflector-by-reflector warp
- * ring. */
+ * cores): n in (64, 128] on k_leaf_apply_dmma, n <= 64 on k_leaf_q_dmma (for n in (32, 64]:
+ * 64-column CTAs, two per SM; 2 = 32-column CTAs, 3 = one CTA per SM); 0 = the
+ * reflector-by-reflector warp ring. */
 #define CAQR_TUNE_DMMA_APPLY 10
 /* CAQR_TUNE_DMMA_Q: 1 (default) = Q C (explicit Q, apply_q) for leaves with 16-row chain tiles
- * and n in (32, 128] runs the DMMA ring backward (compact WY per 8-reflector panel, panels in
- * reverse order); 0 = the reflector-by-reflector warp ring. */
+ * and n <= 128 runs the DMMA ring backward (compact WY per 8-reflector panel, panels in reverse
+ * order); for n in (32, 64]: 2 = 32-column CTAs, 3 = one CTA per SM; 0 = the
+ * reflector-by-reflector warp ring. */
 #define CAQR_TUNE_DMMA_Q 11
-/* CAQR_TUNE_DMMA_TREE: 1 (default) = Q C / Q^T C of the tree nodes (STACKED factors) for
- * n in (32, 128] runs k_tree_apply_dmma (compact WY per 8 reflectors, two CTA barriers per panel);
- * 0 = the reflector-by-reflector k_tree_apply. */
+/* CAQR_TUNE_DMMA_TREE: 1 (default) = Q C / Q^T C of the tree nodes (STACKED factors) runs
+ * k_tree_apply_dmma (compact WY per 8 reflectors, two CTA barriers per panel); 0 = the
+ * reflector-by-reflector k_tree_apply / k_tree_apply_w32. */
 #define CAQR_TUNE_DMMA_TREE 12
 int caqr_tune(int key, int value);
 

@@ -100,6 +100,11 @@ def load():
     if lib.caqr_sm100_abi_version() != ABI_VERSION:
         raise NativeLibraryError("ABI version mismatch; rebuild the library")
     _lib = lib
+    # CAQR_TUNE="key=value,..." (caqr_tune keys, e.g. "12=0"): A/B runs of unmodified scripts
+    for item in filter(None, os.environ.get("CAQR_TUNE", "").split(",")):
+        k, v = item.split("=")
+        check(lib.caqr_tune(int(k), int(v)), "CAQR_TUNE")
+        TUNE_DEFAULTS[int(k)] = int(v)
     return lib
 
 

@@ -52,8 +52,8 @@ static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R o
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
-static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves on the DMMA ring
-static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of n in (32,128] tree nodes on DMMA
+static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
+static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
@@ -1311,17 +1311,7 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
     }                                                                                           \
     break;                                                                                      \
   }
-  if (p == 32) {
-    dim3 g32((unsigned)((nev + 3) / 4), (unsigned)((ncols + 31) / 32));
-    if (transpose)
-      k_tree_apply_w32<true><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
-                                                  slot_rows, ncols, zero_partner);
-    else
-      k_tree_apply_w32<false><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
-                                                   slot_rows, ncols, zero_partner);
-    return check_launch("k_tree_apply_w32");
-  }
-  if ((p == 128 || p == 64) && g_dmma_tree) {
+  if (g_dmma_tree) {
     const size_t sm = TreeApplyDmmaSmem::bytes;
     dim3 gd((unsigned)nev, (unsigned)((ncols + TA_KB - 1) / TA_KB));
 #define TAD_LAUNCH(TR)                                                                             \
@@ -1334,6 +1324,16 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
     if (transpose) TAD_LAUNCH(true) else TAD_LAUNCH(false)
 #undef TAD_LAUNCH
     return check_launch("k_tree_apply_dmma");
+  }
+  if (p == 32) {
+    dim3 g32((unsigned)((nev + 3) / 4), (unsigned)((ncols + 31) / 32));
+    if (transpose)
+      k_tree_apply_w32<true><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+                                                  slot_rows, ncols, zero_partner);
+    else
+      k_tree_apply_w32<false><<<g32, 128, 0, st>>>(Ynode, taunode, (int)n, events, (int)nev, C, ldc,
+                                                   slot_rows, ncols, zero_partner);
+    return check_launch("k_tree_apply_w32");
   }
   switch (p) { TA_CASE(32) TA_CASE(64) TA_CASE(128) }
 #undef TA_CASE
@@ -1371,8 +1371,10 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
-  const bool q16 = (p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16);
-  if ((!transpose && g_dmma_q && q16) || (transpose && p == 64 && g_dmma_apply && q16)) {
+  const int var = transpose ? g_dmma_apply : g_dmma_q;
+  const bool q16 = (p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16) ||
+                   (p == 32 && g_ht[0] == 16);
+  if ((!transpose && g_dmma_q && q16) || (transpose && p <= 64 && g_dmma_apply && q16)) {
 #define LQ_LAUNCH(NPV, KBQ, MB, TR)                                                               \
     {                                                                                             \
       const size_t sm = DmmaQSmem<NPV, KBQ>::bytes;                                               \
@@ -1381,8 +1383,9 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
       k_leaf_q_dmma<NPV, KBQ, MB, TR><<<gq, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,         \
           (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init);                   \
     }
-    const int var = transpose ? g_dmma_apply : g_dmma_q;
-    if (transpose) {
+    if (p == 32) {
+      if (transpose) LQ_LAUNCH(32, 32, 2, true) else LQ_LAUNCH(32, 32, 2, false)
+    } else if (transpose) {
       if (var == 2) LQ_LAUNCH(64, 32, 2, true)
       else if (var == 3) LQ_LAUNCH(64, 64, 1, true)
       else LQ_LAUNCH(64, 64, 2, true)
@@ -1506,16 +1509,17 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_TREE) {
-    g_dmma_tree = value ? 1 : 0;
+    if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_TREE takes 0, 1 or 2");
+    g_dmma_tree = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_Q) {
-    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_Q takes 0 .. 3");
+    if (value < 0 || value > 4) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_Q takes 0 .. 4");
     g_dmma_q = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_APPLY) {
-    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_APPLY takes 0 .. 3");
+    if (value < 0 || value > 4) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA_APPLY takes 0 .. 4");
     g_dmma_apply = value;
     return CAQR_OK;
   }

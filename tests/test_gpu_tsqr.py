@@ -612,3 +612,32 @@ def test_dmma_tree_apply_matches_ring(n):
     for d, r, C in zip(out[0], out[1], (None, Ct, Cf, Cf)):
         scale = 1.0 if C is None else torch.linalg.norm(C).item()
         assert torch.linalg.norm(d - r).item() <= 100 * n * EPS * max(scale, np.sqrt(n))
+
+
+@pytest.mark.parametrize("n", [32, 20])
+def test_dmma_np32_variants_match_ring(n):
+    """The DMMA paths for n <= 32 (k_tree_apply_dmma and k_leaf_q_dmma<32>, defaults;
+    tuning values 2 / 4 / 4 select the same kernels) equal the reflector rings
+    (k_tree_apply_w32, k_leaf_apply; all three keys = 0) for explicit Q, thin and full Q C,
+    and Q^T C."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, explicit_q_device, factor_device
+
+    m, P, k = 4 * 1200 + 9, 4, 45
+    A = torch.from_numpy(philox(21 * n).standard_normal((m, n))).cuda()
+    Cf = torch.from_numpy(philox(22 * n).standard_normal((m, k))).cuda()
+    Ct = torch.from_numpy(philox(23 * n).standard_normal((n, k))).cuda()
+    f = factor_device(A, P, want_q=True)
+    out = []
+    try:
+        for tv in ((2, 4, 4), (0, 0, 0)):
+            _lib.tune(_lib.TUNE_DMMA_TREE, tv[0])
+            _lib.tune(_lib.TUNE_DMMA_Q, tv[1])
+            _lib.tune(_lib.TUNE_DMMA_APPLY, tv[2])
+            out.append((explicit_q_device(f), apply_q_device(f, Ct, transpose=False),
+                        apply_q_device(f, Cf, transpose=False), apply_q_device(f, Cf, transpose=True)))
+    finally:
+        _lib.reset_tuning()
+    for d, r, C in zip(out[0], out[1], (None, Ct, Cf, Cf)):
+        scale = 1.0 if C is None else torch.linalg.norm(C).item()
+        assert torch.linalg.norm(d - r).item() <= 100 * n * EPS * max(scale, np.sqrt(n))
