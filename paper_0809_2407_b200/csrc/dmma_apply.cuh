@@ -699,3 +699,195 @@ k_tree_apply_dmma(const double* __restrict__ Ynode, const double* __restrict__ t
     if (c < ncb) Cag[(int64_t)r * ldc + c] = Ca[r * TA_LDC + c];
   }
 }
+
+// ---------------------------------------------------------------------------
+// DMMA tree factor: the STACKED combine [R_a; R_b] -> R, node Y / tau
+// (qr_stacked_triangles, q = 2, householder.py:263-294) for n <= 64 with the
+// node factor kept (explicit / implicit Q).  One CTA per event; warp w owns
+// column block w (8 columns) of R_b in registers -- all NP rows as NG 16-row
+// groups in the DMMA accumulator layout of k_leaf_dmma -- and of the pivot
+// rows R_a (shared memory).  Panel p (8 reflectors) is factored Level-2 by the
+// warp that owns block p (dr_gen over NG groups), which publishes Y_p and T_p
+// (shared memory, version counter); every warp owning a later block then
+// applies the panel in compact WY on the tensor cores.  The owner of block p+1
+// factors panel p+1 as soon as its own block has panel p applied: the
+// critical path is one panel factor + one block update per 8 reflectors
+// instead of two CTA barriers per reflector (k_tree_factor).  R_b is treated
+// as a dense NP-row block: its zeros below the diagonal stay exactly zero.
+// ---------------------------------------------------------------------------
+template <int NP>
+struct TreeFactorDmmaSmem {
+  static constexpr int NCB = NP / 8, LDA = NP + 2, LDY = 9;
+  static constexpr size_t doubles =
+      (size_t)NP * LDA + (size_t)NCB * NP * LDY + NCB * 64 + NCB * 64 + NCB * 8;
+  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * NCB;
+};
+
+// dr_gen over NG 16-row groups (the pivot row x0 and the column sums are
+// shared by all groups).
+template <int I, int NG>
+__device__ __forceinline__ void tf_gen(double (&x)[NG][4], double rgi, double* Rrow, double* gs,
+                                       double* taus) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int src = 4 * I + q;
+  double xi[NG][4];
+#pragma unroll
+  for (int j = 0; j < NG; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xi[j][k] = __shfl_sync(FULL, x[j][k], src);
+  const double x0 = __shfl_sync(FULL, rgi, 4 * I);
+  double s = 0.0, s2 = 0.0, pd = 0.0, pd2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    s = fma(xi[j][0], xi[j][0], s);
+    s2 = fma(xi[j][2], xi[j][2], s2);
+    s = fma(xi[j][1], xi[j][1], s);
+    s2 = fma(xi[j][3], xi[j][3], s2);
+    pd = fma(xi[j][0], x[j][0], pd);
+    pd2 = fma(xi[j][2], x[j][2], pd2);
+    pd = fma(xi[j][1], x[j][1], pd);
+    pd2 = fma(xi[j][3], x[j][3], pd2);
+  }
+  s += s2;
+  pd += pd2;
+  s += __shfl_xor_sync(FULL, s, 1);
+  pd += __shfl_xor_sync(FULL, pd, 1);
+  s += __shfl_xor_sync(FULL, s, 2);
+  pd += __shfl_xor_sync(FULL, pd, 2);
+  double beta, tau, scale, invb;
+  house_fast(x0, s, beta, tau, scale, invb);
+  const double tw = fma(scale, pd, rgi);
+  const double wv = tau * tw;
+  const bool upd = g > I;
+  const double f = upd ? tw * invb : ((g == I) ? scale - 1.0 : 0.0);
+#pragma unroll
+  for (int j = 0; j < NG; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[j][k] = fma(f, xi[j][k], x[j][k]);
+  double* dst = upd ? Rrow + g : ((g == I) ? Rrow + I : gs + g * 8 + I);
+  *dst = upd ? rgi - wv : ((g == I) ? beta : scale * pd);
+  taus[I] = tau;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(THREADS, 1)
+k_tree_factor_dmma(double* Rslots, int n, const int* __restrict__ ev, double* Ynode,
+                   double* taunode) {
+  using SMT = TreeFactorDmmaSmem<NP>;
+  constexpr int NG = NP / 16, NCB = SMT::NCB, LDA = SMT::LDA, LDY = SMT::LDY;
+  extern __shared__ __align__(16) double sm[];
+  double* Ra = sm;                         // pivot rows, NP x LDA
+  double* Ys = Ra + NP * LDA;              // [panel][row NP][LDY]
+  double* tbs = Ys + NCB * NP * LDY;       // [panel][lane][2]
+  double* gss = tbs + NCB * 64;            // [panel][8 x 8]
+  double* tss = gss + NCB * 64;            // [panel][8]
+  int* ver = reinterpret_cast<int*>(tss + NCB * 8);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int a = ev[3 * blockIdx.x], b = ev[3 * blockIdx.x + 1], id = ev[3 * blockIdx.x + 2];
+  const double* Rag = Rslots + (int64_t)a * n * n;
+  const double* Rbg = Rslots + (int64_t)b * n * n;
+  for (int idx = threadIdx.x; idx < NP * NP; idx += THREADS) {
+    const int r = idx / NP, c = idx - r * NP;
+    Ra[r * LDA + c] = (r < n && c < n && c >= r) ? Rag[r * n + c] : 0.0;
+  }
+  if (threadIdx.x < NCB) ver[threadIdx.x] = 0;
+  double C[NG][2][2];  // block w of R_b: rows 16 j + 8 bb + 2 q + e, column 8 w + g
+#pragma unroll
+  for (int j = 0; j < NG; ++j)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 16 * j + 8 * bb + 2 * q + e, c = 8 * w + g;
+        C[j][bb][e] = (w < NCB && r < n && c < n && c >= r) ? Rbg[r * n + c] : 0.0;
+      }
+  __syncthreads();
+  const int npan = (n + 7) >> 3;
+  double* Yo = Ynode + (int64_t)id * n * n;
+  double* to = taunode + (int64_t)id * n;
+  const int pmax = (w < npan) ? w : -1;  // warps past the last panel own padding only
+  for (int p = 0; p <= pmax; ++p) {
+    const int pc = 8 * p;
+    if (p == w) {  // factor panel p (my block)
+      double* gs = gss + p * 64;
+      double* taus = tss + p * 8;
+      double rg[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rg[i] = Ra[(pc + i) * LDA + pc + g];
+      double x[NG][4];
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        x[j][0] = C[j][0][0]; x[j][1] = C[j][0][1]; x[j][2] = C[j][1][0]; x[j][3] = C[j][1][1];
+      }
+      double* Rrow = Ra + pc * LDA + pc;
+      tf_gen<0, NG>(x, rg[0], Rrow, gs, taus);
+      tf_gen<1, NG>(x, rg[1], Rrow + LDA, gs, taus);
+      tf_gen<2, NG>(x, rg[2], Rrow + 2 * LDA, gs, taus);
+      tf_gen<3, NG>(x, rg[3], Rrow + 3 * LDA, gs, taus);
+      tf_gen<4, NG>(x, rg[4], Rrow + 4 * LDA, gs, taus);
+      tf_gen<5, NG>(x, rg[5], Rrow + 5 * LDA, gs, taus);
+      tf_gen<6, NG>(x, rg[6], Rrow + 6 * LDA, gs, taus);
+      tf_gen<7, NG>(x, rg[7], Rrow + 7 * LDA, gs, taus);
+      double* ys = Ys + p * NP * LDY;
+#pragma unroll
+      for (int j = 0; j < NG; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = 16 * j + 8 * (k >> 1) + 2 * q + (k & 1);
+          ys[r * LDY + g] = x[j][k];
+          if (r < n && pc + g < n) Yo[(int64_t)r * n + pc + g] = x[j][k];
+        }
+      __syncwarp();
+      double tb0, tb1;
+      dr_form_t(gs, taus, tb0, tb1);
+      tbs[p * 64 + 2 * lane] = tb0;
+      tbs[p * 64 + 2 * lane + 1] = tb1;
+      if (lane < 8 && pc + lane < n) to[pc + lane] = taus[lane];
+      dr_signal(ver + p, 1, lane);
+    } else {  // apply panel p to my block (w > p)
+      dr_wait(ver + p, 1, lane);
+      const double* ys = Ys + p * NP * LDY;
+      double xv[NG][4], vb[NG][2][2];
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[j][k] = ys[(16 * j + 8 * (k >> 1) + 2 * q + (k & 1)) * LDY + g];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int s = 0; s < 2; ++s) vb[j][bb][s] = ys[(16 * j + 8 * bb + g) * LDY + 2 * q + s];
+      }
+      const double tb0 = tbs[p * 64 + 2 * lane], tb1 = tbs[p * 64 + 2 * lane + 1];
+      double* rp = Ra + (pc + 2 * q) * LDA + 8 * w + g;
+      const double ro0 = rp[0], ro1 = rp[LDA];
+      double w0 = ro0, w1 = ro1;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        dmma(w0, w1, C[j][0][0], xv[j][0]);
+        dmma(w0, w1, C[j][1][0], xv[j][2]);
+        dmma(w0, w1, C[j][0][1], xv[j][1]);
+        dmma(w0, w1, C[j][1][1], xv[j][3]);
+      }
+      double u0 = 0.0, u1 = 0.0;
+      dmma(u0, u1, w0, tb0);
+      dmma(u0, u1, w1, tb1);
+      rp[0] = ro0 - u0;
+      rp[LDA] = ro1 - u1;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        dmma(C[j][0][0], C[j][0][1], -u0, vb[j][0][0]);
+        dmma(C[j][1][0], C[j][1][1], -u0, vb[j][1][0]);
+        dmma(C[j][0][0], C[j][0][1], -u1, vb[j][0][1]);
+        dmma(C[j][1][0], C[j][1][1], -u1, vb[j][1][1]);
+      }
+    }
+  }
+  __syncthreads();
+  double* Ro = Rslots + (int64_t)a * n * n;
+  for (int idx = threadIdx.x; idx < n * n; idx += THREADS) {
+    const int r = idx / n, c = idx - r * n;
+    Ro[idx] = (c >= r) ? Ra[r * LDA + c] : 0.0;
+  }
+}

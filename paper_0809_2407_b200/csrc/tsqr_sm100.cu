@@ -53,6 +53,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
+static int g_dmma_tree_factor = 0;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA (opt-in)
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
@@ -1276,6 +1277,18 @@ int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events,
         events, Ynode, taunode, 0);                                                      \
     break;                                                                               \
   }
+  if (p <= 64 && g_dmma_tree_factor) {
+#define TFD_LAUNCH(NPV)                                                                  \
+    {                                                                                    \
+      int rc = prep(k_tree_factor_dmma<NPV>, TreeFactorDmmaSmem<NPV>::bytes);            \
+      if (rc) return rc;                                                                 \
+      k_tree_factor_dmma<NPV><<<(int)nev, THREADS, TreeFactorDmmaSmem<NPV>::bytes, st>>>( \
+          Rslots, (int)n, events, Ynode, taunode);                                       \
+    }
+    if (p == 32) TFD_LAUNCH(32) else TFD_LAUNCH(64)
+#undef TFD_LAUNCH
+    return check_launch("k_tree_factor_dmma");
+  }
   if (p == 32) {
     k_tree_factor_w32<<<(int)((nev + 3) / 4), 128, 0, st>>>(Rslots, (int)n, events, (int)nev, Ynode,
                                                            taunode, 0);
@@ -1506,6 +1519,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_BLOCKED) {
     g_blocked = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DMMA_TREE_FACTOR) {
+    g_dmma_tree_factor = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_TREE) {

@@ -11,7 +11,7 @@ from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
 
 m, n, P = 1048576, 64, 256
 A = torch.randn(m, n, dtype=torch.float64, device="cuda")
-settings = [(2, 16, 1, 1), (2, 16, 1, 0)]
+settings = [(2, 16, 1, 1, 1), (2, 16, 1, 1, 0)]
 res = {s: [] for s in settings}
 
 
@@ -26,6 +26,7 @@ for rnd in range(5):
         _lib.tune(_lib.TUNE_CHAIN_HT[64], s[1])
         _lib.tune(_lib.TUNE_DMMA_Q, s[2])
         _lib.tune(_lib.TUNE_DMMA_TREE, s[3])
+        _lib.tune(_lib.TUNE_DMMA_TREE_FACTOR, s[4])
         for _ in range(3):
             step()
         torch.cuda.synchronize()
@@ -38,5 +39,5 @@ for rnd in range(5):
         res[s].append(e0.elapsed_time(e1) / 10)
 for s in settings:
     v = sorted(res[s])
-    print(f"dmma={s[0]} ht64={s[1]} dmma_q={s[2]} dmma_tree={s[3]}: median {v[len(v) // 2]:.3f} ms  min {v[0]:.3f}")
+    print(f"dmma={s[0]} ht64={s[1]} dmma_q={s[2]} dmma_tree={s[3]} tree_factor={s[4]}: median {v[len(v) // 2]:.3f} ms  min {v[0]:.3f}")
 _lib.reset_tuning()
