@@ -15,8 +15,8 @@ for n in (8, 17, 32):
     A = np.random.Generator(np.random.Philox(31 * n)).standard_normal((m, n))
     At = torch.from_numpy(A).cuda()
     for tf in (1, 0):
-        for dq in (1, 0):
-            for tr in (1, 0):
+        for dq in (1,):
+            for tr in (1,):
                 _lib.tune(_lib.TUNE_DMMA_TREE_FACTOR, tf)
                 _lib.tune(_lib.TUNE_DMMA_Q, dq)
                 _lib.tune(_lib.TUNE_DMMA_TREE, tr)
