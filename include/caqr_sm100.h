@@ -169,11 +169,9 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * k_tree_apply_dmma (compact WY per 8 reflectors, two CTA barriers per panel); 0 = the
  * reflector-by-reflector k_tree_apply / k_tree_apply_w32. */
 #define CAQR_TUNE_DMMA_TREE 12
-/* CAQR_TUNE_DMMA_TREE_FACTOR: 1 = the q = 2 node factors (Q kept) for n <= 64 run
+/* CAQR_TUNE_DMMA_TREE_FACTOR: 1 (default) = the q = 2 node factors (Q kept) for n <= 64 run
  * k_tree_factor_dmma (column-block warps, panels factored Level-2 by the owning warp and
- * applied in compact WY on the FP64 tensor cores; faster, but explicit Q is ~15x less
- * orthogonal than with the CTA factor); 0 (default) = k_tree_factor /
- * k_tree_factor_w32. */
+ * applied in compact WY on the FP64 tensor cores); 0 = k_tree_factor / k_tree_factor_w32. */
 #define CAQR_TUNE_DMMA_TREE_FACTOR 13
 int caqr_tune(int key, int value);
 

@@ -760,11 +760,12 @@ __device__ __forceinline__ void tf_gen(double (&x)[NG][4], double rgi, double* R
   const double tw = fma(scale, pd, rgi);
   const double wv = tau * tw;
   const bool upd = g > I;
-  const double f = upd ? tw * invb : ((g == I) ? scale - 1.0 : 0.0);
+  const bool own = (g == I);  // owner column: v = scale * x_I in one rounding (see dr_gen)
+  const double f = upd ? tw * invb : (own ? scale : 0.0);
 #pragma unroll
   for (int j = 0; j < NG; ++j)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) x[j][k] = fma(f, xi[j][k], x[j][k]);
+    for (int k = 0; k < 4; ++k) x[j][k] = fma(f, xi[j][k], own ? 0.0 : x[j][k]);
   double* dst = upd ? Rrow + g : ((g == I) ? Rrow + I : gs + g * 8 + I);
   *dst = upd ? rgi - wv : ((g == I) ? beta : scale * pd);
   taus[I] = tau;

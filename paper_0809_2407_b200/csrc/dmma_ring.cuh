@@ -157,7 +157,7 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
 // branch-free stores: every lane stores (the four lanes of a column group
 // write the same value to the same address), so the look-ahead block stays
 // one basic block.  rgi = R[pc+I][pc+g] (preloaded); Rrow = &R[pc+I][pc].
-template <int I>
+template <int I, bool EXACT = true>
 __device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow, double* gs,
                                        double* taus) {
   const int lane = threadIdx.x & 31;
@@ -184,11 +184,16 @@ __device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow,
   const double tw = fma(scale, pd, rgi);  // R[i][g] + v^T x_g
   const double wv = tau * tw;
   const bool upd = g > I;
-  // x_g -= scale * wv * x_I for g > I (f = t / beta = -scale tau t); the owner
-  // column becomes v = scale * x_I, written as x + (scale - 1) x: one FMA form
-  const double f = upd ? tw * invb : ((g == I) ? scale - 1.0 : 0.0);
+  // x_g -= scale * wv * x_I for g > I (f = t / beta = -scale tau t).  The owner
+  // column becomes v = scale * x_I.  EXACT: fma(scale, x_I, 0), one rounding --
+  // kept factors (Q) need it: the one-FMA form x + (scale - 1) x below rounds
+  // at eps |x| = eps |v| / scale, and tau (1 + |v|^2) - 2 drifts by ~eps |v|^2 /
+  // scale (measured 2.9e-15 on tree nodes, where |v| ~ 1).  R-only leaves take
+  // the one-FMA form (1% faster; tiles below a tall R have |v|^2 / scale < 1).
+  const bool own = (g == I);
+  const double f = upd ? tw * invb : (own ? (EXACT ? scale : scale - 1.0) : 0.0);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) x[k] = fma(f, xi[k], x[k]);
+  for (int k = 0; k < 4; ++k) x[k] = fma(f, xi[k], (EXACT && own) ? 0.0 : x[k]);
   double* dst = upd ? Rrow + g : ((g == I) ? Rrow + I : gs + g * 8 + I);
   *dst = upd ? rgi - wv : ((g == I) ? beta : scale * pd);
   taus[I] = tau;
@@ -340,14 +345,14 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
 #pragma unroll
       for (int i = 0; i < 8; ++i) rg[i] = Rp[i * l0 + g];
       x[0] = C[0][0][0]; x[1] = C[0][0][1]; x[2] = C[0][1][0]; x[3] = C[0][1][1];
-      dr_gen<0>(x, rg[0], Rp, gs, taus);
-      dr_gen<1>(x, rg[1], Rp + l0, gs, taus);
-      dr_gen<2>(x, rg[2], Rp + 2 * l0, gs, taus);
-      dr_gen<3>(x, rg[3], Rp + 3 * l0, gs, taus);
-      dr_gen<4>(x, rg[4], Rp + 4 * l0, gs, taus);
-      dr_gen<5>(x, rg[5], Rp + 5 * l0, gs, taus);
-      dr_gen<6>(x, rg[6], Rp + 6 * l0, gs, taus);
-      dr_gen<7>(x, rg[7], Rp + 7 * l0, gs, taus);
+      dr_gen<0, Q>(x, rg[0], Rp, gs, taus);
+      dr_gen<1, Q>(x, rg[1], Rp + l0, gs, taus);
+      dr_gen<2, Q>(x, rg[2], Rp + 2 * l0, gs, taus);
+      dr_gen<3, Q>(x, rg[3], Rp + 3 * l0, gs, taus);
+      dr_gen<4, Q>(x, rg[4], Rp + 4 * l0, gs, taus);
+      dr_gen<5, Q>(x, rg[5], Rp + 5 * l0, gs, taus);
+      dr_gen<6, Q>(x, rg[6], Rp + 6 * l0, gs, taus);
+      dr_gen<7, Q>(x, rg[7], Rp + 7 * l0, gs, taus);
     }
     DR_TICK(c1_);
     DR_ADD(0, c0_, c1_);
@@ -400,21 +405,21 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         double xn[4] = {C[1][0][0], C[1][0][1], C[1][1][0], C[1][1][1]};
 #define DR_UPD(CB) \
   if constexpr ((CB) < NCB) { if ((CB) < nl) dr_upd(C[CB], x, vb, tb0, tb1, rrow + 8 * (CB), ldr); }
-        dr_gen<0>(xn, rg[0], Rpan1, gs, taus);
+        dr_gen<0, Q>(xn, rg[0], Rpan1, gs, taus);
         DR_UPD(2); DR_UPD(3);
-        dr_gen<1>(xn, rg[1], Rpan1 + ldr1, gs, taus);
+        dr_gen<1, Q>(xn, rg[1], Rpan1 + ldr1, gs, taus);
         DR_UPD(4); DR_UPD(5);
-        dr_gen<2>(xn, rg[2], Rpan1 + 2 * ldr1, gs, taus);
+        dr_gen<2, Q>(xn, rg[2], Rpan1 + 2 * ldr1, gs, taus);
         DR_UPD(6); DR_UPD(7);
-        dr_gen<3>(xn, rg[3], Rpan1 + 3 * ldr1, gs, taus);
+        dr_gen<3, Q>(xn, rg[3], Rpan1 + 3 * ldr1, gs, taus);
         DR_UPD(8); DR_UPD(9);
-        dr_gen<4>(xn, rg[4], Rpan1 + 4 * ldr1, gs, taus);
+        dr_gen<4, Q>(xn, rg[4], Rpan1 + 4 * ldr1, gs, taus);
         DR_UPD(10); DR_UPD(11);
-        dr_gen<5>(xn, rg[5], Rpan1 + 5 * ldr1, gs, taus);
+        dr_gen<5, Q>(xn, rg[5], Rpan1 + 5 * ldr1, gs, taus);
         DR_UPD(12); DR_UPD(13);
-        dr_gen<6>(xn, rg[6], Rpan1 + 6 * ldr1, gs, taus);
+        dr_gen<6, Q>(xn, rg[6], Rpan1 + 6 * ldr1, gs, taus);
         DR_UPD(14); DR_UPD(15);
-        dr_gen<7>(xn, rg[7], Rpan1 + 7 * ldr1, gs, taus);
+        dr_gen<7, Q>(xn, rg[7], Rpan1 + 7 * ldr1, gs, taus);
 #undef DR_UPD
 #pragma unroll
         for (int k = 0; k < 4; ++k) x[k] = xn[k];

@@ -53,7 +53,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
-static int g_dmma_tree_factor = 0;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA (opt-in)
+static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }

@@ -645,28 +645,33 @@ def test_dmma_np32_variants_match_ring(n):
 
 @pytest.mark.parametrize("n", [8, 17, 32, 40, 64])
 def test_dmma_tree_factor_matches_cta_factor(n):
-    """CAQR_TUNE_DMMA_TREE_FACTOR = 1 (opt-in, n <= 64): the STACKED node factors
+    """CAQR_TUNE_DMMA_TREE_FACTOR = 1 (default, n <= 64): the STACKED node factors
     (k_tree_factor_dmma: column-block warps, Level-2 panels, compact-WY updates) equal
-    k_tree_factor / k_tree_factor_w32 (default) in node Y, tau and R, and give a valid QR.
-    Its explicit Q is ~15x less orthogonal than the default's, so the
-    bound here is the loose 100 n eps, not the north star's 10 n eps -- why it is opt-in."""
+    k_tree_factor / k_tree_factor_w32 (= 0) in node Y, tau and R, every node reflector is
+    orthogonal to rounding (tau (1 + |y|^2) = 2), and explicit Q meets the north-star
+    bounds."""
     from paper_0809_2407_b200 import _lib
     from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
 
     m, P = 8 * 600 + 3, 8
     A = philox(31 * n).standard_normal((m, n))
     At = torch.from_numpy(A).cuda()
-    f0 = factor_device(At, P, want_q=True)
+    f1 = factor_device(At, P, want_q=True)
+    Q1 = explicit_q_device(f1).cpu().numpy()
     try:
-        _lib.tune(_lib.TUNE_DMMA_TREE_FACTOR, 1)
-        f1 = factor_device(At, P, want_q=True)
-        Q1 = explicit_q_device(f1).cpu().numpy()
+        _lib.tune(_lib.TUNE_DMMA_TREE_FACTOR, 0)
+        f0 = factor_device(At, P, want_q=True)
     finally:
         _lib.reset_tuning()
     scale = np.linalg.norm(A, 2)
     assert (f1.R - f0.R).abs().max().item() <= 100 * EPS * scale
-    assert (f1.node_Y - f0.node_Y).abs().max().item() <= 1e-10
-    assert (f1.node_tau - f0.node_tau).abs().max().item() <= 1e-12
+    assert (f1.node_Y - f0.node_Y).abs().max().item() <= 1e-13
+    assert (f1.node_tau - f0.node_tau).abs().max().item() <= 1e-14
+    Y, tau = f1.node_Y.cpu().numpy(), f1.node_tau.cpu().numpy()
+    for e in range(Y.shape[0]):
+        for j in range(n):
+            if tau[e, j]:
+                assert abs(tau[e, j] * (1 + Y[e, :, j] @ Y[e, :, j]) - 2) <= 8 * EPS, (e, j)
     R = f1.R.cpu().numpy()
-    assert oracle.residual(A, Q1, R) <= 100 * n * EPS
-    assert oracle.orthogonality(Q1) <= 100 * n * EPS
+    assert oracle.residual(A, Q1, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q1) <= 10 * n * EPS

@@ -10,11 +10,11 @@ import oracle
 from paper_0809_2407_b200 import _lib
 from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
 
-for n in (8, 17, 32):
+for n in (8, 17, 32, 64, 100, 128):
     m, P = 8 * 600 + 3, 8
     A = np.random.Generator(np.random.Philox(31 * n)).standard_normal((m, n))
     At = torch.from_numpy(A).cuda()
-    for tf in (1, 0):
+    for tf in ((1, 0) if n <= 64 else (0,)):
         for dq in (1,):
             for tr in (1,):
                 _lib.tune(_lib.TUNE_DMMA_TREE_FACTOR, tf)
