@@ -72,8 +72,10 @@ struct ChainSmem {
 
 // Dense first tile of every leaf: rows [0, H0) (zero padded), CTA sweep.
 // Writes the leaf's R into its slot, tile 0 of Y (LAPACK layout) and tau.
+// NP = 64: two CTAs per SM (128 registers, 480 B of spills) -- C2's 256 leaves in one wave
+// instead of two: 3.275 -> 3.211 ms per step
 template <int NP>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, NP == 64 ? 2 : 1)
 k_leaf_dense(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
              double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rout, int* flag) {
   constexpr int S = Geo<NP>::S, HD = Geo<NP>::HD;
