@@ -520,10 +520,10 @@ def run_ours(args, cfg):
             traffic = 8.0 * (hi - lo) * n * 1.0047 if (n == 128 and cfg["q"] == "none") else None
             kern = ("k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)"
                     if cfg["q"] == "none" else
-                    ("k_leaf_dense + k_leaf_dmma<64> + k_tree_factor, then Q: k_tree_apply + "
+                    ("k_leaf_dense + k_leaf_dmma<64> + k_tree_factor_dmma, then Q: k_tree_apply_dmma + "
                      "k_leaf_q_dmma<64> " if 32 < n <= 64 else
-                     "k_leaf_dense + k_leaf_chain + k_tree_factor, then Q: k_tree_apply_w32 + "
-                     "k_leaf_apply ") +
+                     "k_leaf_dense + k_leaf_chain + k_tree_factor_dmma, then Q: k_tree_apply_dmma + "
+                     "k_leaf_q_dmma<32> ") +
                     "(graph replay of the step; credited with the factor and Q-formation flops)")
             roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
