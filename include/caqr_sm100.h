@@ -151,8 +151,8 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 /* CAQR_TUNE_DMMA: 1 (default) = leaves with n in (64, 128] run the DMMA warp ring
  * (16-row tiles per warp in registers, 8-column Level-2 panels with look-ahead,
  * compact-WY trailing updates on the FP64 tensor cores); 2 = also n in (32, 64] (the NP = 64
- * ring, two CTAs per SM; implicit-Q leaves need CAQR_TUNE_CHAIN_HT_64 = 16); 0 = the rank-1
- * warp ring. */
+ * ring, two CTAs per SM; implicit-Q leaves need CAQR_TUNE_CHAIN_HT_64 = 16); 3 = also n <= 32
+ * (NP = 32 ring; no gain on C1); 0 = the rank-1 warp ring. */
 #define CAQR_TUNE_DMMA 9
 /* CAQR_TUNE_DMMA_APPLY: 1 (default) = Q^T C for leaves with 16-row chain tiles (the CAQR
  * trailing update) runs on the DMMA ring (compact-WY per 8-reflector panel on the FP64 tensor

@@ -1134,7 +1134,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   }
 #define DMMA_LAUNCH(NPX, V16, Q)                                                                 \
   {                                                                                             \
-    constexpr int NPD = NPX == 128 ? 128 : 64;                                                  \
+    constexpr int NPD = NPX == 128 ? 128 : (NPX == 64 ? 64 : 32);                              \
     rc = prep(k_leaf_dmma<NPD, V16, Q>, DmmaRingSmem<NPD>::bytes);                              \
     if (rc) return rc;                                                                          \
     k_leaf_dmma<NPD, V16, Q><<<grid, DR_WARPS * 32, DmmaRingSmem<NPD>::bytes, st>>>(A, lda, m,  \
@@ -1151,7 +1151,8 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
     if ((NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) ||                                    \
-        (NPV == 64 && g_dmma >= 2 && (zs || g_ht[1] == 16))) {                                  \
+        (NPV == 64 && g_dmma >= 2 && (zs || g_ht[1] == 16)) ||                                  \
+        (NPV == 32 && g_dmma >= 3 && (zs || g_ht[0] == 16))) {                                  \
       const int h0d = zs ? 0 : WARPS * Geo<NPV>::HD;                                            \
       const bool v16 = (n % 2 == 0) && (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);            \
       if (v16 && Y) DMMA_LAUNCH(NPV, true, true)                                                     \
@@ -1543,7 +1544,7 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA) {
-    if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0, 1 or 2");
+    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0 .. 3");
     g_dmma = value;
     return CAQR_OK;
   }

@@ -675,3 +675,38 @@ def test_dmma_tree_factor_matches_cta_factor(n):
     R = f1.R.cpu().numpy()
     assert oracle.residual(A, Q1, R) <= 10 * n * EPS
     assert oracle.orthogonality(Q1) <= 10 * n * EPS
+
+
+@pytest.mark.parametrize("m,n,P", [(1500, 32, 2), (4096, 20, 5), (999, 9, 3)])
+def test_dmma_ring_np32_matches_oracle(m, n, P):
+    """CAQR_TUNE_DMMA = 3 (opt-in): leaves with n <= 32 on the NP = 32 DMMA ring; chain-tile
+    factors (Y, tau) against the oracle's hybrid chain, explicit Q against the oracle's Q, and
+    R-only (zero-start) leaves against LAPACK."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import explicit_q_device
+
+    A = philox(9 * m + n).standard_normal((m, n))
+    try:
+        _lib.tune(_lib.TUNE_DMMA, 3)
+        _, h0, ht = geom(n)
+        f = factor(A, P)
+        Q = explicit_q_device(f).cpu().numpy()
+        _lib.tune(_lib.TUNE_NARROW, 0)  # n = 9 would take the lane-private kernel otherwise
+        Rz = factor(A, P, want_q=False).R.cpu().numpy()
+    finally:
+        _lib.reset_tuning()
+    ref = oracle.tsqr_hybrid(A, P, h0, ht)
+    scale = np.linalg.norm(A, 2)
+    R = f.R.cpu().numpy()
+    assert np.max(np.abs(R - ref["R"])) <= 200 * EPS * scale
+    Y, tau, offs = f.Y.cpu().numpy(), f.tau.cpu().numpy(), ref["offs"]
+    for i, tiles in enumerate(ref["leaves"]):
+        bnds = oracle.tsqr.chain_tiles(offs[i + 1] - offs[i], h0, ht)
+        for k, ((V, t), (s, e)) in enumerate(zip(tiles[1:], bnds[1:]), start=1):
+            Vg = Y[offs[i] + s: offs[i] + e]
+            assert np.max(np.abs(Vg - V)) <= 1e-9 * max(1.0, np.max(np.abs(V))), (i, k)
+            assert np.max(np.abs(tau[i, k] - t)) <= 1e-12, (i, k)
+    assert np.max(np.abs(Q - oracle.tsqr_hybrid_q(ref))) <= 1e-11
+    assert oracle.residual(A, Q, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q) <= 10 * n * EPS
+    assert oracle.r_diff(Rz, np.linalg.qr(A, mode="r"), scale) <= 1000 * EPS
