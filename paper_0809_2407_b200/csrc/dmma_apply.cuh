@@ -1,3 +1,7 @@
+// FP64-tensor-core (DMMA) apply and tree kernels: k_leaf_apply_dmma (below),
+// k_leaf_q_dmma (leaf Q / Q^T), k_tree_apply_dmma (node Q / Q^T) and
+// k_tree_factor_dmma (node factor, n <= 64).
+//
 // DMMA leaf apply: C[leaf rows] <- Q_leaf^T C for the chain leaves of n in
 // (64, 128] (Y / tau in the layout of k_leaf_chain<128, 16> / k_leaf_dmma) --
 // the CAQR trailing update, _apply_yt with transpose (householder.py:175-186,

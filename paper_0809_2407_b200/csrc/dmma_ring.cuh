@@ -1,4 +1,5 @@
-// DMMA warp-ring leaf (R only, 64 < n <= 128): the C3 hot kernel.
+// DMMA warp-ring leaf (NP = 128: 64 < n <= 128, the C3 hot kernel; NP = 64: 32 < n <= 64;
+// NP = 32 opt-in), R only or keeping the chain tiles' factors (Q).
 //
 // The flat chain of triangle-on-rectangle steps of a leaf (Alg. 2,
 // PAPER.md:840-866; one step = qr_triangle_on_rect, householder.py:297-332)

@@ -1,18 +1,25 @@
 // FP64 TSQR / CAQR kernels for B200 (sm_100a) and their C-ABI.
 //
-// Kernels (all FP64, see tsqr_device.cuh for the register layout):
-//   k_leaf_factor   : one CTA per leaf row-block: dense first tile (CTA sweep)
-//                     then the flat chain of triangle-on-rectangle tiles as a
-//                     warp ring.  Reads A once; writes R (and optionally the
-//                     implicit-Q storage Y, tau).            [SURVEY 8(a) a3,a10]
-//   k_tree_factor   : one CTA per combine event of one tree level: QR of two
-//                     stacked n x n triangles on the sparsity profile.  [a9]
-//   k_tree_apply    : Q or Q^T of a stacked node factor applied to the two
-//                     n-row blocks of C it acts on (tree walk / CAQR).  [a11,a12]
-//   k_leaf_apply    : Q or Q^T of a leaf chain applied to the leaf's rows of C
-//                     (explicit Q, implicit-Q apply, CAQR trailing update). [a6,a12]
-//   k_block_factor  : single-CTA DENSE / TRIRECT factorization of a small block
-//                     (kernel-level API mirrors of qr_unblocked, qr_triangle_on_rect).
+// Kernels (all FP64, see tsqr_device.cuh for the register layout).  Defaults
+// for n > 32 run on the FP64 tensor cores (mma.m8n8k4.f64, DMMA):
+//   k_leaf_dense    : dense first tile of a leaf that keeps Q (CTA sweep).    [a3]
+//   k_leaf_dmma     : (dmma_ring.cuh) the leaf's flat chain of
+//                     triangle-on-rectangle tiles as a DMMA warp ring, 8-column
+//                     Level-2 panels + compact-WY updates; NP = 128 / 64 (/ 32).
+//                     The C3 hot kernel.                                       [a10]
+//   k_leaf_chain    : the rank-1 warp ring (n <= 32, tuning fallback).        [a10]
+//   k_leaf_narrow   : n <= 8, R only: lane-private rows + fused ticket tree.  [C4]
+//   k_tree_ring     : R-only stacked combine as a warp ring.                  [a9]
+//   k_tree_factor_dmma / k_tree_factor / k_tree_factor_w32 : stacked combine
+//                     with node factors (dmma: n <= 64, column-block warps).  [a9]
+//   k_tree_apply_dmma / k_tree_apply / k_tree_apply_w32 : Q or Q^T of a stacked
+//                     node on the two n-row blocks of C it acts on.       [a11,a12]
+//   k_leaf_apply_dmma (Q^T, 64 < n <= 128), k_leaf_q_dmma (Q, n <= 128; Q^T,
+//                     n <= 64), k_leaf_apply (reflector ring): a leaf chain's
+//                     Q / Q^T on the leaf's rows of C (explicit Q, apply_q, the
+//                     CAQR trailing update).                                [a6,a12]
+//   k_block_factor / k_block_apply : single-CTA DENSE / TRIRECT factorization
+//                     and apply of a small block (kernel-level API mirrors).
 //   k_peak_probe    : DFMA / DMMA throughput microbenchmark.
 #include <cuda_runtime.h>
 #include <stdint.h>
