@@ -173,6 +173,11 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * k_tree_factor_dmma (column-block warps, panels factored Level-2 by the owning warp and
  * applied in compact WY on the FP64 tensor cores); 0 = k_tree_factor / k_tree_factor_w32. */
 #define CAQR_TUNE_DMMA_TREE_FACTOR 13
+/* CAQR_TUNE_DMMA_DENSE: 1 = the dense first tile of leaves that keep Q, n <= 64, runs
+ * k_leaf_dense_dmma (column-block warps, masked Level-2 panels, compact-WY updates on the FP64
+ * tensor cores; parity-tested but slower: one warp per panel serialises the tall tile);
+ * 0 (default) = the CTA sweep k_leaf_dense. */
+#define CAQR_TUNE_DMMA_DENSE 14
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

@@ -896,3 +896,187 @@ k_tree_factor_dmma(double* Rslots, int n, const int* __restrict__ ev, double* Yn
     Ro[idx] = (c >= r) ? Ra[r * LDA + c] : 0.0;
   }
 }
+
+// ---------------------------------------------------------------------------
+// DMMA dense first tile (n <= 64): the DENSE QR of a leaf's first H0 rows
+// (qr_unblocked, householder.py:128-145; LAPACK layout: R on and above the
+// diagonal, V below it) as column-block warps like k_tree_factor_dmma: warp w
+// holds column block w of the whole tile (NG = H0/16 row groups) in
+// registers; the owner of block p factors panel p Level-2 (dd_gen: the pivot
+// row is inside the column, so every sum is masked by row index), publishes V_p
+// (unit lower trapezoidal) and T_p, and the owners of later blocks apply
+// I - V T^T V^T on the tensor cores.  Replaces k_leaf_dense's two CTA barriers
+// per reflector with one panel factor + one block update per 8 reflectors.
+// ---------------------------------------------------------------------------
+template <int NP>
+struct DenseDmmaSmem {
+  static constexpr int NCB = NP / 8, H0 = WARPS * Geo<NP>::HD, LDY = 9;
+  static constexpr size_t doubles = (size_t)NCB * H0 * LDY + NCB * 64 + NCB * 64 + NCB * 8;
+  static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * NCB;
+};
+
+// Generation I of panel pc (pivot row jr = pc + I) over the NG groups of the
+// owner's registers x (lane (g, q): rows 16 J + 8 (k >> 1) + 2 q + (k & 1) of
+// column pc + g).  Column I's values are shuffled twice (sums, then update)
+// rather than held, to keep the register count down.
+template <int I, int NG>
+__device__ __forceinline__ void dd_gen(double (&x)[NG][4], int pc, double* gs, double* taus) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int src = 4 * I + q, jr = pc + I;
+  double s = 0.0, pd = 0.0, x0 = 0.0, xg0 = 0.0;
+#pragma unroll
+  for (int J = 0; J < NG; ++J)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = 16 * J + 8 * (k >> 1) + 2 * q + (k & 1);
+      const double v = __shfl_sync(FULL, x[J][k], src);
+      const double vb = r > jr ? v : 0.0;
+      s = fma(vb, vb, s);
+      pd = fma(vb, x[J][k], pd);
+      x0 += r == jr ? v : 0.0;
+      xg0 += r == jr ? x[J][k] : 0.0;
+    }
+  s += __shfl_xor_sync(FULL, s, 1);
+  pd += __shfl_xor_sync(FULL, pd, 1);
+  x0 += __shfl_xor_sync(FULL, x0, 1);
+  xg0 += __shfl_xor_sync(FULL, xg0, 1);
+  s += __shfl_xor_sync(FULL, s, 2);
+  pd += __shfl_xor_sync(FULL, pd, 2);
+  x0 += __shfl_xor_sync(FULL, x0, 2);
+  xg0 += __shfl_xor_sync(FULL, xg0, 2);
+  double beta, tau, scale;
+  house_scalars(x0, s, beta, tau, scale);
+  const double invb = (s == 0.0) ? 0.0 : __drcp_rn(beta);
+  const double tw = fma(scale, pd, xg0);  // w_g = x[jr][g] + v^T x_g (below jr)
+  const bool upd = g > I, own = g == I;
+  const double f = upd ? tw * invb : (own ? scale : 0.0);  // below jr
+  const double pn = upd ? fma(-tau, tw, xg0) : beta;        // row jr (g >= I)
+#pragma unroll
+  for (int J = 0; J < NG; ++J)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = 16 * J + 8 * (k >> 1) + 2 * q + (k & 1);
+      const double v = __shfl_sync(FULL, x[J][k], src);
+      const double nb = fma(f, v, own ? 0.0 : x[J][k]);
+      x[J][k] = r > jr ? nb : ((r == jr && g >= I) ? pn : x[J][k]);
+    }
+  if (g < I) gs[g * 8 + I] = tw;  // G[g][I] = v_g^T v_I
+  taus[I] = tau;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(THREADS, 1)
+k_leaf_dense_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
+                  double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rout, int* flag) {
+  using SMD = DenseDmmaSmem<NP>;
+  constexpr int NCB = SMD::NCB, H0 = SMD::H0, NG = H0 / 16, LDY = SMD::LDY;
+  extern __shared__ __align__(16) double sm[];
+  double* Ys = sm;                      // [panel][row H0][LDY]: V_p, unit lower trapezoidal
+  double* tbs = Ys + NCB * H0 * LDY;    // [panel][lane][2]
+  double* gss = tbs + NCB * 64;         // [panel][8 x 8]
+  double* tss = gss + NCB * 64;         // [panel][8]
+  int* ver = reinterpret_cast<int*>(tss + NCB * 8);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int leaf = blockIdx.x;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const int rows = (int)min64(H0, b);
+  double* tl = tau ? tau + (int64_t)leaf * tau_stride : nullptr;
+  if (threadIdx.x < NCB) ver[threadIdx.x] = 0;
+  bool bad = false;
+  double C[NG][4];  // block w: rows 16 J + 8 (k >> 1) + 2 q + (k & 1), column 8 w + g
+  const int c = 8 * w + g;
+#pragma unroll
+  for (int J = 0; J < NG; ++J)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = 16 * J + 8 * (k >> 1) + 2 * q + (k & 1);
+      double v = 0.0;
+      if (w < NCB && r < rows && c < n) v = A[(r0 + r) * lda + c];
+      bad |= !isfinite(v);
+      C[J][k] = v;
+    }
+  __syncthreads();
+  const int npan = (n + 7) >> 3;
+  const int pmax = (w < npan) ? w : -1;
+  for (int p = 0; p <= pmax; ++p) {
+    const int pc = 8 * p;
+    if (p == w) {  // factor panel p (my block)
+      double* gs = gss + p * 64;
+      double* taus = tss + p * 8;
+      dd_gen<0, NG>(C, pc, gs, taus);
+      dd_gen<1, NG>(C, pc, gs, taus);
+      dd_gen<2, NG>(C, pc, gs, taus);
+      dd_gen<3, NG>(C, pc, gs, taus);
+      dd_gen<4, NG>(C, pc, gs, taus);
+      dd_gen<5, NG>(C, pc, gs, taus);
+      dd_gen<6, NG>(C, pc, gs, taus);
+      dd_gen<7, NG>(C, pc, gs, taus);
+      double* ys = Ys + p * H0 * LDY;
+#pragma unroll
+      for (int J = 0; J < NG; ++J)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = 16 * J + 8 * (k >> 1) + 2 * q + (k & 1);
+          ys[r * LDY + g] = r > pc + g ? C[J][k] : (r == pc + g ? 1.0 : 0.0);
+        }
+      __syncwarp();
+      double tb0, tb1;
+      dr_form_t(gs, taus, tb0, tb1);
+      tbs[p * 64 + 2 * lane] = tb0;
+      tbs[p * 64 + 2 * lane + 1] = tb1;
+      if (tl && lane < 8 && pc + lane < n) tl[pc + lane] = taus[lane];
+      dr_signal(ver + p, 1, lane);
+    } else {  // apply panel p to my block: C -= V (T^T (V^T C))
+      dr_wait(ver + p, 1, lane);
+      const double* ys = Ys + p * H0 * LDY;
+      const double tb0 = tbs[p * 64 + 2 * lane], tb1 = tbs[p * 64 + 2 * lane + 1];
+      const int J0 = pc >> 4;  // V_p is zero above row pc
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int J = 0; J < NG; ++J) {
+        if (J < J0) continue;
+        double xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[k] = ys[(16 * J + 8 * (k >> 1) + 2 * q + (k & 1)) * LDY + g];
+        dmma(w0, w1, C[J][0], xv[0]);
+        dmma(w0, w1, C[J][2], xv[2]);
+        dmma(w0, w1, C[J][1], xv[1]);
+        dmma(w0, w1, C[J][3], xv[3]);
+      }
+      double u0 = 0.0, u1 = 0.0;
+      dmma(u0, u1, w0, tb0);
+      dmma(u0, u1, w1, tb1);
+#pragma unroll
+      for (int J = 0; J < NG; ++J) {
+        if (J < J0) continue;
+        double vb[2][2];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) vb[bb][s2] = ys[(16 * J + 8 * bb + g) * LDY + 2 * q + s2];
+        dmma(C[J][0], C[J][1], -u0, vb[0][0]);
+        dmma(C[J][2], C[J][3], -u0, vb[1][0]);
+        dmma(C[J][0], C[J][1], -u1, vb[0][1]);
+        dmma(C[J][2], C[J][3], -u1, vb[1][1]);
+      }
+    }
+  }
+  // the tile (R on / above the diagonal, V below) to Y; R to the leaf's slot
+  double* Ro = Rout + (int64_t)leaf * n * n;
+  if (w < npan) {
+#pragma unroll
+    for (int J = 0; J < NG; ++J)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = 16 * J + 8 * (k >> 1) + 2 * q + (k & 1);
+        if (c < n) {
+          if (Y && r < rows) Y[(r0 + r) * ldy + c] = C[J][k];
+          if (r < n) Ro[r * n + c] = (c >= r) ? C[J][k] : 0.0;
+        }
+      }
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}

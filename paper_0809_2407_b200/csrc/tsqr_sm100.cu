@@ -60,6 +60,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
+static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles on DMMA (opt-in, slower)
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
@@ -1151,7 +1152,13 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   case NPV: {                                                                                   \
     const bool zs = !Y && g_zstart;                                                             \
     int rc = 0;                                                                                 \
-    if (!zs) {                                                                                  \
+    if (!zs && NPV <= 64 && g_dmma_dense) {                                                     \
+      constexpr int NPQ = NPV <= 32 ? 32 : 64;                                                  \
+      rc = prep(k_leaf_dense_dmma<NPQ>, DenseDmmaSmem<NPQ>::bytes);                             \
+      if (rc) return rc;                                                                        \
+      k_leaf_dense_dmma<NPQ><<<grid, THREADS, DenseDmmaSmem<NPQ>::bytes, st>>>(A, lda, m,       \
+          (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag);                              \
+    } else if (!zs) {                                                                           \
       rc = prep(k_leaf_dense<NPV>, DenseSmem<NPV>::bytes);                                      \
       if (rc) return rc;                                                                        \
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
@@ -1529,6 +1536,10 @@ int caqr_tune(int key, int value) {
   }
   if (key == CAQR_TUNE_BLOCKED) {
     g_blocked = value ? 1 : 0;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_DMMA_DENSE) {
+    g_dmma_dense = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_TREE_FACTOR) {

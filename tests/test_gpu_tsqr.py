@@ -710,3 +710,29 @@ def test_dmma_ring_np32_matches_oracle(m, n, P):
     assert oracle.residual(A, Q, R) <= 10 * n * EPS
     assert oracle.orthogonality(Q) <= 10 * n * EPS
     assert oracle.r_diff(Rz, np.linalg.qr(A, mode="r"), scale) <= 1000 * EPS
+
+
+@pytest.mark.parametrize("m,n,P", [(300, 32, 2), (5000, 20, 3), (2000, 64, 4), (129, 64, 1),
+                                   (4100, 8, 2)])
+def test_dmma_dense_tile_matches_cta_sweep(m, n, P):
+    """CAQR_TUNE_DMMA_DENSE = 1 (opt-in, n <= 64): the dense first tile on
+    k_leaf_dense_dmma equals the CTA sweep k_leaf_dense (default) in Y (LAPACK layout), tau
+    and R, including leaves shorter than the tile; explicit Q meets the north-star bounds."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import explicit_q_device
+
+    A = philox(13 * m + n).standard_normal((m, n))
+    f0 = factor(A, P)
+    try:
+        _lib.tune(_lib.TUNE_DMMA_DENSE, 1)
+        f1 = factor(A, P)
+        Q1 = explicit_q_device(f1).cpu().numpy()
+    finally:
+        _lib.reset_tuning()
+    scale = np.linalg.norm(A, 2)
+    assert (f1.R - f0.R).abs().max().item() <= 100 * EPS * scale
+    assert (f1.Y - f0.Y).abs().max().item() <= 1e-12 * max(1.0, f0.Y.abs().max().item())
+    assert (f1.tau - f0.tau).abs().max().item() <= 1e-13
+    R = f1.R.cpu().numpy()
+    assert oracle.residual(A, Q1, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q1) <= 10 * n * EPS
