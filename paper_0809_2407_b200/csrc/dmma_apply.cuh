@@ -315,7 +315,6 @@ struct DmmaQSmem {
   static constexpr int SCR = WARPS * 8 * KB + WARPS * 64 + 8 * KB;  // dense phase: W, G, W'
   static constexpr size_t doubles = (size_t)NP * LDC + SCR;
   static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * (NP / 8);
-  static constexpr int MINB = NP == 128 ? 1 : 2;
 };
 
 template <int NP, int KB, int MB, bool TR>
