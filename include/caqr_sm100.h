@@ -178,6 +178,9 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * tensor cores; parity-tested but slower: one warp per panel serialises the tall tile);
  * 0 (default) = the CTA sweep k_leaf_dense. */
 #define CAQR_TUNE_DMMA_DENSE 14
+/* CAQR_TUNE_CC: 0 (default) = R-only leaves with n in (64, 128] run the DMMA warp ring;
+ * 2 = the split-role ring (generation warps + update warps, tiles in shared memory). */
+#define CAQR_TUNE_CC 15
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

@@ -18,7 +18,7 @@ from .core import (  # noqa: F401
     partition_block_rows,
     rng_for,
 )
-from .executor import DeviceExecutor, ExecutorError, LocalExecutor  # noqa: F401
+from .executor import DeviceExecutor, ExecutorError, LocalExecutor, Message, payload_words  # noqa: F401
 from .trees import ReductionTree, TreeError, parse_tree  # noqa: F401
 
 __version__ = "0.1.0"

@@ -240,10 +240,15 @@ def _caqr_on_grid(A, layout: BlockCyclicLayout, leaf_rows: int, device):
     At, host = to_device(A, device)
     if (layout.m, layout.n) != tuple(At.shape):
         raise DimensionError("layout does not match A")
+    # the grid's row / column groups belong to the default group they were made
+    # in: after destroy / re-init the cached groups are dead, so the cache entry
+    # keeps that group and is rebuilt when it is no longer the current one
     key = (layout.m, layout.n, layout.b, layout.Pr, layout.Pc)
-    grid = _GRIDS.get(key)
-    if grid is None:  # every rank reaches this call in the same order (collective)
-        grid = _GRIDS[key] = make_grid(layout)
+    world = dist.group.WORLD
+    grid, made_in = _GRIDS.get(key, (None, None))
+    if grid is None or made_in is not world:  # every rank reaches this in the same order
+        grid = make_grid(layout)
+        _GRIDS[key] = (grid, world)
     res = caqr_grid(scatter_local(At, grid), grid, GpuBackend(leaf_rows=leaf_rows))
     R = grid_gather_R(res)
     res.R = None if R is None else _out(R, host)

@@ -64,6 +64,7 @@ static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
+static int g_cc = 0;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 2 split-role ring, 0 DMMA ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -246,7 +247,7 @@ __device__ __forceinline__ void narrow_load(double (&Bt)[K][8], const double* __
     const int64_t row = q * 32 * K + (int64_t)k * 32 + lane;  // rows interleaved over lanes
     const bool ok = row < b;
     const double* src = A + (r0 + row) * lda;
-    if (ok && n == 8 && lda == 8) {
+    if (ok && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // 16-byte granules only when aligned
       const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -1037,6 +1038,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 
 #include "dmma_ring.cuh"
 #include "dmma_apply.cuh"
+#include "split_leaf.cuh"
 
 // ===========================================================================
 // C-ABI
@@ -1107,7 +1109,7 @@ static int launch_narrow(const double* A, int64_t lda, int64_t m, int64_t n, int
     k_leaf_narrow<true, KK, NP_::W><<<(int)((P + NP_::W - 1) / NP_::W), NP_::W * 32, NP_::SMEM, \
                                       st>>>(A, lda, m, (int)n, (int)P, base, R, flag, tickets); \
   }
-  if (g_narrow >= 2 && n == 8 && lda == 8) {
+  if (g_narrow >= 2 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // cp.async 16 B granules
     NARROW_PIPE(4)
   } else {
     k_leaf_narrow<false><<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
@@ -1115,6 +1117,17 @@ static int launch_narrow(const double* A, int64_t lda, int64_t m, int64_t n, int
   }
 #undef NARROW_PIPE
   return check_launch("k_leaf_narrow");
+}
+
+// Smallest tau row stride of a leaf that keeps Q: the dense first tile (h0
+// rows) plus ceil((b - h0) / ht) chain tiles of n scalars each, b the tallest
+// (last) leaf.
+static int64_t min_tau_stride(int64_t m, int64_t n, int64_t P, int64_t base) {
+  int64_t np_ = 0, h0 = 0, ht = 0;
+  if (tsqr_f64_geometry(n, &np_, &h0, &ht) != CAQR_OK) return INT64_MAX;
+  const int64_t b = m - (P - 1) * base;
+  const int64_t tiles = 1 + (b > h0 ? (b - h0 + ht - 1) / ht : 0);
+  return tiles * n;
 }
 
 // Leaves of `base` rows, the last one taking the remainder (m - (P-1) base >= base).
@@ -1127,6 +1140,8 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
   if ((Y == nullptr) != (tau == nullptr)) return set_err(CAQR_ERR_ARG, "Y and tau go together");
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
   if (m - (P - 1) * base < base) return set_err(CAQR_ERR_ARG, "last leaf shorter than base");
+  if (tau && tau_stride < min_tau_stride(m, n, P, base))
+    return set_err(CAQR_ERR_ARG, "tau_stride below the leaf's tiles * n");
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)P;
   if (n <= 8 && !Y && g_narrow) {
@@ -1164,7 +1179,20 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if ((NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) ||                                    \
+    if (NPV == 128 && zs && g_cc == 2) {                                                        \
+      const bool v16 = (n % 2 == 0) && (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);            \
+      if (v16) {                                                                                \
+        rc = prep(k_leaf_split<true>, SpSmem::bytes);                                           \
+        if (rc) return rc;                                                                      \
+        k_leaf_split<true><<<grid, SP_THREADS, SpSmem::bytes, st>>>(A, lda, m, (int)n, (int)P,  \
+                                                                    base, R, flag);             \
+      } else {                                                                                  \
+        rc = prep(k_leaf_split<false>, SpSmem::bytes);                                          \
+        if (rc) return rc;                                                                      \
+        k_leaf_split<false><<<grid, SP_THREADS, SpSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, \
+                                                                     base, R, flag);            \
+      }                                                                                         \
+    } else if ((NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) ||                             \
         (NPV == 64 && g_dmma >= 2 && (zs || g_ht[1] == 16)) ||                                  \
         (NPV == 32 && g_dmma >= 3 && (zs || g_ht[0] == 16))) {                                  \
       const int h0d = zs ? 0 : WARPS * Geo<NPV>::HD;                                            \
@@ -1321,7 +1349,8 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
                               int64_t slot_rows, int64_t ncols, int transpose, int zero_partner,
                               void* stream) {
   const int p = padded(n);
-  if (!p || !Ynode || !taunode || !events || !C || ncols < 1 || ldc < ncols)
+  if (!p || !Ynode || !taunode || !events || !C || ncols < 1 || ldc < ncols || nev < 0 ||
+      slot_rows < n)
     return set_err(CAQR_ERR_ARG, "tsqr_f64_tree_apply_level: bad arguments");
   if (nev == 0) return CAQR_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1375,8 +1404,10 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
                         const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
                         int zero_init, int tri_skip, void* stream) {
   const int p = padded(n);
-  if (!p || !Y || !tau || !C || P < 1 || m < n * P || ncols < 1 || ldc < ncols)
+  if (!p || !Y || !tau || !C || P < 1 || m < n * P || ncols < 1 || ldc < ncols || ldy < n)
     return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_apply: bad arguments");
+  if (tau_stride < min_tau_stride(m, n, P, m / P))
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_apply: tau_stride below the leaf's tiles * n");
   if (transpose && (S || zero_init || tri_skip))
     return set_err(CAQR_ERR_ARG, "S / zero_init / tri_skip only apply to Q (not Q^T)");
   const int64_t base = m / P;
@@ -1564,6 +1595,11 @@ int caqr_tune(int key, int value) {
   if (key == CAQR_TUNE_DMMA) {
     if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0 .. 3");
     g_dmma = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_CC) {
+    if (value != 0 && value != 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_CC takes 0 or 2");
+    g_cc = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_ZSTART) {

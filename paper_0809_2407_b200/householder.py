@@ -222,10 +222,10 @@ def qr_stacked_triangles(Rs, counter: FlopCounter | None = None):
         raise DimensionError(f"GPU block kernel supports (q-1) n <= {BLOCK_ROWS}")
     Rtop = tris[0].clone()
     low = torch.cat(tris[1:], dim=0).contiguous()
-    Yl, tau = _block_factor(low, n, 3 if q > 2 else 3, Rtop)
+    Yl, tau = _block_factor(low, n, 3, Rtop)
     Y = torch.cat([torch.eye(n, dtype=torch.float64, device=Yl.device), Yl], dim=0)
     if counter is not None:
-        f_, d_ = count_stacked(n) if q == 2 else (0, 0)
+        f_, d_ = count_stacked(n, q)
         counter.add(f_, d_)
     f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), STACKED, q=q, impl=(Y, tau))
     return f, _out(Rtop, host)

@@ -267,3 +267,68 @@ def test_mat1_format_matches_the_reference_layout(tmp_path):
     np.savetxt(tmp_path / "nan.csv", B, delimiter=",")
     with pytest.raises(ValueError):
         read_matrix(tmp_path / "nan.csv")
+
+
+class _RingSum:
+    """SPMD program for LocalExecutor.run: each worker passes its value around
+    a ring for P-1 supersteps and sums what it receives."""
+
+    def __init__(self, P):
+        self.n_workers = P
+        self.n_steps = P
+
+    def setup(self, w):
+        return {"acc": float(w), "val": np.array([float(w)])}
+
+    def step(self, w, st, step, inbox):
+        from caqr.executor import Message
+
+        for msg in inbox:
+            st["acc"] += float(msg.payload[0])
+            st["val"] = msg.payload
+        if step == self.n_steps - 1:
+            return []
+        return [Message(w, (w + 1) % self.n_workers, "v", st["val"])]
+
+    def finish(self, w, st):
+        return st["acc"]
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_local_executor_runs_reference_programs(threads):
+    """caqr.executor keeps the reference API (executor.py:20-94): Message,
+    payload_words and LocalExecutor.run -> (results, recorders)."""
+    from caqr.executor import ExecutorError, LocalExecutor, Message, payload_words
+
+    assert payload_words(np.zeros((3, 4))) == 12
+    assert payload_words({"a": 1.0, "b": (np.zeros(2), None)}) == 3
+    assert Message(0, 1, "t", np.zeros(5)).words == 5
+    P = 5
+    res, recs = LocalExecutor(threads=threads).run(_RingSum(P))
+    assert res == [float(P * (P - 1) / 2)] * P
+    assert all(r.words_sent == P - 1 and r.words_received == P - 1 for r in recs)
+
+    class Bad(_RingSum):
+        def step(self, w, st, step, inbox):
+            return [Message((w + 1) % P, w, "x", None)]
+
+    with pytest.raises(ExecutorError):
+        LocalExecutor(threads=threads).run(Bad(P))
+    with pytest.raises(ValueError):
+        LocalExecutor(threads=0)
+
+
+def test_stacked_flop_count_qary():
+    """q-ary stacked profile: reflector j has length 1 + (q-1)(j+1); counts
+    equal the reference's own counter (tests/golden/flops_stacked.json,
+    oracle/make_golden_flops.py)."""
+    import json
+    import os
+
+    from paper_0809_2407_b200.counters import count_stacked
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "flops_stacked.json")) as fh:
+        gold = json.load(fh)
+    for key, (flops, divs) in gold.items():
+        n, q = map(int, key.split("x"))
+        assert count_stacked(n, q) == (flops, divs), key
