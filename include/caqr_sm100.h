@@ -30,6 +30,8 @@
  *   tsqr_f64_block_factor      <- qr_unblocked (mode 0) / qr_triangle_on_rect
  *                                 (mode 2) on blocks of <= 128 rows
  *   tsqr_f64_block_apply       <- apply_q / apply_qt on those single-block factors
+ *   tsqr_f64_geqr2             <- qr_unblocked of any shape (householder.py:128-145)
+ *   tsqr_f64_form_t            <- form_t (householder.py:148-164)
  *                                 (householder.py:377-396)
  */
 #ifndef CAQR_SM100_H
@@ -123,6 +125,21 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
 int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
                           double* Y, int64_t ldy, double* tau, int mode, int* flag, void* stream);
 
+/* qr_unblocked (householder.py:128-145) of any m x n block, in place in LAPACK
+ * layout (R on/above the diagonal, reflectors v_j below it with v_j[0] = 1
+ * implicit) plus tau[n]; house_gen scalars (:89-114), update skipped for tau = 0
+ * (:142).  Single CTA, no shape limit: the kernel-level API beyond the
+ * shared-memory block kernels (qr_unblocked / qr_blocked panels / qr_recursive
+ * leaves / house_gen / stacked and triangle-on-rectangle factors). */
+int tsqr_f64_geqr2(double* A, int64_t lda, int64_t m, int64_t n, double* tau, int* flag,
+                   void* stream);
+
+/* form_t (householder.py:148-164): upper-triangular T (n x n, ldt) from the Gram
+ * G = Y^T Y (strict upper part read, ldg) and tau: T[j][j] = tau_j,
+ * T[:j, j] = -tau_j T[:j, :j] G[:j, j], skipped when tau_j = 0. */
+int tsqr_f64_form_t(const double* G, int64_t ldg, int64_t n, const double* tau, double* T,
+                    int64_t ldt, void* stream);
+
 /* Q C / Q^T C for a single-block factor of tsqr_f64_block_factor: mode 0 =
  * DENSE (C has rows rows), mode 2 = TRIRECT (C = [Ctop (n rows, ldt); C
  * (rows rows)]); rows <= 128. */
@@ -144,10 +161,7 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 /* CAQR_TUNE_ZSTART: 1 (default) = R-only leaves (no Y stored) run the chain from
  * R = 0 over all their rows instead of a dense first tile + chain. */
 #define CAQR_TUNE_ZSTART 6
-/* CAQR_TUNE_BLOCKED: 1 = R-only leaves with n in (64, 128] run the tall-tile kernel (128-row
- * tiles in shared memory, 16-column panels, compact-WY trailing update on the FP64 tensor
- * cores); 0 (default) = the warp-ring chain. */
-#define CAQR_TUNE_BLOCKED 8
+/* (key 8 retired: the tall-tile leaf measured slower than the DMMA ring and was removed) */
 /* CAQR_TUNE_DMMA: 1 (default) = leaves with n in (64, 128] run the DMMA warp ring
  * (16-row tiles per warp in registers, 8-column Level-2 panels with look-ahead,
  * compact-WY trailing updates on the FP64 tensor cores); 2 = also n in (32, 64] (the NP = 64

@@ -29,6 +29,8 @@ SYMBOLS = (
     "tsqr_f64_leaf_apply",
     "tsqr_f64_block_factor",
     "tsqr_f64_block_apply",
+    "tsqr_f64_geqr2",
+    "tsqr_f64_form_t",
     "caqr_tune",
     "caqr_f64_peak_probe",
 )
@@ -74,6 +76,10 @@ def _sig(lib):
     lib.tsqr_f64_block_factor.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i32, ip, vp]
     lib.tsqr_f64_block_apply.restype = i32
     lib.tsqr_f64_block_apply.argtypes = [dp, i64, i64, i64, dp, dp, i64, dp, i64, i64, i32, i32, vp]
+    lib.tsqr_f64_geqr2.restype = i32
+    lib.tsqr_f64_geqr2.argtypes = [dp, i64, i64, i64, dp, ip, vp]
+    lib.tsqr_f64_form_t.restype = i32
+    lib.tsqr_f64_form_t.argtypes = [dp, i64, i64, dp, dp, i64, vp]
     lib.caqr_tune.restype = i32
     lib.caqr_tune.argtypes = [i32, i32]
     lib.caqr_f64_peak_probe.restype = i32
@@ -126,7 +132,6 @@ def check(rc: int, what: str) -> None:
 TUNE_CHAIN_HT = {32: 1, 64: 2, 128: 3}
 TUNE_NARROW = 4
 TUNE_ZSTART = 6
-TUNE_BLOCKED = 8
 TUNE_DMMA = 9
 TUNE_DMMA_APPLY = 10
 TUNE_DMMA_Q = 11
@@ -138,7 +143,7 @@ TUNE_CC = 15
 
 # the library's defaults (csrc/tsqr_sm100.cu, g_ht / g_narrow / ... initialisers)
 TUNE_DEFAULTS = {TUNE_CHAIN_HT[32]: 16, TUNE_CHAIN_HT[64]: 16, TUNE_CHAIN_HT[128]: 16,
-                 TUNE_NARROW: 2, TUNE_ZSTART: 1, TUNE_BLOCKED: 0, TUNE_DMMA: 2,
+                 TUNE_NARROW: 2, TUNE_ZSTART: 1, TUNE_DMMA: 2,
                  TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1, TUNE_DMMA_TREE: 1,
                  TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 0}
 

@@ -235,6 +235,10 @@ k_leaf_split(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
         SP_ADD(9, u1_, u2_);
         double* rrow = Rpan + 2 * q * ldr + g;
         int bb = p + 2;
+#ifdef SP_NOUPD
+        bb = npan;  // probe only: skip the trailing updates (wrong R)
+        dr_signal(ufirst + s, job + 1, lane);
+#endif
         // two blocks at a time: independent DMMA chains side by side
         for (; bb + 1 < npan; bb += 2) {
           double c0[4], c1[4];

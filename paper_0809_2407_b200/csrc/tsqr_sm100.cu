@@ -57,7 +57,6 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 static int g_ht[3] = {16, 16, 16};  // NP = 32, 64, 128 (16: the DMMA rings' tile)
 static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
-static int g_blocked = 0;  // CAQR_TUNE_BLOCKED: R-only n in (64,128] leaves on the tall-tile DMMA kernel
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
 static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles on DMMA (opt-in, slower)
@@ -176,7 +175,6 @@ k_leaf_chain(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P,
 }
 
 
-#include "blocked_leaf.cuh"
 
 // ---------------------------------------------------------------------------
 // Narrow leaves (n <= 8, R only): one warp per leaf, lane-private chains.
@@ -1039,6 +1037,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 #include "dmma_ring.cuh"
 #include "dmma_apply.cuh"
 #include "split_leaf.cuh"
+#include "dense_geqr2.cuh"
 
 // ===========================================================================
 // C-ABI
@@ -1201,11 +1200,6 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       else if (v16) DMMA_LAUNCH(NPV, true, false)                                                    \
       else if (Y) DMMA_LAUNCH(NPV, false, true)                                                      \
       else DMMA_LAUNCH(NPV, false, false)                                                            \
-    } else if (NPV == 128 && zs && g_blocked) {                                                 \
-      rc = prep(k_leaf_blocked, BlockedSmem::bytes);                                         \
-      if (rc) return rc;                                                                        \
-      k_leaf_blocked<<<grid, 256, BlockedSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, base,  \
-                                                               R, flag);                        \
     } else if (zs || m - base * (P - 1) > (int64_t)WARPS * Geo<NPV>::HD) {                       \
       if (g_ht[np_index(NPV)] == HA) CHAIN_LAUNCH(NPV, HA)                                      \
       else if (NPV == 64 && g_ht[1] == 24) CHAIN_LAUNCH(64, 24)                                 \
@@ -1551,6 +1545,22 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
   return check_launch("k_block_apply");
 }
 
+int tsqr_f64_geqr2(double* A, int64_t lda, int64_t m, int64_t n, double* tau, int* flag,
+                   void* stream) {
+  if (!A || !tau || m < 1 || n < 1 || n > INT32_MAX || lda < n)
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_geqr2: bad arguments");
+  k_geqr2<<<1, GQ_THREADS, 0, (cudaStream_t)stream>>>(A, lda, m, (int)n, tau, flag);
+  return check_launch("k_geqr2");
+}
+
+int tsqr_f64_form_t(const double* G, int64_t ldg, int64_t n, const double* tau, double* T,
+                    int64_t ldt, void* stream) {
+  if (!G || !tau || !T || n < 1 || n > INT32_MAX || ldg < n || ldt < n)
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_form_t: bad arguments");
+  k_form_t<<<1, 1024, 0, (cudaStream_t)stream>>>(G, ldg, (int)n, tau, T, ldt);
+  return check_launch("k_form_t");
+}
+
 int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
@@ -1563,10 +1573,6 @@ int caqr_tune(int key, int value) {
   if (key == CAQR_TUNE_NARROW) {
     if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW takes 0, 1 or 2");
     g_narrow = value;
-    return CAQR_OK;
-  }
-  if (key == CAQR_TUNE_BLOCKED) {
-    g_blocked = value ? 1 : 0;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_DMMA_DENSE) {

@@ -2,19 +2,27 @@
 
 Mirrors ``pkg/src/caqr/householder.py``: every
 function keeps the reference's signature, return convention ``(factor, R)``,
-shape tags and error types, and runs on the sm_100a library:
+shape tags and error types, and has no shape limit beyond the reference's own:
 
-* house_gen, qr_unblocked (m <= 128), qr_recursive (m <= 128),
-  qr_triangle_on_rect (rectangle <= 128 rows), qr_stacked_triangles
-  ((q-1) n <= 128)  -> single-CTA sweep ``tsqr_f64_block_factor``;
-* qr_unblocked / qr_recursive on taller matrices -> the TSQR leaf kernel with
-  one leaf, returned as a ``CHAIN`` factor (dense first tile + flat chain of
-  triangle-on-rectangle tiles; same R, different but equivalent implicit Q);
-* qr_blocked -> CAQR with panel width nb (the SPEC's Pr = Pc = 1 case);
-* apply_q / apply_qt / explicit_q / apply_qt_structured -> the apply kernels.
+* blocks of <= 128 rows and columns -> the single-CTA shared-memory sweep
+  ``tsqr_f64_block_factor`` (qr_unblocked, qr_triangle_on_rect,
+  qr_stacked_triangles, house_gen);
+* anything larger -> ``tsqr_f64_geqr2``, the general in-place geqr2 kernel
+  (dense factors; on stacked triangles / [R; B] its exact zeros reproduce the
+  structured reflectors);
+* qr_blocked -> the reference's algorithm (:189-211): qr_unblocked panels,
+  form_t, and the compact-WY trailing update as library GEMMs; nb = 1 is
+  qr_unblocked itself, as in the reference (:199-200);
+* qr_recursive -> Elmroth-Gustavson recursion (:214-251): the halves
+  factored recursively, the left half applied to the right one in compact WY,
+  T merged as T12 = -T1 (Y1^T Y2) T2;
+* form_t -> Gram by one library GEMM, recurrence ``tsqr_f64_form_t``;
+* apply_q / apply_qt / explicit_q / apply_qt_structured -> the block apply
+  kernels up to 128 rows, compact WY (I - Y T Y^T) above.
 
-Inputs may be numpy (results come back as numpy, like the reference) or CUDA
-torch tensors.  There is no CPU fallback.
+The SPEC drivers (tsqr, caqr) are in ``tsqr`` / ``caqr``.  Inputs may be numpy
+(results come back as numpy, like the reference) or CUDA torch tensors.  There
+is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -140,67 +148,156 @@ def house_gen(x, counter: FlopCounter | None = None):
     if xt.ndim != 1 or xt.numel() == 0:
         raise DimensionError("house_gen expects a nonempty vector")
     L = xt.numel()
-    if L > BLOCK_ROWS:
-        raise DimensionError(f"house_gen on the GPU supports vectors of <= {BLOCK_ROWS} entries")
     A = xt.to("cuda").reshape(L, 1).contiguous()
-    R = torch.zeros((1, 1), dtype=torch.float64, device=A.device)
-    Y, tau = _block_factor(A, 1, 0, R)
-    v = Y[:, 0].clone()
+    if L <= BLOCK_ROWS:
+        R = torch.zeros((1, 1), dtype=torch.float64, device=A.device)
+        Y, tau = _block_factor(A, 1, 0, R)
+        v = Y[:, 0].clone()
+        beta = float(R[0, 0])
+    else:
+        W, tau = _geqr2(A)
+        v = W[:, 0].clone()
+        beta = float(W[0, 0])
     v[0] = 1.0
     if counter is not None:
         counter.add(*count_house(L))
-    return v.cpu().numpy(), float(tau[0]), float(R[0, 0])
+    return v.cpu().numpy(), float(tau[0]), beta
+
+
+def _geqr2(At: torch.Tensor):
+    """In-place geqr2 of a copy of At (LAPACK layout) -> (W, tau)."""
+    lib = _lib.load()
+    W = At.clone().contiguous()
+    m, n = W.shape
+    tau = torch.zeros(n, dtype=torch.float64, device=W.device)
+    flag = _flag(W.device)
+    _lib.check(lib.tsqr_f64_geqr2(_ptr(W), n, m, n, _ptr(tau), _ptr(flag), _stream(W.device)),
+               "tsqr_f64_geqr2")
+    if int(flag.item()):
+        raise ValueError("matrix contains NaN or Inf entries")
+    return W, tau
+
+
+def _unit_lower(W: torch.Tensor, n: int) -> torch.Tensor:
+    Y = torch.tril(W[:, :n], -1)
+    Y[torch.arange(n), torch.arange(n)] = 1.0
+    return Y
+
+
+def _dense_qr(At: torch.Tensor):
+    """qr_unblocked on the device: (Y m x n unit lower trapezoid, tau, R)."""
+    m, n = At.shape
+    if m <= BLOCK_ROWS:
+        R = torch.zeros((n, n), dtype=torch.float64, device=At.device)
+        Yraw, tau = _block_factor(At.contiguous(), n, 0, R)
+        return _unit_lower(Yraw, n), tau, R
+    W, tau = _geqr2(At)
+    return _unit_lower(W, n), tau, torch.triu(W[:n])
 
 
 def qr_unblocked(A, counter: FlopCounter | None = None):
-    """Householder QR (householder.py:128-145): (factor, R)."""
+    """Householder QR (householder.py:128-145): (DENSE factor, R)."""
     At, host = to_device(A)
     m, n = At.shape
     if m < n:
         raise DimensionError(f"need m >= n, got {m} x {n}")
-    if n > BLOCK_ROWS:
-        raise DimensionError(f"GPU kernels support n <= {BLOCK_ROWS}")
-    if m <= BLOCK_ROWS:
-        R = torch.zeros((n, n), dtype=torch.float64, device=At.device)
-        Yraw, tau = _block_factor(At, n, 0, R)
-        Y = torch.tril(Yraw, -1)
-        Y[torch.arange(n), torch.arange(n)] = 1.0
-        if counter is not None:
-            counter.add(*count_geqr2(m, n))
-        f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), DENSE,
-                              impl=(Y, tau))
-        return f, _out(R, host)
-    from .tsqr import factor_device
-
-    tf = factor_device(At, 1, want_q=True, counter=counter, host=host)
-    f = HouseholderFactor(tf.Y.cpu().numpy(), tf.tau.cpu().numpy().reshape(-1), CHAIN, impl=tf)
-    return f, tf.R_out()
+    Y, tau, R = _dense_qr(At)
+    if counter is not None:
+        counter.add(*count_geqr2(m, n))
+    f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), DENSE, impl=(Y, tau))
+    return f, _out(R, host)
 
 
-def qr_recursive(A, min_width: int = 4, counter: FlopCounter | None = None):
-    """Same R as qr_unblocked (householder.py:214-251); T cached on the factor."""
-    if min_width < 1:
-        raise DimensionError("min_width must be >= 1")
-    f, R = qr_unblocked(A, counter)
-    if f.shape_tag == DENSE:
-        f.T = form_t(f.Y, f.tau)
-    return f, R
+def _apply_yt(C: torch.Tensor, Y: torch.Tensor, T: torch.Tensor, transpose: bool) -> None:
+    """C := (I - Y T Y^T)^(T?) C in place (householder.py:175-186), as GEMMs."""
+    W = Y.T @ C
+    W = (T.T if transpose else T) @ W
+    C -= Y @ W
+
+
+def _form_t_dev(Y: torch.Tensor, tau: torch.Tensor) -> torch.Tensor:
+    lib = _lib.load()
+    n = Y.shape[1]
+    G = (Y.T @ Y).contiguous()
+    T = torch.empty((n, n), dtype=torch.float64, device=Y.device)
+    if n <= 512:
+        _lib.check(lib.tsqr_f64_form_t(_ptr(G), n, n, _ptr(tau), _ptr(T), n, _stream(Y.device)),
+                   "tsqr_f64_form_t")
+        return T
+    # T = D (I + S D)^-1 with S = striu(G), D = diag(tau): the recurrence in closed form
+    D = torch.diag(tau)
+    U = torch.eye(n, dtype=torch.float64, device=Y.device) + torch.triu(G, 1) @ D
+    return torch.linalg.solve_triangular(U, D, upper=True, left=False, unitriangular=True)
 
 
 def qr_blocked(A, nb: int, counter: FlopCounter | None = None):
-    """Blocked QR (householder.py:189-211) = CAQR with panel width nb on one GPU."""
+    """Blocked QR (householder.py:189-211): qr_unblocked panels of width nb,
+    trailing update through each panel's T; nb = 1 is qr_unblocked itself."""
     At, host = to_device(A)
     m, n = At.shape
     if m < n:
         raise DimensionError(f"need m >= n, got {m} x {n}")
     if not 1 <= nb <= n:
         raise DimensionError(f"nb must be in [1, {n}], got {nb}")
-    from .caqr import caqr_factor
+    if nb == 1:
+        return qr_unblocked(A, counter)
+    W = At.clone()
+    Y = torch.zeros((m, n), dtype=torch.float64, device=W.device)
+    tau = torch.zeros(n, dtype=torch.float64, device=W.device)
+    for j0 in range(0, n, nb):
+        j1 = min(j0 + nb, n)
+        Yp, tp, Rp = _dense_qr(W[j0:, j0:j1])
+        Y[j0:, j0:j1] = Yp
+        tau[j0:j1] = tp
+        W[j0:, j0:j1] = 0.0
+        W[j0:j1, j0:j1] = Rp
+        if j1 < n:
+            _apply_yt(W[j0:, j1:], Yp, _form_t_dev(Yp, tp), transpose=True)
+        if counter is not None:
+            counter.add(*count_geqr2(m - j0, j1 - j0))
+    R = torch.triu(W[:n, :n])
+    f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), DENSE, impl=(Y, tau))
+    return f, _out(R, host)
 
-    res = caqr_factor(At, b=min(nb, BLOCK_ROWS), counter=counter)
-    res.host = host
-    f = HouseholderFactor(np.zeros((0, n)), np.zeros(0), BLOCKED, impl=res)
-    return f, res.R
+
+def qr_recursive(A, min_width: int = 4, counter: FlopCounter | None = None):
+    """Recursive QR (householder.py:214-251): halving column splits, T merged
+    on the way up (T12 = -T1 (Y1^T Y2) T2); the factor carries T."""
+    At, host = to_device(A)
+    m, n = At.shape
+    if m < n:
+        raise DimensionError(f"need m >= n, got {m} x {n}")
+    if min_width < 1:
+        raise DimensionError("min_width must be >= 1")
+    W = At.clone()
+
+    def rec(block: torch.Tensor):
+        bm, bn = block.shape
+        if bn <= min_width:
+            Yb, tb, Rb = _dense_qr(block)
+            block.zero_()
+            block[:bn] = Rb
+            if counter is not None:
+                counter.add(*count_geqr2(bm, bn))
+            return Yb, tb, _form_t_dev(Yb, tb)
+        n1 = bn // 2
+        Y1, t1, T1 = rec(block[:, :n1])
+        _apply_yt(block[:, n1:], Y1, T1, transpose=True)
+        Y2, t2, T2 = rec(block[n1:, n1:])
+        Yb = torch.zeros((bm, bn), dtype=torch.float64, device=block.device)
+        Yb[:, :n1] = Y1
+        Yb[n1:, n1:] = Y2
+        Tb = torch.zeros((bn, bn), dtype=torch.float64, device=block.device)
+        Tb[:n1, :n1] = T1
+        Tb[n1:, n1:] = T2
+        Tb[:n1, n1:] = -T1 @ ((Y1[n1:].T @ Y2) @ T2)
+        return Yb, torch.cat([t1, t2]), Tb
+
+    Y, tau, T = rec(W)
+    R = torch.triu(W[:n, :n])
+    f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), DENSE, T=T.cpu().numpy(),
+                          impl=(Y, tau))
+    return f, _out(R, host)
 
 
 def qr_stacked_triangles(Rs, counter: FlopCounter | None = None):
@@ -218,12 +315,15 @@ def qr_stacked_triangles(Rs, counter: FlopCounter | None = None):
     for t, R in enumerate(tris):
         if tuple(R.shape) != (n, n):
             raise DimensionError(f"triangle {t} has shape {tuple(R.shape)}, expected {(n, n)}")
-    if (q - 1) * n > BLOCK_ROWS:
-        raise DimensionError(f"GPU block kernel supports (q-1) n <= {BLOCK_ROWS}")
-    Rtop = tris[0].clone()
-    low = torch.cat(tris[1:], dim=0).contiguous()
-    Yl, tau = _block_factor(low, n, 3, Rtop)
-    Y = torch.cat([torch.eye(n, dtype=torch.float64, device=Yl.device), Yl], dim=0)
+    if (q - 1) * n <= BLOCK_ROWS:
+        Rtop = tris[0].clone()
+        low = torch.cat(tris[1:], dim=0).contiguous()
+        Yl, tau = _block_factor(low, n, 3, Rtop)
+        Y = torch.cat([torch.eye(n, dtype=torch.float64, device=Yl.device), Yl], dim=0)
+    else:  # dense geqr2 of the stack: its exact zeros keep the stacked profile
+        Wst, tau = _geqr2(torch.cat(tris, dim=0))
+        Y = _unit_lower(Wst, n)
+        Rtop = torch.triu(Wst[:n])
     if counter is not None:
         f_, d_ = count_stacked(n, q)
         counter.add(f_, d_)
@@ -238,10 +338,13 @@ def qr_triangle_on_rect(Rtri, B, counter: FlopCounter | None = None):
     n, r = Rt.shape[0], Bt.shape[0]
     if Bt.shape[1] != n:
         raise DimensionError(f"rectangle has {Bt.shape[1]} columns, triangle has {n}")
-    if r > BLOCK_ROWS or n > BLOCK_ROWS:
-        raise DimensionError(f"GPU block kernel supports rectangles of <= {BLOCK_ROWS} rows")
-    Rw = Rt.clone()
-    Y, tau = _block_factor(Bt, n, 2, Rw)
+    if r <= BLOCK_ROWS and n <= BLOCK_ROWS:
+        Rw = Rt.clone()
+        Y, tau = _block_factor(Bt, n, 2, Rw)
+    else:  # dense geqr2 of [R; B]: zeros below R's diagonal keep the identity top
+        Wst, tau = _geqr2(torch.cat([Rt, Bt], dim=0))
+        Y = Wst[n:].contiguous()
+        Rw = torch.triu(Wst[:n])
     if counter is not None:
         counter.add(*count_tri_rect(n, r))
     f = HouseholderFactor(Y.cpu().numpy(), tau.cpu().numpy(), TRI_ON_RECT, rows_rect=r,
@@ -250,22 +353,13 @@ def qr_triangle_on_rect(Rtri, B, counter: FlopCounter | None = None):
 
 
 def form_t(Y, tau, counter: FlopCounter | None = None):
-    """T with I - Y T Y^T = H_0 ... H_{n-1} (householder.py:148-164).
-
-    The Gram Y^T Y is one cuBLAS GEMM; the triangular recurrence runs on device.
-    """
+    """T with I - Y T Y^T = H_0 ... H_{n-1} (householder.py:148-164): the Gram
+    Y^T Y as one library GEMM, the recurrence in ``tsqr_f64_form_t``."""
     Yt = torch.as_tensor(np.asarray(Y) if not isinstance(Y, torch.Tensor) else Y,
                          dtype=torch.float64).to("cuda")
     tt = torch.as_tensor(np.asarray(tau) if not isinstance(tau, torch.Tensor) else tau,
-                         dtype=torch.float64).to(Yt.device)
-    n = Yt.shape[1]
-    G = Yt.T @ Yt
-    T = torch.zeros((n, n), dtype=torch.float64, device=Yt.device)
-    for j in range(n):
-        T[j, j] = tt[j]
-        if j:
-            z = T[:j, :j] @ G[:j, j]
-            T[:j, j] = torch.where(tt[j] != 0, -tt[j] * z, torch.zeros_like(z))
+                         dtype=torch.float64).to(Yt.device).contiguous()
+    T = _form_t_dev(Yt, tt)
     return T.cpu().numpy() if not isinstance(Y, torch.Tensor) else T
 
 
@@ -298,10 +392,15 @@ def apply_q(factor: HouseholderFactor, C, transpose: bool = False,
     tag = factor.shape_tag
     out = Ct.clone()
     n = factor.n
-    if tag == DENSE:
+    big = factor.m > BLOCK_ROWS or n > BLOCK_ROWS or (tag == STACKED and factor.q != 2)
+    if tag in (DENSE, STACKED, TRI_ON_RECT) and big:
+        # compact WY: Q = I - Y T Y^T (T cached on the factor)
+        if factor.T is None:
+            factor.T = form_t(factor.full_y(), factor.tau)
+        Yf = _dev(factor.full_y(), out)
+        _apply_yt(out, Yf, _dev(factor.T, out), transpose)
+    elif tag == DENSE:
         Y, tau = factor.impl if factor.impl is not None else (_dev(factor.Y), _dev(factor.tau))
-        if factor.m > BLOCK_ROWS:
-            raise DimensionError("DENSE factors above 128 rows come from the CHAIN path")
         _block_apply(Y.contiguous(), tau, factor.m, n, out, 0, transpose)
     elif tag == TRI_ON_RECT:
         Y, tau = factor.impl if factor.impl is not None else (_dev(factor.Y), _dev(factor.tau))
@@ -311,8 +410,6 @@ def apply_q(factor: HouseholderFactor, C, transpose: bool = False,
         out = torch.cat([top, bot], dim=0)
     elif tag == STACKED:
         Y, tau = factor.impl if factor.impl is not None else (_dev(factor.Y), _dev(factor.tau))
-        if factor.q != 2:
-            raise DimensionError("GPU apply supports stacked factors with q = 2")
         lib = _lib.load()
         ev = torch.tensor([[0, 1, 0]], dtype=torch.int32, device=out.device)
         Yb = Y[n:].contiguous()

@@ -21,6 +21,7 @@ from .core import as_matrix
 
 MAGIC = b"TSQRMAT1"
 _HEAD = struct.Struct("<8sIIII")  # magic, rows, cols, 2 x reserved (matio.py:22)
+HEADER = _HEAD  # the reference's public name (tests build headers with it)
 
 
 class FormatError(ValueError):

@@ -46,12 +46,16 @@ def test_unblocked_against_golden(golden):
         assert np.max(np.abs(f.Y - g[f"{tag}_Y"])) <= 1e-12
         assert np.max(np.abs(f.tau - g[f"{tag}_tau"])) <= 1e-13
         assert np.max(np.abs(explicit_q(f) - g[f"{tag}_Q"])) <= 1e-12
-    # taller than one block: CHAIN factor, same R up to rounding
+    # taller than one block: the general geqr2 kernel, a DENSE factor with the
+    # reference's own reflectors
     A = g["unb_160x64_A"]
     f, R = qr_unblocked(A)
-    assert f.shape_tag == "chain"
+    assert f.shape_tag == "dense"
     assert oracle.r_diff(R, g["unb_160x64_R"]) <= 100 * EPS
+    assert np.max(np.abs(f.Y - g["unb_160x64_Y"])) <= 1e-12
+    assert np.max(np.abs(f.tau - g["unb_160x64_tau"])) <= 1e-13
     Q = explicit_q(f)
+    assert np.max(np.abs(Q - g["unb_160x64_Q"])) <= 1e-12
     assert oracle.residual(A, Q, R) <= 10 * 64 * EPS
 
 
@@ -124,9 +128,104 @@ def test_triangle_on_rect_against_golden(golden):
     assert np.array_equal(R2, R) and np.all(f.tau == 0.0)
 
 
-def test_blocked_is_caqr(golden):
+def test_blocked_against_golden(golden):
+    """qr_blocked keeps the reference's DENSE factor (geqr2 reflectors, tau)."""
     from paper_0809_2407_b200.householder import qr_blocked
 
     g = golden["kernels"]
     f, R = qr_blocked(g["blk_256x128_A"], 32)
+    assert f.shape_tag == "dense"
     assert oracle.r_diff(R, g["blk_256x128_R"]) <= 1000 * EPS
+    assert np.max(np.abs(f.tau - g["blk_256x128_tau"])) <= 1e-12
+
+
+def test_general_shapes_beyond_one_block():
+    """No shape limit beyond the reference's (householder.py:89-332): the general
+    geqr2 kernel covers house_gen L > 128, qr_unblocked n > 128, stacked factors
+    with (q-1) n > 128 and triangle-on-rectangle with r > 128, checked against
+    the oracle restatement element by element."""
+    from paper_0809_2407_b200.householder import (apply_q, explicit_q, house_gen,
+                                                  qr_stacked_triangles, qr_triangle_on_rect,
+                                                  qr_unblocked)
+
+    x = philox(50).standard_normal(1000)
+    v, tau, beta = house_gen(x)
+    vo, to, bo = oracle.reflector(x)
+    assert abs(beta - bo) <= 4 * EPS * abs(bo) and abs(tau - to) <= 4 * EPS
+    assert np.max(np.abs(v - vo)) <= 1e-13
+    A = philox(51).standard_normal((300, 150))
+    f, R = qr_unblocked(A)
+    Yo, to, Ro = oracle.geqr2(A)
+    assert np.max(np.abs(R - Ro)) <= 100 * EPS * np.abs(Ro).max()
+    assert np.max(np.abs(f.Y - Yo)) <= 1e-11 and np.max(np.abs(f.tau - to)) <= 1e-12
+    Q = explicit_q(f)
+    assert oracle.residual(A, Q, R) <= 10 * 150 * EPS and oracle.orthogonality(Q) <= 10 * 150 * EPS
+    C = philox(52).standard_normal((300, 7))
+    assert np.max(np.abs(apply_q(f, apply_q(f, C), transpose=True) - C)) <= 1e-12
+    # q = 3 stacked triangles, n = 80: dense geqr2 of the stack keeps the profile
+    rng = philox(53)
+    Rs = [np.triu(rng.standard_normal((80, 80))) for _ in range(3)]
+    fs, Rst = qr_stacked_triangles(Rs)
+    S = np.vstack(Rs)
+    assert oracle.r_diff(Rst, np.linalg.qr(S, mode="r")) <= 100 * EPS
+    prof = np.zeros_like(fs.Y, dtype=bool)
+    for j in range(80):
+        prof[fs.reflector(j)[0], j] = True
+    assert np.all(fs.Y[~prof] == 0.0) and np.array_equal(fs.Y[:80], np.eye(80))
+    Qs = explicit_q(fs)
+    assert oracle.residual(S, Qs, Rst) <= 10 * 80 * EPS
+    # triangle on a 200-row rectangle
+    R0 = np.triu(rng.standard_normal((70, 70)))
+    B = rng.standard_normal((200, 70))
+    ft, Rt = qr_triangle_on_rect(R0, B)
+    Vo, tauo, Rto = oracle.tri_rect_qr(R0, B)
+    assert np.max(np.abs(Rt - Rto)) <= 100 * EPS * np.abs(Rto).max()
+    assert np.max(np.abs(ft.Y - Vo)) <= 1e-12 and np.max(np.abs(ft.tau - tauo)) <= 1e-13
+
+
+def test_blocked_recursive_bitwise_relations():
+    """The reference's own structural identities (test_householder.py:98-128):
+    qr_blocked(nb = 1) IS qr_unblocked, qr_recursive without a split IS
+    qr_blocked(nb = n) -- bitwise, on one block and beyond it."""
+    from paper_0809_2407_b200.householder import qr_blocked, qr_recursive, qr_unblocked
+
+    for (m, n) in [(16, 6), (20, 6), (400, 140)]:
+        A = philox(60 + m).standard_normal((m, n))
+        _, R1 = qr_unblocked(A)
+        _, R2 = qr_blocked(A, nb=1)
+        assert np.array_equal(R1, R2)
+        _, R3 = qr_blocked(A, nb=n)
+        _, R4 = qr_recursive(A, min_width=n)
+        assert np.array_equal(R3, R4) and np.array_equal(R1, R3)
+
+
+def test_recursive_elmroth_gustavson():
+    """qr_recursive splits columns in halves and merges T (householder.py:214-251):
+    R against the oracle, the cached T reproduces Q = I - Y T Y^T."""
+    from paper_0809_2407_b200.householder import explicit_q, form_t, qr_recursive
+
+    for (m, n, mw) in [(32, 8, 2), (300, 130, 16), (64, 33, 1)]:
+        A = philox(70 + n).standard_normal((m, n))
+        f, R = qr_recursive(A, min_width=mw)
+        Ro = oracle.geqr2(A)[2]
+        assert oracle.r_diff(R, Ro) <= 100 * EPS
+        Y = f.Y
+        Qt = np.eye(m)[:, :n] - Y @ (f.T @ (Y[:n].T))
+        Q = explicit_q(f)
+        assert np.max(np.abs(Q - Qt)) <= 1e-12
+        assert oracle.residual(A, Q, R) <= 10 * n * EPS
+        assert np.max(np.abs(form_t(Y, f.tau) - f.T)) <= 1e-12 * max(1.0, np.abs(f.T).max())
+
+
+def test_form_t_kernel_against_oracle():
+    """form_t (householder.py:148-164): the device recurrence equals the oracle's
+    larft, including tau = 0 columns (the recurrence is skipped there)."""
+    from paper_0809_2407_b200.householder import form_t
+
+    Y, tau, _ = oracle.geqr2(philox(80).standard_normal((300, 40)))
+    tau = tau.copy()
+    tau[[3, 17]] = 0.0
+    T = form_t(Y, tau)
+    To = oracle.larft(Y, tau)
+    assert np.max(np.abs(T - To)) <= 1e-13 * np.abs(To).max()
+    assert np.all(T[:4, 3] == 0.0) and np.all(T[:18, 17] == 0.0)

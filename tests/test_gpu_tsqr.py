@@ -323,28 +323,6 @@ def test_tsqr_from_mat1_file_is_bitwise_the_in_memory_r(tmp_path, m, n, leaf, K)
     assert np.array_equal(Rk, factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy())
 
 
-def test_blocked_tall_tile_leaf_parity():
-    """CAQR_TUNE_BLOCKED = 1: R-only leaves with n in (64, 128] on the tall-tile
-    kernel (shared-memory tiles, DMMA compact-WY trailing updates)."""
-    from paper_0809_2407_b200 import _lib
-    from paper_0809_2407_b200.tsqr import factor_device
-
-    try:
-        _lib.tune(_lib.TUNE_BLOCKED, 1)
-        for (m, n, P) in [(4096, 128, 2), (20000, 100, 4), (3000, 70, 1), (9001, 128, 3)]:
-            A = philox(m + n).standard_normal((m, n))
-            R = factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy()
-            assert np.array_equal(R, np.triu(R))
-            assert oracle.r_diff(R, np.linalg.qr(A, mode="r"), np.linalg.norm(A, 2)) <= 1000 * EPS
-        A = philox(7).standard_normal((5000, 96))
-        A[4321, 50] = np.nan
-        with pytest.raises(ValueError):
-            factor_device(torch.from_numpy(A).cuda(), 2)
-    finally:
-        _lib.reset_tuning()
-
-
-@pytest.mark.parametrize("v16", [True, False])
 def test_dmma_ring_leaf_parity(v16):
     """CAQR_TUNE_DMMA = 1 (default): R-only leaves with n in (64, 128] on the
     DMMA warp ring (16-row register tiles, 8-column Level-2 panels with
