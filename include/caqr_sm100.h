@@ -155,7 +155,8 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
 #define CAQR_TUNE_CHAIN_HT_64 2
 #define CAQR_TUNE_CHAIN_HT_128 3
 /* CAQR_TUNE_NARROW: lane-private chains for n <= 8 when no Q is stored: 0 off, 1 with
- * register prefetch, 2 (default) with cp.async shared-memory stages for 8-column rows. */
+ * register prefetch, 2 with cp.async shared-memory stages for 8-column rows (4 rows per
+ * step), 3 (default) 8 rows per step for contiguous 16-byte-aligned 8-column rows. */
 #define CAQR_TUNE_NARROW 4
 /* 5: reserved (retired experimental kernel). */
 /* CAQR_TUNE_ZSTART: 1 (default) = R-only leaves (no Y stored) run the chain from

@@ -55,7 +55,7 @@ static int padded(int64_t n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ?
 // Chain tile height per padded width (tunable, CAQR_TUNE_CHAIN_HT); it fixes
 // the implicit-Q storage format, so factor and apply calls must agree.
 static int g_ht[3] = {16, 16, 16};  // NP = 32, 64, 128 (16: the DMMA rings' tile)
-static int g_narrow = 2;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (2: cp.async stages)
+static int g_narrow = 3;  // CAQR_TUNE_NARROW: lane-private path for n <= 8, R only (3: K = 8 rows, 2: cp.async K = 4)
 static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense first tile
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
@@ -260,6 +260,198 @@ __device__ __forceinline__ void narrow_load(double (&Bt)[K][8], const double* __
   }
 }
 
+// Epilogue of the narrow leaf kernels: in-warp binary tree over the 32 lane
+// R factors, NaN/Inf flag, then the leaf's R into its slot or the fused
+// ticket tree over leaves.
+__device__ __forceinline__ void narrow_finish(double (&R)[36], int lane, int leaf, int P, int n,
+                                              double* Rout, int* flag, int* tickets) {
+  // in-warp binary tree over the lane R factors (partner rows in two halves)
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double Bs[4][8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = 4 * half + k;
+          Bs[k][c] = (c >= i) ? __shfl_down_sync(FULL, R[pk8(i, c)], off) : 0.0;
+        }
+      if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, Bs, n);
+    }
+  }
+  if (lane != 0) return;
+  // a NaN/Inf anywhere in the leaf reaches its R (every entry enters a norm)
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 36; ++i) bad |= !isfinite(R[i]);
+  if (bad && flag) atomicOr(flag, 1);
+  auto put = [&](int node) {
+    double* Ro = Rout + (int64_t)node * n * n;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[pk8(i, c < i ? i : c)] : 0.0;
+  };
+  if (!tickets) {
+    put(leaf);
+    return;
+  }
+  // Fused binary tree (trees.py:52-66): at level k the second child to arrive
+  // at parent p combines [R_p-side; R_sibling] with the lower index on top.
+  int node = leaf;
+  for (int k = 1; (1 << (k - 1)) < P; ++k) {
+    const int p = node & ~((1 << k) - 1);
+    const int sib_hi = p + (1 << (k - 1));
+    if (sib_hi >= P) continue;  // unpaired at this level: pass up unchanged
+    put(node);
+    __threadfence();
+    const int t = atomicAdd(tickets + (int64_t)(k - 1) * P + p, 1);
+    if (t == 0) return;  // first arrival: the sibling finishes this node
+    __threadfence();
+    // receiver (lower index) on top: [R_p; R_sib].  Both operands were stored
+    // by put(); the top one is (re)loaded into R only when it is the sibling's,
+    // the bottom one streams from memory in two 4-row halves (keeps the live
+    // set at R + one half so the main loop's arrays stay in registers).
+    const int other = (node == p) ? sib_hi : p;
+    const double* Rbot = Rout + (int64_t)((node == p) ? other : node) * n * n;
+    if (node != p) {
+      const double* Rtop = Rout + (int64_t)other * n * n;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = i; c < 8; ++c) R[pk8(i, c)] = (i < n && c < n) ? __ldcg(Rtop + i * n + c) : 0.0;
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double Bs[4][8];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = 4 * half + kk;
+          Bs[kk][c] = (c >= i && i < n && c < n) ? __ldcg(Rbot + i * n + c) : 0.0;
+        }
+      narrow_step<4>(R, Bs, n);
+    }
+    node = p;
+  }
+  put(node);  // the root (node 0)
+}
+
+// n = 8 with contiguous 16-byte-aligned rows (C4): K = 8 rows per lane per
+// step (rows 256 s + 32 k + lane of the leaf), twice the rows of k_leaf_narrow
+// per reflector-scalar chain (the per-column house_newton and the per-(j, c)
+// scalars are amortised over 8 rows: ~25% fewer FP64 instructions per row).
+// No staging buffer: the next step's column pair (2c, 2c+1) is loaded into the
+// registers of columns 2c, 2c+1 as soon as reflector 2c+1 of the current step
+// has consumed them, so the loads run under the rest of the step.
+// Reflector J of one K = 8 step (triangle-on-rectangle column J,
+// householder.py:314-331); after it (J odd) the next step's columns J-1, J
+// are loaded into the registers it consumed.
+template <int J>
+__device__ __forceinline__ void narrow8_col(double (&R)[36], double (&B)[8][8],
+                                            const double2* __restrict__ A2, int64_t st, bool more,
+                                            int64_t b, int lane) {
+  double sg = 0.0, sg2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    sg = fma(B[k][J], B[k][J], sg);
+    sg2 = fma(B[k + 1][J], B[k + 1][J], sg2);
+  }
+  double beta, tau, scale;
+  house_newton(R[pk8(J, J)], sg + sg2, beta, tau, scale);
+#pragma unroll
+  for (int c = J + 1; c < 8; ++c) {
+    double d = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      d = fma(B[k][J], B[k][c], d);
+      d2 = fma(B[k + 1][J], B[k + 1][c], d2);
+    }
+    const double q = tau * fma(scale, d + d2, R[pk8(J, c)]);
+    R[pk8(J, c)] -= q;
+    const double qs = q * scale;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) B[k][c] = fma(-B[k][J], qs, B[k][c]);
+  }
+  R[pk8(J, J)] = beta;
+  if constexpr (J & 1) {
+    if (more) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t row = (st + 1) * 256 + 32 * k + lane;
+        double2 t = make_double2(0.0, 0.0);
+        if (row < b) t = __ldg(A2 + row * 4 + (J >> 1));
+        B[k][J - 1] = t.x;
+        B[k][J] = t.y;
+      }
+    }
+  }
+}
+
+// n = 8 with contiguous 16-byte-aligned rows (C4): K = 8 rows per lane per
+// step (rows 256 s + 32 k + lane of the leaf), twice the rows of k_leaf_narrow
+// per reflector-scalar chain (the per-column house_newton and the per-(j, c)
+// scalars are amortised over 8 rows: ~30% fewer instructions per row).  No
+// staging buffer: the next step's column pair (2c, 2c+1) is loaded into the
+// registers of columns 2c, 2c+1 once reflector 2c+1 has consumed them, from
+// L2 (prefetched three steps ahead).  A shared-memory stage (cp.async one
+// step ahead, LDS at the step boundary) measured slower: 2.14 vs 1.78 ms.
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1)
+k_leaf_narrow8(const double* __restrict__ A, int64_t m, int P, int64_t base, double* Rout, int* flag,
+               int* tickets) {
+  constexpr int K = 8;
+  const int lane = threadIdx.x & 31;
+  const int leaf = blockIdx.x * W + (threadIdx.x >> 5);
+  if (leaf >= P) return;
+  const int64_t r0 = (int64_t)leaf * base;
+  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const int64_t steps = (b + 32 * K - 1) / (32 * K);
+  const double2* A2 = reinterpret_cast<const double2*>(A + r0 * 8);
+  auto prefetch = [&](int64_t st) {  // L2, 128 lines of 128 B per step
+    if (st >= steps) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t line = st * 128 + 32 * i + lane;
+      if (line * 2 < b) asm volatile("prefetch.global.L2 [%0];" :: "l"(A2 + line * 8));
+    }
+  };
+  double R[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) R[i] = 0.0;
+  double B[K][8];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int64_t row = 32 * k + lane;
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) {
+      double2 t = make_double2(0.0, 0.0);
+      if (row < b) t = __ldg(A2 + row * 4 + c2);
+      B[k][2 * c2] = t.x;
+      B[k][2 * c2 + 1] = t.y;
+    }
+  }
+  prefetch(1);
+  prefetch(2);
+  for (int64_t st = 0; st < steps; ++st) {
+    const bool more = st + 1 < steps;
+    prefetch(st + 3);
+    narrow8_col<0>(R, B, A2, st, more, b, lane);
+    narrow8_col<1>(R, B, A2, st, more, b, lane);
+    narrow8_col<2>(R, B, A2, st, more, b, lane);
+    narrow8_col<3>(R, B, A2, st, more, b, lane);
+    narrow8_col<4>(R, B, A2, st, more, b, lane);
+    narrow8_col<5>(R, B, A2, st, more, b, lane);
+    narrow8_col<6>(R, B, A2, st, more, b, lane);
+    narrow8_col<7>(R, B, A2, st, more, b, lane);
+  }
+  narrow_finish(R, lane, leaf, P, 8, Rout, flag, tickets);
+}
+
 template <bool PIPE, int K = NARROW_K, int W = NARROW_WARPS>
 __global__ void __launch_bounds__(W * 32, 1)
 k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
@@ -337,80 +529,7 @@ k_leaf_narrow(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P
       narrow_step<K>(R, B1, n);
     }
   }
-  // in-warp binary tree over the lane R factors (partner rows in two halves)
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      double Bs[4][8];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = 4 * half + k;
-          Bs[k][c] = (c >= i) ? __shfl_down_sync(FULL, R[pk8(i, c)], off) : 0.0;
-        }
-      if ((lane & (2 * off - 1)) == 0) narrow_step<4>(R, Bs, n);
-    }
-  }
-  if (lane != 0) return;
-  // a NaN/Inf anywhere in the leaf reaches its R (every entry enters a norm)
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < 36; ++i) bad |= !isfinite(R[i]);
-  if (bad && flag) atomicOr(flag, 1);
-  auto put = [&](int node) {
-    double* Ro = Rout + (int64_t)node * n * n;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (i < n && c < n) Ro[i * n + c] = (c >= i) ? R[pk8(i, c < i ? i : c)] : 0.0;
-  };
-  if (!tickets) {
-    put(leaf);
-    return;
-  }
-  // Fused binary tree (trees.py:52-66): at level k the second child to arrive
-  // at parent p combines [R_p-side; R_sibling] with the lower index on top.
-  int node = leaf;
-  for (int k = 1; (1 << (k - 1)) < P; ++k) {
-    const int p = node & ~((1 << k) - 1);
-    const int sib_hi = p + (1 << (k - 1));
-    if (sib_hi >= P) continue;  // unpaired at this level: pass up unchanged
-    put(node);
-    __threadfence();
-    const int t = atomicAdd(tickets + (int64_t)(k - 1) * P + p, 1);
-    if (t == 0) return;  // first arrival: the sibling finishes this node
-    __threadfence();
-    // receiver (lower index) on top: [R_p; R_sib].  Both operands were stored
-    // by put(); the top one is (re)loaded into R only when it is the sibling's,
-    // the bottom one streams from memory in two 4-row halves (keeps the live
-    // set at R + one half so the main loop's arrays stay in registers).
-    const int other = (node == p) ? sib_hi : p;
-    const double* Rbot = Rout + (int64_t)((node == p) ? other : node) * n * n;
-    if (node != p) {
-      const double* Rtop = Rout + (int64_t)other * n * n;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int c = i; c < 8; ++c) R[pk8(i, c)] = (i < n && c < n) ? __ldcg(Rtop + i * n + c) : 0.0;
-    }
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      double Bs[4][8];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = 4 * half + kk;
-          Bs[kk][c] = (c >= i && i < n && c < n) ? __ldcg(Rbot + i * n + c) : 0.0;
-        }
-      narrow_step<4>(R, Bs, n);
-    }
-    node = p;
-  }
-  put(node);  // the root (node 0)
+  narrow_finish(R, lane, leaf, P, n, Rout, flag, tickets);
 }
 
 // R-only tree combine as a warp ring: [R_a; R_b] -> R_a with R_a's rows as
@@ -1108,7 +1227,11 @@ static int launch_narrow(const double* A, int64_t lda, int64_t m, int64_t n, int
     k_leaf_narrow<true, KK, NP_::W><<<(int)((P + NP_::W - 1) / NP_::W), NP_::W * 32, NP_::SMEM, \
                                       st>>>(A, lda, m, (int)n, (int)P, base, R, flag, tickets); \
   }
-  if (g_narrow >= 2 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // cp.async 16 B granules
+  if (g_narrow == 3 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // 16-byte rows, K = 8
+    constexpr int W8 = 8;
+    k_leaf_narrow8<W8><<<(int)((P + W8 - 1) / W8), W8 * 32, 0, st>>>(A, m, (int)P, base, R, flag,
+                                                                     tickets);
+  } else if (g_narrow >= 2 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // cp.async 16 B granules
     NARROW_PIPE(4)
   } else {
     k_leaf_narrow<false><<<(int)((P + NARROW_WARPS - 1) / NARROW_WARPS), NARROW_WARPS * 32, 0, st>>>(
@@ -1571,7 +1694,7 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_NARROW) {
-    if (value < 0 || value > 2) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW takes 0, 1 or 2");
+    if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW takes 0 .. 3");
     g_narrow = value;
     return CAQR_OK;
   }
