@@ -31,18 +31,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
+# DRAM bytes (read + write) over the 8mn algorithmic bytes, from this round's
+# ncu --set full captures (profiles/r02/*_ncu_summary.txt)
+NARROW8_TRAFFIC = (8.596103e9 + 10.115584e6) / (8.0 * 134217728 * 8)
+DMMA_TRAFFIC = 1.0047  # k_leaf_dmma, profiles/r01/dmma_kernel_ncu_summary.txt (kernel unchanged)
 METRIC = "TSQR fp64 GFLOP/s & % of roofline"
 
 CONFIGS = {
-    "c1": dict(m=65536, n=32, leaf=8192, q="explicit", dist="normal",
+    "c1": dict(key="c1", m=65536, n=32, leaf=8192, q="explicit", dist="normal",
                name="C1 TSQR 65536x32 N(0,1), 8 leaves of 8192, R + explicit Q"),
-    "c2": dict(m=1048576, n=64, leaf=4096, q="explicit", dist="cond",
+    "c2": dict(key="c2", m=1048576, n=64, leaf=4096, q="explicit", dist="cond",
                name="C2 TSQR 1048576x64 kappa=1e12, leaves of 4096, R + explicit Q"),
-    "c3": dict(m=16777216, n=128, leaf=8192, q="none", dist="normal",
+    "c3": dict(key="c3", m=16777216, n=128, leaf=8192, q="none", dist="normal",
                name="C3 TSQR 16777216x128 N(0,1), leaves of 8192x128, R only"),
-    "c4": dict(m=134217728, n=8, leaf=16384, q="none", dist="uniform",
+    "c4": dict(key="c4", m=134217728, n=8, leaf=16384, q="none", dist="uniform",
                name="C4 TSQR 134217728x8 U(-1,1), leaves of 16384x8, R only"),
-    "c5": dict(m=16384, n=16384, leaf=2048, q="implicit", dist="normal",
+    "c5": dict(key="c5", m=16384, n=16384, leaf=2048, q="implicit", dist="normal",
                name="C5 CAQR 16384x16384 N(0,1), b=128, TSQR leaf 2048, R + implicit Q"),
 }
 
@@ -113,22 +117,76 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # inputs
 # ---------------------------------------------------------------------------
-def make_input(cfg, device, seed=0, rows=None):
+def make_input(cfg, device, lo=0, hi=None, data="reference", seed=0):
+    """Rows [lo, hi) of the config's input on ``device``.
+
+    data = "reference" (default): the reference's own generators, bit for bit
+    (rng_for(0) Philox draws, gen_cond_matrix for C2; paper_0809_2407_b200.synth
+    regenerates any row range from recorded Philox states, so every rank draws
+    only its shard).  data = "torch": torch Philox on the device (fast, for
+    quick runs; not the reference's bits)."""
     import torch
 
-    m = rows if rows is not None else cfg["m"]
+    hi = cfg["m"] if hi is None else hi
+    if data == "reference":
+        from paper_0809_2407_b200 import synth
+
+        return synth.device_input(cfg["key"], device, lo, hi)
     n = cfg["n"]
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     if cfg["dist"] == "uniform":
-        A = torch.rand((m, n), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
-    elif cfg["dist"] == "cond":
+        return torch.rand((hi - lo, n), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+    if cfg["dist"] == "cond":
         from paper_0809_2407_b200.core import CondSpec, gen_cond_matrix
 
-        A = torch.from_numpy(gen_cond_matrix(CondSpec(m, n, kappa=1e12, seed=seed))).to(device)
+        return torch.from_numpy(gen_cond_matrix(CondSpec(hi - lo, n, kappa=1e12, seed=seed))).to(device)
+    return torch.randn((hi - lo, n), generator=g, dtype=torch.float64, device=device)
+
+
+def host_sample(cfg, rows):
+    """The first ``rows`` rows of the config's reference input, on the host."""
+    from paper_0809_2407_b200 import synth
+
+    out = np.empty((rows, cfg["n"]))
+
+    def sink(r0, blk):
+        out[r0:r0 + blk.shape[0]] = blk
+
+    synth.chunks(cfg["key"], 0, rows, sink)
+    return out
+
+
+def parity_vs_reference(cfg, R):
+    """The timed run's R against the reference's R on the same input
+    (tests/golden/fullsize_<cfg>.npz, made by oracle/make_fullsize.py from the
+    read-only reference): max |sn(R) - sn(R_ref)| in eps ||A||_2, bar 1000
+    (pkg/tests/test_householder.py:340-350).  None when the fixture is absent."""
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{cfg['key']}.npz")
+    if R is None or not os.path.exists(path):
+        return None
+    f = np.load(path)
+    Rn = R.detach().cpu().numpy() if hasattr(R, "detach") else np.asarray(R)
+    eps = float(np.finfo(np.float64).eps)
+
+    def sn(X):
+        d = np.sign(np.diag(X)).copy()
+        d[d == 0] = 1.0
+        return d[:, None] * X
+
+    if cfg["key"] == "c5":
+        d = np.sign(np.diag(Rn)).copy()
+        d[d == 0] = 1.0
+        rows = f["rows"]
+        err = max(float(np.max(np.abs(d[rows, None] * Rn[rows] - f["ref_rows"]))),
+                  float(np.max(np.abs(d * np.diag(Rn) - f["ref_diag"]))))
+        err /= float(f["norm2"]) * eps
+        what = "reference qr_blocked(A, 128): sign-normalised diagonal + 8 rows"
     else:
-        A = torch.randn((m, n), generator=g, dtype=torch.float64, device=device)
-    return A
+        err = float(np.max(np.abs(sn(Rn) - sn(f["R_ref"])))) / (float(f["norm2"]) * eps)
+        what = "reference Alg. 1 composition (qr_unblocked leaves + qr_stacked_triangles tree)"
+    return {"vs": what, "fixture": os.path.relpath(path, ROOT), "r_err_eps_norm2": err,
+            "bar": 1000.0, "ok": bool(err <= 1000.0)}
 
 
 # ---------------------------------------------------------------------------
@@ -143,31 +201,31 @@ def cpu_baseline(cfg, budget_s=15.0, threads=None):
         threadpool_limits = None
     n = cfg["n"]
     leaf = min(cfg["leaf"], cfg["m"])
-    rng = np.random.Generator(np.random.Philox(1))
     ctx = threadpool_limits(limits=threads) if (threadpool_limits and threads) else None
     if ctx:
         ctx.__enter__()
     try:
         if cfg is CONFIGS["c5"]:
             N = 2048
-            A = rng.standard_normal((N, N))
+            A = host_sample(cfg, N)[:, :N].copy()  # leading 2048 x 2048 block of the C5 input
             t0 = time.perf_counter()
             oracle.blocked_qr(A, 128)
             dt = time.perf_counter() - t0
             return {"value": flops(N, N) / dt / 1e9, "unit": "GFLOP/s",
-                    "sample": f"reference qr_blocked(A, nb=128) on {N}x{N} (C5 scaled 1/8)",
-                    "seconds": dt}
-        # one leaf first to size the sample
-        Aleaf = rng.standard_normal((leaf, n))
+                    "sample": f"reference qr_blocked(A, nb=128) on the leading {N}x{N} block "
+                              f"of the C5 input (C5 scaled 1/8)", "seconds": dt}
+        # one leaf first to size the sample; leaves are the config input's first rows
+        Aleaf = host_sample(cfg, leaf)
         t0 = time.perf_counter()
         Y, tau, R = oracle.geqr2(Aleaf)
         t_leaf = time.perf_counter() - t0
         Rs = [R]
         t_comb = 0.0
         nleaves = max(2, min(int(budget_s / max(t_leaf, 1e-3)), cfg["m"] // leaf))
+        Asamp = host_sample(cfg, nleaves * leaf)
         t0 = time.perf_counter()
-        for _ in range(nleaves - 1):
-            Y, tau, R = oracle.geqr2(rng.standard_normal((leaf, n)))
+        for i in range(1, nleaves):
+            Y, tau, R = oracle.geqr2(Asamp[i * leaf:(i + 1) * leaf])
             Rs.append(R)
         t_rest = time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -178,8 +236,8 @@ def cpu_baseline(cfg, budget_s=15.0, threads=None):
         m_s = nleaves * leaf
         q = cfg["q"] != "none"
         return {"value": flops(m_s, n) / dt / 1e9, "unit": "GFLOP/s",
-                "sample": (f"reference path (geqr2 leaves + stacked_qr binary tree), {nleaves} "
-                           f"leaves of {leaf}x{n} = {m_s} rows, R only"
+                "sample": (f"reference path (geqr2 leaves + stacked_qr binary tree), the first "
+                           f"{nleaves} leaves of {leaf}x{n} of the config input = {m_s} rows, R only"
                            + ("; Q not formed in the sample" if q else "")),
                 "seconds": dt}
     finally:
@@ -204,7 +262,8 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.median([c["seconds"] for c in vals]) * 1e3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (Philox N(0,1) per config)",
+        "data": "synthetic: the reference's generators (rng_for(0) / gen_cond_matrix), the same "
+                "bits as the GPU arm's input",
         "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "leaf_rows": cfg["leaf"]},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": ncpu, "kind": "port",
                          "sample": vals[0]["sample"]},
@@ -260,6 +319,15 @@ def caqr_roofline(A, cfg, args):
              "algorithmic_flops_per_launch": F, "launch_ms": t * 1e3}, launches)
 
 
+def data_note(cfg, args):
+    if args.data == "reference":
+        return ("synthetic: the reference's own generators, bit for bit (" +
+                ("gen_cond_matrix(CondSpec(2**20, 64, 1e12, 0)), pinned BLAS" if cfg["key"] == "c2"
+                 else "rng_for(0) Philox draws, " + cfg["dist"]) +
+                "; each rank regenerates its row shard; paper_0809_2407_b200.synth)")
+    return "synthetic iid " + cfg["dist"] + " (torch Philox on device, seed = rank)"
+
+
 def run_grid(args, cfg, ws, rank, local):
     """C5 on a 2 x (N/2) process grid (Algorithm 3, paper_0809_2407_b200.grid):
     block-cyclic 128 x 128 blocks, one rank per GPU, NCCL row / column groups.
@@ -275,7 +343,7 @@ def run_grid(args, cfg, ws, rank, local):
     Pr = 2 if ws % 2 == 0 else 1  # C5: 2 x 4 at 8 GPUs
     Pc = ws // Pr
     grid = make_grid(BlockCyclicLayout(m, n, b, Pr, Pc))
-    A = make_input(cfg, dev)
+    A = make_input(cfg, dev, data=args.data)
     base = scatter_local(A, grid)
     del A
     be = GpuBackend(leaf_rows=cfg["leaf"])
@@ -340,7 +408,7 @@ def run_grid(args, cfg, ws, rank, local):
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic iid " + cfg["dist"] + " (torch Philox on device, same seed on every rank)",
+            "data": data_note(cfg, args),
             "config": {"workload": cfg["name"] + f", {Pr}x{Pc} grid", "m": m, "n": n, "b": b,
                        "leaf_rows": cfg["leaf"], "parallelism": f"2-D block-cyclic {Pr}x{Pc}",
                        "l2": "inputs larger than L2 (no flush needed)",
@@ -382,7 +450,8 @@ def run_ours(args, cfg):
     from paper_0809_2407_b200.dist import shard_rows, tsqr_sharded
 
     lo, hi = shard_rows(m, ws, rank)
-    A = make_input(cfg, dev, seed=rank, rows=hi - lo) if not is_caqr else make_input(cfg, dev)
+    A = (make_input(cfg, dev, lo, hi, data=args.data, seed=rank) if not is_caqr
+         else make_input(cfg, dev, data=args.data))
     P = _leaves_for(hi - lo, n, cfg["leaf"])
     from paper_0809_2407_b200.tsqr import split_leaves
 
@@ -392,17 +461,20 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
 
     leaf_ev = []
+    last = {}
 
     def step(record=False):
         if is_caqr:
             from paper_0809_2407_b200.caqr import caqr_factor
 
-            return caqr_factor(A, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+            last["f"] = caqr_factor(A, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+            return last["f"]
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         f = factor_device(A, P, want_q=want_q)
+        last["f"] = f
         if record:
             e1.record(stream)
             leaf_ev.append((e0, e1))
@@ -480,13 +552,38 @@ def run_ours(args, cfg):
     ms = float(ms_t.item())
     F = flops(m, n)
     value = F / (ms * 1e-3) / 1e9
+    # parity of the timed computation's R against the reference's R on the same input
+    R_timed = None
+    if graph is not None:
+        R_timed = holder["f"].R_out()
+    elif is_caqr:
+        R_timed = last["f"].R if last else None
+    elif last:
+        f_last = last["f"]
+        if ws > 1:
+            from paper_0809_2407_b200.dist import cross_tree, gpu_combine
+
+            R_timed, _ = cross_tree(f_last.R, gpu_combine)
+        else:
+            R_timed = f_last.R_out()
+    parity = parity_vs_reference(cfg, R_timed) if (rank == 0 and args.data == "reference") else None
+    del R_timed
 
     # roofline of the dominant kernel: the leaf factorization (factor_device's
     # leaf + tree events bracket; the tree is < 2% of it, see profiles/)
     roof = None
     caqr_launches = None
     if is_caqr:
-        roof, caqr_launches = caqr_roofline(A, cfg, args)
+        detail, caqr_launches = caqr_roofline(A, cfg, args)
+        ach = F / (ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "the whole CAQR step (panel TSQRs, leaf- and tree-level trailing updates, "
+                          "two-stream lookahead): F = 2mn^2 - 2n^3/3 over ms_per_step",
+                "peak_source": detail["peak_source"], "algorithmic_flops_per_launch": F,
+                "detail_panel0_trailing_update": {k: detail[k] for k in
+                                                  ("kernel", "achieved", "frac", "launch_ms",
+                                                   "algorithmic_flops_per_launch")}}
     if leaf_ev:
         # the timed bracket: one factor_device call (or the graph replay of the
         # step, which for explicit-Q configs also forms Q: 2x the flops)
@@ -505,10 +602,12 @@ def run_ours(args, cfg):
             # HBM-bound (C4, AI = n/4 flop/B < the 5.7 ridge): bytes of A per launch
             ach = 8.0 * (hi - lo) * n / t_leaf / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": 8.0 * (hi - lo) * n * 1.0011 if narrow else None,
-                    "traffic_source": "ncu --set full of k_leaf_narrow (profiles/r01/"
-                                      "narrow_kernel_ncu_summary.txt): 1.0011 x 8mn, scaled per launch",
-                    "kernel": "k_leaf_narrow (cp.async stages) + fused ticket tree (one factor_device call)",
+                    "traffic": 8.0 * (hi - lo) * n * NARROW8_TRAFFIC if narrow else None,
+                    "traffic_source": "ncu --set full of k_leaf_narrow8 (profiles/r02/"
+                                      "narrow8_kernel_ncu_summary.txt): dram read + write = "
+                                      f"{NARROW8_TRAFFIC:.4f} x 8mn, scaled per launch",
+                    "kernel": "k_leaf_narrow8 (8 rows per reflector chain) + fused ticket tree "
+                              "(one factor_device call)",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "algorithmic_bytes_per_launch": 8.0 * (hi - lo) * n}
         else:
@@ -517,7 +616,7 @@ def run_ours(args, cfg):
             # (profiles/r01/dmma_kernel_ncu_summary.txt: 1.2432e9 B read + 4.1e6 B
             # written for 148 leaves of 8192 x 128 = 1.0047x the 8mn algorithmic
             # bytes), scaled to this launch's rows; None for other widths.
-            traffic = 8.0 * (hi - lo) * n * 1.0047 if (n == 128 and cfg["q"] == "none") else None
+            traffic = 8.0 * (hi - lo) * n * DMMA_TRAFFIC if (n == 128 and cfg["q"] == "none") else None
             kern = ("k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)"
                     if cfg["q"] == "none" else
                     ("k_leaf_dense + k_leaf_dmma<64> + k_tree_factor_dmma, then Q: k_tree_apply_dmma + "
@@ -607,12 +706,12 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic iid " + cfg["dist"] + " (torch Philox on device, seed = rank)",
+            "data": data_note(cfg, args),
             "config": {"workload": cfg["name"], "m": m, "n": n, "leaf_rows": cfg["leaf"],
                        "leaves_per_gpu": P // chains, "gpu_chains_per_leaf": chains, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
                        "l2": "inputs larger than L2 (no flush needed)" if 8 * m * n > 256e6
                        else "inputs smaller than L2"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "clocks": clk.summary(), "gpu_launches": launches,
             "cuda_graph": graph is not None,
             "gflops_roofline_frac": value / (FP64_PEAK_TFLOPS * 1e3 * ws),
@@ -636,6 +735,8 @@ def main():
                     help="replay each TSQR step as one captured CUDA graph (1 GPU, not CAQR)")
     ap.add_argument("--grid", action="store_true",
                     help="c5: run the Pr x Pc grid driver even on one GPU (1 x 1 grid)")
+    ap.add_argument("--data", default="reference", choices=["reference", "torch"],
+                    help="inputs: the reference's generators bit for bit (default) or torch Philox")
     ap.add_argument("--panel-chains", type=int, default=4,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()

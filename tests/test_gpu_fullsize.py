@@ -1,8 +1,8 @@
 """Full-size, same-seed parity of C1-C5 against the reference itself.
 
 Every config's input is regenerated on the GPU box bit for bit from the
-reference generators (``oracle.fullsize``; SHA-256 checked against the
-fixture) and factored by the CUDA path.  The fixtures in
+reference generators (``paper_0809_2407_b200.synth``, the bench's generator;
+SHA-256 checked against the fixture) and factored by the CUDA path.  The fixtures in
 ``tests/golden/fullsize_*.npz`` come from ``oracle/make_fullsize.py``, which
 ran the read-only reference kernels composed as Algorithm 1 (C1-C4) or the
 reference's ``qr_blocked`` (C5), plus LAPACK, in the build container.
@@ -54,12 +54,9 @@ def device_input(cfg):
         pin[:t.numel()].copy_(t.reshape(-1))
         A[r0:r0 + blk.shape[0]].copy_(pin[:t.numel()].view(blk.shape), non_blocking=True)
 
-    if cfg in ("c1", "c2"):
-        for r0, blk in fullsize.chunks(cfg):
-            sink(r0, blk)
-    else:
-        st = np.load(os.path.join(GOLD, "fullsize_states.npz"))
-        fullsize.parallel_chunks(cfg, st[f"{cfg}_states"], sink)
+    from paper_0809_2407_b200 import synth
+
+    synth.chunks(cfg, sink=sink)
     torch.cuda.synchronize()
     want = str(_fix(cfg)["sha256"]) if cfg != "c5" else str(_fix("c5")["sha256"])
     assert sha.hexdigest() == want, f"{cfg}: regenerated input differs from the fixture's"

@@ -323,6 +323,7 @@ def test_tsqr_from_mat1_file_is_bitwise_the_in_memory_r(tmp_path, m, n, leaf, K)
     assert np.array_equal(Rk, factor_device(torch.from_numpy(A).cuda(), P).R.cpu().numpy())
 
 
+@pytest.mark.parametrize("v16", [True, False])
 def test_dmma_ring_leaf_parity(v16):
     """CAQR_TUNE_DMMA = 1 (default): R-only leaves with n in (64, 128] on the
     DMMA warp ring (16-row register tiles, 8-column Level-2 panels with
@@ -714,3 +715,51 @@ def test_dmma_dense_tile_matches_cta_sweep(m, n, P):
     R = f1.R.cpu().numpy()
     assert oracle.residual(A, Q1, R) <= 10 * n * EPS
     assert oracle.orthogonality(Q1) <= 10 * n * EPS
+
+
+def test_split_role_leaf_bitwise_equal_to_ring():
+    """CAQR_TUNE_CC = 2: the split-role ring (generation warps + update warps,
+    tiles in shared memory) runs the same arithmetic as the DMMA warp ring:
+    R bitwise equal, and within the R bar of LAPACK."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    try:
+        for (m, n, P) in [(4096, 128, 2), (20000, 100, 4), (3000, 72, 1), (9001, 128, 3)]:
+            A = torch.from_numpy(philox(m + 7 * n).standard_normal((m, n))).cuda()
+            _lib.tune(_lib.TUNE_CC, 2)
+            R2 = factor_device(A, P).R.cpu().numpy()
+            _lib.tune(_lib.TUNE_CC, 0)
+            R0 = factor_device(A, P).R.cpu().numpy()
+            assert np.array_equal(R2, R0)
+            assert oracle.r_diff(R2, np.linalg.qr(A.cpu().numpy(), mode="r"),
+                                 np.linalg.norm(A.cpu().numpy(), 2)) <= 1000 * EPS
+    finally:
+        _lib.reset_tuning()
+
+
+@pytest.mark.parametrize("m,P", [(16384 * 5, 5), (16384 * 3 + 333, 3), (300, 1), (256 * 7 + 1, 2)])
+def test_narrow8_parity_and_variants(m, P):
+    """CAQR_TUNE_NARROW = 3 (default for contiguous aligned n = 8): 8 rows per
+    reflector chain.  R against LAPACK and against the K = 4 kernels (2 / 1),
+    ragged last step and short leaves included; misaligned views fall back."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = philox(m).uniform(-1, 1, (m, 8))
+    At = torch.from_numpy(A).cuda()
+    Rl = np.linalg.qr(A, mode="r")
+    nrm = np.linalg.norm(A, 2)
+    try:
+        Rs = {}
+        for v in (3, 2, 1):
+            _lib.tune(_lib.TUNE_NARROW, v)
+            Rs[v] = factor_device(At, P).R.cpu().numpy()
+            assert oracle.r_diff(Rs[v], Rl, nrm) <= 1000 * EPS
+        _lib.tune(_lib.TUNE_NARROW, 3)
+        big = torch.zeros(m * 8 + 1, dtype=torch.float64, device="cuda")
+        view = big[1:].view(m, 8)  # 8-byte aligned only: the 8-byte path
+        view.copy_(At)
+        assert oracle.r_diff(factor_device(view, P).R.cpu().numpy(), Rl, nrm) <= 1000 * EPS
+    finally:
+        _lib.reset_tuning()

@@ -332,3 +332,26 @@ def test_stacked_flop_count_qary():
     for key, (flops, divs) in gold.items():
         n, q = map(int, key.split("x"))
         assert count_stacked(n, q) == (flops, divs), key
+
+
+def test_synth_regenerates_reference_bits():
+    """paper_0809_2407_b200.synth (the bench's input generator) redraws any row
+    range from the recorded Philox states bit for bit like a sequential pass of
+    the reference generator (core.rng_for), checked on slices of C3 and C4."""
+    from oracle import fullsize
+    from paper_0809_2407_b200 import synth
+
+    for cfg, lo, hi in [("c3", 5 * (1 << 20) - 3, 5 * (1 << 20) + 7), ("c4", 2 * (1 << 23) + 11, 2 * (1 << 23) + 40)]:
+        got = {}
+        synth.chunks(cfg, lo, hi, lambda r0, b: got.__setitem__(r0, b.copy()))
+        want = None
+        for r0, blk in fullsize.chunks(cfg):
+            if r0 + blk.shape[0] > lo:
+                if want is None:
+                    want = blk[lo - r0:]
+                else:
+                    want = np.vstack([want, blk])
+            if r0 + blk.shape[0] >= hi:
+                break
+        seq = np.vstack([got[k] for k in sorted(got)])
+        assert np.array_equal(seq, want[:hi - lo])
