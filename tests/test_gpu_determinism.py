@@ -1,0 +1,80 @@
+"""Run-to-run bitwise determinism of every kernel with a synchronisation
+protocol (same input, same R -- reduce and all-reduce).
+
+compute-sanitizer is closed on the GPU pool (profiles/r02/
+compute_sanitizer_closed.txt), so the warp-ring acquire/release protocols
+(dr_wait / dr_signal, the split-role ring's counters, the narrow kernels'
+ticket trees, CAQR's two-stream lookahead) are exercised here instead: every
+kernel family runs repeatedly at full occupancy (one wave of 148 leaves, plus
+odd shapes) and each result must be bitwise identical to the first -- a
+missed acquire or a torn read shows up as a run-to-run difference.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+REPS = 12
+
+
+def _same(fn):
+    first = [t.clone() for t in fn()]
+    for _ in range(REPS - 1):
+        out = fn()
+        for a, b in zip(first, out):
+            assert torch.equal(a, b)
+
+
+def _rand(seed, shape, uniform=False):
+    g = np.random.Generator(np.random.Philox(seed))
+    a = g.uniform(-1, 1, shape) if uniform else g.standard_normal(shape)
+    return torch.from_numpy(a).cuda()
+
+
+def test_tsqr_r_only_rings_deterministic():
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = _rand(1, (148 * 2048, 128))
+    B = _rand(2, (3001 * 3, 100))
+    try:
+        for cc in (0, 2):  # DMMA ring / split-role ring
+            _lib.tune(_lib.TUNE_CC, cc)
+            _same(lambda: [factor_device(A, 148).R, factor_device(B, 3).R])
+    finally:
+        _lib.reset_tuning()
+
+
+def test_tsqr_q_paths_deterministic():
+    from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
+
+    for (m, n, P) in [(148 * 1024, 64, 148), (65536, 32, 8), (40000, 128, 16)]:
+        A = _rand(m + n, (m, n))
+
+        def run():
+            f = factor_device(A, P, want_q=True)
+            return [f.R, explicit_q_device(f)]
+
+        _same(run)
+
+
+def test_narrow_ticket_trees_deterministic():
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = _rand(3, (8192 * 512, 8), uniform=True)
+    try:
+        for v in (3, 2):
+            _lib.tune(_lib.TUNE_NARROW, v)
+            _same(lambda: [factor_device(A, 512).R])
+    finally:
+        _lib.reset_tuning()
+
+
+def test_caqr_lookahead_deterministic():
+    from paper_0809_2407_b200.caqr import caqr_factor
+
+    A = _rand(4, (3072, 2048))
+    _same(lambda: [caqr_factor(A, b=128, leaf_rows=1024).R])
