@@ -15,8 +15,9 @@ local Q; Q^T C applies the local Q^T and then the cross tree bottom-up
 and back; forming Q explicitly skips the upward message (the partner's
 block is still zero on the way down).
 
-Transport: ``torch.distributed`` point-to-point (NCCL over NVLink on GPUs,
-gloo on CPU for the host-logic tests).  ``combine`` and ``local`` are
+Transport: ``torch.distributed`` point-to-point (NCCL over NVLink on GPUs;
+gloo, with device tensors staged through host memory, for the host-logic
+tests and for several ranks sharing one GPU).  ``combine`` and ``local`` are
 injectable so the host logic is testable without a GPU.
 """
 
@@ -26,6 +27,39 @@ import torch
 import torch.distributed as dist
 
 from .trees import ReductionTree
+
+
+# ---------------------------------------------------------------------------
+# transport: NCCL moves device tensors directly; gloo (the host-logic tests,
+# and several ranks sharing one GPU) stages device tensors through host memory
+# ---------------------------------------------------------------------------
+def _staged(t: torch.Tensor, group) -> bool:
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def send(t: torch.Tensor, group=None, group_dst=None, dst=None) -> None:
+    x = t.cpu() if _staged(t, group) else t
+    if group_dst is not None:
+        dist.send(x, group=group, group_dst=group_dst)
+    else:
+        dist.send(x, dst=dst, group=group)
+
+
+def recv(t: torch.Tensor, group=None, group_src=None, src=None) -> None:
+    x = torch.empty(t.shape, dtype=t.dtype) if _staged(t, group) else t
+    if group_src is not None:
+        dist.recv(x, group=group, group_src=group_src)
+    else:
+        dist.recv(x, src=src, group=group)
+    if x is not t:
+        t.copy_(x)
+
+
+def broadcast(t: torch.Tensor, group=None, group_src=None) -> None:
+    x = t.cpu() if _staged(t, group) else t
+    dist.broadcast(x, group=group, group_src=group_src)
+    if x is not t:
+        t.copy_(x)
 
 
 def pack_upper(R: torch.Tensor) -> torch.Tensor:
@@ -77,12 +111,12 @@ def cross_tree(R_local: torch.Tensor, combine, group=None, all_reduce: bool = Fa
     for lvl, grp in enumerate(tree.levels, start=1):
         for (a, b) in grp:
             if v == b:
-                dist.send(pack_upper(R), group=group, group_dst=mem[a])
+                send(pack_upper(R), group=group, group_dst=mem[a])
                 if recorder is not None:
                     recorder.record_send(words)
             elif v == a:
                 buf = torch.empty(words, dtype=R.dtype, device=R.device)
-                dist.recv(buf, group=group, group_src=mem[b])
+                recv(buf, group=group, group_src=mem[b])
                 if recorder is not None:
                     recorder.record_recv(words, stage=(lvl, "R"))
                 R, node = combine(R, unpack_upper(buf, n))
@@ -93,7 +127,7 @@ def cross_tree(R_local: torch.Tensor, combine, group=None, all_reduce: bool = Fa
         if len(mem) != dist.get_world_size(group):
             raise ValueError("all-reduce mode needs every rank of the group")
         buf = pack_upper(R) if is_root else torch.empty(words, dtype=R.dtype, device=R.device)
-        dist.broadcast(buf, group=group, group_src=mem[tree.root])
+        broadcast(buf, group=group, group_src=mem[tree.root])
         R = unpack_upper(buf, n)
         return R, nodes
     return (R if is_root else None), nodes
@@ -122,11 +156,11 @@ def cross_apply(nodes, C_top: torch.Tensor, apply_node, transpose: bool = False,
         for (a, b) in grp:
             if v == b:
                 if not skip_up:
-                    dist.send(C, group=group, group_dst=mem[a])
+                    send(C, group=group, group_dst=mem[a])
                     if recorder is not None:
                         recorder.record_send(words)
                 buf = torch.empty_like(C)
-                dist.recv(buf, group=group, group_src=mem[a])
+                recv(buf, group=group, group_src=mem[a])
                 if recorder is not None:
                     recorder.record_recv(words, stage=(lvl, "Q"))
                 C = buf
@@ -135,12 +169,12 @@ def cross_apply(nodes, C_top: torch.Tensor, apply_node, transpose: bool = False,
                     Cb = torch.zeros_like(C)
                 else:
                     Cb = torch.empty_like(C)
-                    dist.recv(Cb, group=group, group_src=mem[b])
+                    recv(Cb, group=group, group_src=mem[b])
                     if recorder is not None:
                         recorder.record_recv(words, stage=(lvl, "Q"))
                 C, Cb = apply_node(node_of[(lvl, b)], C, Cb, transpose)
                 C = C.contiguous()
-                dist.send(Cb.contiguous(), group=group, group_dst=mem[b])
+                send(Cb.contiguous(), group=group, group_dst=mem[b])
                 if recorder is not None:
                     recorder.record_send(words)
     return C

@@ -34,7 +34,7 @@ import torch
 import torch.distributed as dist
 
 from .core import BlockCyclicLayout, BlockRowLayout, DimensionError
-from .dist import cross_apply, cross_tree
+from .dist import broadcast, cross_apply, cross_tree, recv, send
 from .trees import BINARY, ReductionTree
 
 
@@ -246,7 +246,7 @@ def caqr_grid(local: torch.Tensor, grid: GridInfo, backend, recorder=None) -> Gr
                 ts = [torch.empty(s, dtype=torch.float64, device=dev)
                       for s in backend.shapes(m_r, b, keys)]
             for t in ts:
-                dist.broadcast(t, group=grid.row_group, group_src=cj)
+                broadcast(t, group=grid.row_group, group_src=cj)
                 res.broadcast_words += t.numel() if grid.c == cj else 0
             if grid.c != cj:
                 f, nodes = backend.unpack(ts, m_r, b, keys)
@@ -282,7 +282,7 @@ def gather_R(res: GridCaqrResult):
     if rank != 0:
         mine = res.local[:rows_of(grid.r), :cols_of(grid.c)].contiguous()
         if mine.numel():
-            dist.send(mine, dst=0)
+            send(mine, dst=0)
         return None
     R = torch.zeros((L.n, L.n), dtype=torch.float64, device=res.local.device)
     for src in range(world):
@@ -294,7 +294,7 @@ def gather_R(res: GridCaqrResult):
             blk = res.local[:shape[0], :shape[1]]
         else:
             blk = torch.empty(shape, dtype=torch.float64, device=res.local.device)
-            dist.recv(blk, src=src)
+            recv(blk, src=src)
         for li in range(shape[0] // b):
             i = r + li * L.Pr
             for lj in range(shape[1] // b):
