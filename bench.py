@@ -352,7 +352,7 @@ def run_grid(args, cfg, ws, rank, local):
 
     def step():
         work.copy_(base)
-        return caqr_grid(work, grid, be)
+        return caqr_grid(work, grid, be, lookahead=args.grid_lookahead)
 
     for _ in range(args.warmup):
         step()
@@ -737,6 +737,7 @@ def main():
                     help="c5: run the Pr x Pc grid driver even on one GPU (1 x 1 grid)")
     ap.add_argument("--data", default="reference", choices=["reference", "torch"],
                     help="inputs: the reference's generators bit for bit (default) or torch Philox")
+    ap.add_argument("--grid-lookahead", action="store_true", help="c5 grid: two-stream lookahead")
     ap.add_argument("--panel-chains", type=int, default=4,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()

@@ -140,6 +140,12 @@ int tsqr_f64_geqr2(double* A, int64_t lda, int64_t m, int64_t n, double* tau, in
 int tsqr_f64_form_t(const double* G, int64_t ldg, int64_t n, const double* tau, double* T,
                     int64_t ldt, void* stream);
 
+/* Unblocked Cholesky of the Gram G = A^T A in place (upper triangle -> R with
+ * G = R^T R) for the CholeskyQR competitor of the stability sweep
+ * (SPEC.md:409-415); *info (device int) = j + 1 at the first nonpositive
+ * pivot j, 0 on success. */
+int tsqr_f64_cholesky(double* G, int64_t ldg, int64_t n, int* info, void* stream);
+
 /* Q C / Q^T C for a single-block factor of tsqr_f64_block_factor: mode 0 =
  * DENSE (C has rows rows), mode 2 = TRIRECT (C = [Ctop (n rows, ldt); C
  * (rows rows)]); rows <= 128. */

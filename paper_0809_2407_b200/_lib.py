@@ -31,6 +31,7 @@ SYMBOLS = (
     "tsqr_f64_block_apply",
     "tsqr_f64_geqr2",
     "tsqr_f64_form_t",
+    "tsqr_f64_cholesky",
     "caqr_tune",
     "caqr_f64_peak_probe",
 )
@@ -80,6 +81,8 @@ def _sig(lib):
     lib.tsqr_f64_geqr2.argtypes = [dp, i64, i64, i64, dp, ip, vp]
     lib.tsqr_f64_form_t.restype = i32
     lib.tsqr_f64_form_t.argtypes = [dp, i64, i64, dp, dp, i64, vp]
+    lib.tsqr_f64_cholesky.restype = i32
+    lib.tsqr_f64_cholesky.argtypes = [dp, i64, i64, ip, vp]
     lib.caqr_tune.restype = i32
     lib.caqr_tune.argtypes = [i32, i32]
     lib.caqr_f64_peak_probe.restype = i32

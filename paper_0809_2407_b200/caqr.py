@@ -76,7 +76,7 @@ def _panel_leaves(mj: int, w: int, leaf_rows: int) -> int:
 
 def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_rows: int = 2048,
                 device=None, counter=None, lookahead: bool = True,
-                panel_chains: int = 4) -> CaqrResult:
+                panel_chains: int = 4, apply_waves: float = 4.0) -> CaqrResult:
     """CAQR of A (m x n, m >= n) with panel width b <= 128.
 
     With ``lookahead`` (default) the panels run on a high-priority stream:
@@ -87,6 +87,12 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
     factor then only needs a few SMs' worth of work to hide behind the
     trailing update; ``panel_chains`` splits each panel leaf into that many
     ring chains (a deeper binary tree, see tsqr.split_leaves).
+
+    ``apply_waves``: the trailing update runs one CTA per (panel leaf, 128
+    trailing columns); as the trailing matrix shrinks, a panel's leaves are
+    split (more, shorter leaves: the same binary-tree TSQR with more events)
+    until its update fills that many waves of the SMs, so the late panels do
+    not run on a handful of SMs.  0 keeps ``leaf_rows`` leaves throughout.
     """
     lib = _lib.load()
     if layout is not None:
@@ -103,6 +109,7 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         raise DimensionError("layout does not match A")
     W = At.clone() if not host else At
     dev = W.device
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     starts = list(range(0, n, b))
     nb = len(starts)
@@ -120,6 +127,10 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         P = _panel_leaves(mj, w, leaf_rows)
         while panel_chains > 1 and P < panel_chains and mj // (2 * P) >= max(256, 2 * w):
             P *= 2  # split leaves into GPU chains (hybrid tree, see tsqr.split_leaves)
+        if apply_waves > 0 and c1 < n:
+            want = apply_waves * sms / max(1, -(-(n - c1) // 128))
+            while P < want and mj // (2 * P) >= max(256, 2 * w):
+                P *= 2
         lay = BlockRowLayout(mj, w, P)
         _, h0, ht = _lib.geometry(w)
         tiles = _tiles_per_leaf(lay, h0, ht)

@@ -107,3 +107,38 @@ k_form_t(const double* __restrict__ G, int64_t ldg, int n, const double* __restr
     __syncthreads();
   }
 }
+
+// Unblocked Cholesky G = R^T R (upper R, in place in the upper triangle) for
+// CholeskyQR ("our own unblocked kernel with failure
+// detection at nonpositive pivots").  One CTA; info = j + 1 for the first
+// pivot j that is not positive (the factorization stops there), 0 on success.
+__global__ void __launch_bounds__(1024, 1)
+k_cholesky(double* __restrict__ G, int64_t ldg, int n, int* info) {
+  __shared__ double piv;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = G[(int64_t)j * ldg + j];
+      if (!(d > 0.0)) {  // nonpositive or NaN pivot
+        bad = j + 1;
+      } else {
+        piv = sqrt(d);
+        G[(int64_t)j * ldg + j] = piv;
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    const double inv = 1.0 / piv;
+    for (int c = j + 1 + threadIdx.x; c < n; c += blockDim.x) G[(int64_t)j * ldg + c] *= inv;
+    __syncthreads();
+    // trailing update of the upper triangle: G[r][c] -= R[j][r] R[j][c], j < r <= c
+    for (int64_t idx = threadIdx.x; idx < (int64_t)(n - j - 1) * (n - j - 1); idx += blockDim.x) {
+      const int r = j + 1 + (int)(idx / (n - j - 1)), c = j + 1 + (int)(idx % (n - j - 1));
+      if (c >= r) G[(int64_t)r * ldg + c] -= G[(int64_t)j * ldg + r] * G[(int64_t)j * ldg + c];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *info = bad;
+}

@@ -1684,6 +1684,13 @@ int tsqr_f64_form_t(const double* G, int64_t ldg, int64_t n, const double* tau, 
   return check_launch("k_form_t");
 }
 
+int tsqr_f64_cholesky(double* G, int64_t ldg, int64_t n, int* info, void* stream) {
+  if (!G || !info || n < 1 || n > INT32_MAX || ldg < n)
+    return set_err(CAQR_ERR_ARG, "tsqr_f64_cholesky: bad arguments");
+  k_cholesky<<<1, 1024, 0, (cudaStream_t)stream>>>(G, ldg, (int)n, info);
+  return check_launch("k_cholesky");
+}
+
 int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;

@@ -241,9 +241,10 @@ def _tree_apply(f: TsqrFactor, C: torch.Tensor, slot_rows: int, transpose: bool,
         return
     st = _stream(C.device)
     order = f.levels if transpose else list(reversed(f.levels))
+    ldc = C.stride(0) if C.dim() == 2 and C.stride(1) == 1 else C.shape[1]
     for ev in order:
         _lib.check(lib.tsqr_f64_tree_apply_level(_ptr(f.node_Y), _ptr(f.node_tau), f.n, _ptr(ev),
-                                                 ev.shape[0], _ptr(C), C.shape[1], slot_rows,
+                                                 ev.shape[0], _ptr(C), ldc, slot_rows,
                                                  C.shape[1], int(transpose), int(zero_partner), st),
                    "tsqr_f64_tree_apply_level")
 
@@ -253,8 +254,9 @@ def _leaf_apply(f: TsqrFactor, C: torch.Tensor, transpose: bool, S=None, zero_in
     lib = _lib.load()
     st = _stream(C.device)
     k = C.shape[1]
+    ldc = C.stride(0) if C.stride(1) == 1 else k  # strided column slices apply in place
     _lib.check(lib.tsqr_f64_leaf_apply(_ptr(f.Y), f.n, _ptr(f.tau), f.tau.shape[1] * f.n, f.m,
-                                       f.n, f.P, _ptr(C), k, k, _ptr(S), k,
+                                       f.n, f.P, _ptr(C), ldc, k, _ptr(S), k,
                                        f.n if S is not None else 0, int(transpose),
                                        int(zero_init), int(tri_skip), st),
                "tsqr_f64_leaf_apply")
@@ -271,6 +273,18 @@ def explicit_q_device(f: TsqrFactor) -> torch.Tensor:
     Q = torch.empty((f.m, n), dtype=torch.float64, device=dev)
     _leaf_apply(f, Q, transpose=False, S=S.view(f.P * n, n), zero_init=True, tri_skip=True)
     return Q
+
+
+def apply_qt_inplace(f: TsqrFactor, C: torch.Tensor) -> None:
+    """C := Q^T C in place; C (m x k) may be a column slice of a row-major
+    matrix (unit column stride, any row stride): no copy of the trailing
+    matrix (the CAQR grid's leaf-level update)."""
+    if not f.has_q:
+        raise ValueError("factor was computed without implicit Q (want_q=False)")
+    if C.shape[0] != f.m or C.stride(1) != 1:
+        raise DimensionError("C must have the factor's rows and unit column stride")
+    _leaf_apply(f, C, transpose=True)
+    _tree_apply(f, C, slot_rows=f.layout.base, transpose=True, zero_partner=False)
 
 
 def apply_q_device(f: TsqrFactor, C: torch.Tensor, transpose: bool) -> torch.Tensor:
@@ -451,10 +465,22 @@ def tsqr_parallel(executor, blocks, tree: ReductionTree | None = None, want_q: b
 
 def tsqr_explicit_q(factor: TsqrFactor):
     """Thin Q (m x n) with orthonormal columns."""
+    from .sequential import SequentialTsqrFactor
+
+    if isinstance(factor, SequentialTsqrFactor):
+        return factor.explicit_q()
     return _out(explicit_q_device(factor), factor.host)
 
 
 def tsqr_apply_q(factor: TsqrFactor, C, transpose: bool = False):
     """Q C (C with n or m rows) or Q^T C (C with m rows)."""
+    from .sequential import SequentialTsqrFactor
+
+    if isinstance(factor, SequentialTsqrFactor):
+        return factor.apply_q(C, transpose)
     Ct, host = to_device(C, factor.R.device, name="C")
     return _out(apply_q_device(factor, Ct, transpose), host or factor.host)
+
+
+# SPEC module tsqr also holds the sequential flat-tree driver (SPEC.md:270-294)
+from .sequential import BlockStore, SequentialTsqrFactor, choose_P_sequential, tsqr_sequential  # noqa: E402,F401

@@ -355,3 +355,31 @@ def test_synth_regenerates_reference_bits():
                 break
         seq = np.vstack([got[k] for k in sorted(got)])
         assert np.array_equal(seq, want[:hi - lo])
+
+
+def test_choose_P_sequential_spec_examples():
+    """smallest P with mn/P + n(n+1)/2 <= W."""
+    from paper_0809_2407_b200.sequential import choose_P_sequential
+
+    assert choose_P_sequential(10 ** 6, 50, 10 ** 6) == 51
+    assert choose_P_sequential(100, 5, 10_000) == 1
+    with pytest.raises(ValueError, match="too large for fast memory"):
+        choose_P_sequential(1000, 50, 1000)
+
+
+def test_block_store_layout_and_counters(tmp_path):
+    """BlockStore on disk: meta.json + A_k.mat in MAT1, counted reads."""
+    import json
+
+    from paper_0809_2407_b200.matio import read_mat1
+    from paper_0809_2407_b200.sequential import BlockStore
+
+    A = np.random.Generator(np.random.Philox(5)).standard_normal((103, 6))
+    st = BlockStore.from_matrix(A, 4, directory=str(tmp_path / "store"))
+    meta = json.load(open(tmp_path / "store" / "meta.json"))
+    assert meta == {"m": 103, "n": 6, "P": 4, "block_rows": [25, 25, 25, 28]}
+    assert np.array_equal(read_mat1(tmp_path / "store" / "A_3.mat"), A[75:])
+    again = BlockStore(str(tmp_path / "store"))
+    assert np.array_equal(again.read_block(1), A[25:50])
+    assert again.counters() == {"blocks_read": 1, "blocks_written": 0, "words_read": 150,
+                                "words_written": 0}
