@@ -717,23 +717,32 @@ def test_dmma_dense_tile_matches_cta_sweep(m, n, P):
     assert oracle.orthogonality(Q1) <= 10 * n * EPS
 
 
-def test_split_role_leaf_bitwise_equal_to_ring():
-    """CAQR_TUNE_CC = 2: the split-role ring (generation warps + update warps,
-    tiles in shared memory) runs the same arithmetic as the DMMA warp ring:
-    R bitwise equal, and within the R bar of LAPACK."""
+@pytest.mark.parametrize("cc", [4, 3, 2])
+def test_split_role_leaves_bitwise_equal_to_ring(cc):
+    """CAQR_TUNE_CC = 4 / 3 (default 4): the split-role ring with 16 / 12 tiles in
+    tensor memory; 2: with 8 tiles in shared memory.  All run the DMMA warp
+    ring's arithmetic (generation warps + update warps): R bitwise equal to
+    CAQR_TUNE_CC = 0, and within the R bar of LAPACK.  Shapes cover ragged
+    leaves, n < 128 (dead padded blocks), more and fewer tiles than slots."""
     from paper_0809_2407_b200 import _lib
     from paper_0809_2407_b200.tsqr import factor_device
 
     try:
-        for (m, n, P) in [(4096, 128, 2), (20000, 100, 4), (3000, 72, 1), (9001, 128, 3)]:
+        for (m, n, P) in [(4096, 128, 2), (20000, 100, 4), (3000, 72, 1), (9001, 128, 3),
+                          (148 * 512 + 77, 120, 148), (100, 65, 1)]:
             A = torch.from_numpy(philox(m + 7 * n).standard_normal((m, n))).cuda()
-            _lib.tune(_lib.TUNE_CC, 2)
-            R2 = factor_device(A, P).R.cpu().numpy()
+            _lib.tune(_lib.TUNE_CC, cc)
+            Rc = factor_device(A, P).R.cpu().numpy()
             _lib.tune(_lib.TUNE_CC, 0)
             R0 = factor_device(A, P).R.cpu().numpy()
-            assert np.array_equal(R2, R0)
-            assert oracle.r_diff(R2, np.linalg.qr(A.cpu().numpy(), mode="r"),
+            assert np.array_equal(Rc, R0)
+            assert oracle.r_diff(Rc, np.linalg.qr(A.cpu().numpy(), mode="r"),
                                  np.linalg.norm(A.cpu().numpy(), 2)) <= 1000 * EPS
+        A = philox(7).standard_normal((5000, 96))
+        A[4321, 50] = np.nan
+        _lib.tune(_lib.TUNE_CC, cc)
+        with pytest.raises(ValueError):
+            factor_device(torch.from_numpy(A).cuda(), 2)
     finally:
         _lib.reset_tuning()
 

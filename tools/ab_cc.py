@@ -37,19 +37,19 @@ for (m, n, P) in [(148 * 8192, 128, 148), (1 << 24, 128, 2048), (148 * 8192, 96,
     g = torch.Generator(device="cuda").manual_seed(1)
     A = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
     out = {}
-    for cc in (2, 0):
+    for cc in (4, 3, 0):
         _lib.tune(_lib.TUNE_CC, cc)
         ms = timed(lambda: factor_device(A, P, check=False))
         out[cc] = (ms, factor_device(A, P).R_out().clone())
     flops = 2 * m * n * n - 2 * n ** 3 / 3
     nrm = float(torch.linalg.matrix_norm(out[0][1], 2))
     line = f"m={m} n={n} P={P}:"
-    for cc, name in ((2, "split"), (0, "ring")):
+    for cc, name in ((4, "tmem16"), (3, "tmem12"), (0, "ring")):
         d = float(torch.max(torch.abs(sn(out[cc][1]) - sn(out[0][1])))) / nrm / EPS
         line += f"  {name} {out[cc][0]:.3f} ms ({flops / out[cc][0] / 1e9:.2f} TF/s, dR {d:.2f})"
     print(line, flush=True)
     if m <= 1 << 21:
         Rl = torch.as_tensor(np.linalg.qr(A.cpu().numpy(), mode="r"), device="cuda")
-        d2 = float(torch.max(torch.abs(sn(out[2][1]) - sn(Rl)))) / float(torch.linalg.matrix_norm(Rl, 2)) / EPS
-        print(f"   |R_split - R_lapack| = {d2:.2f} eps*|A|_2", flush=True)
+        d2 = float(torch.max(torch.abs(sn(out[4][1]) - sn(Rl)))) / float(torch.linalg.matrix_norm(Rl, 2)) / EPS
+        print(f"   |R_tmem16 - R_lapack| = {d2:.2f} eps*|A|_2", flush=True)
 _lib.reset_tuning()
