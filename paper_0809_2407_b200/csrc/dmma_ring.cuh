@@ -168,18 +168,17 @@ __device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow,
 #pragma unroll
   for (int k = 0; k < 4; ++k) xi[k] = __shfl_sync(FULL, x[k], src);
   const double x0 = __shfl_sync(FULL, rgi, 4 * I);
-  double s = xi[0] * xi[0], s2 = xi[2] * xi[2];
-  s = fma(xi[1], xi[1], s);
-  s2 = fma(xi[3], xi[3], s2);
+  // p_g = x_I . x_g over the tile; the norm sigma = p_I is the owner column's
+  // own dot product (the same products in the same order as a separate sum of
+  // squares, so bitwise the same), fetched with one shuffle: 7 FP64
+  // instructions fewer per generation on the pipe the DMMAs share
   double pd = xi[0] * x[0], pd2 = xi[2] * x[2];
   pd = fma(xi[1], x[1], pd);
   pd2 = fma(xi[3], x[3], pd2);
-  s += s2;
   pd += pd2;
-  s += __shfl_xor_sync(FULL, s, 1);
   pd += __shfl_xor_sync(FULL, pd, 1);
-  s += __shfl_xor_sync(FULL, s, 2);
   pd += __shfl_xor_sync(FULL, pd, 2);
+  const double s = __shfl_sync(FULL, pd, 4 * I);
   double beta, tau, scale, invb;
   house_fast(x0, s, beta, tau, scale, invb);
   const double tw = fma(scale, pd, rgi);  // R[i][g] + v^T x_g

@@ -26,6 +26,9 @@
 // Included by tsqr_sm100.cu (namespace tsqr), after split_leaf.cuh.
 
 constexpr int TM_U = 8;  // update warps (2 per sub-partition)
+#ifndef TM_GEN
+#define TM_GEN dr_gen_nx
+#endif
 template <int TM_G>      // generation warps = tiles in flight: 12 or 16 (TMEM holds 16)
 struct TmCfg {
   static constexpr int THREADS = (TM_G + TM_U) * 32;
@@ -37,7 +40,8 @@ struct TmSmem {  // offsets in doubles, then ints
   static constexpr int YS = R + dr_pbase<128>(16);  // [slot][2 parities][16 x 8] Y_p
   static constexpr int TB = YS + TM_G * 2 * 128;     // [slot][2 parities][32][2] T
   static constexpr int GS = TB + TM_G * 2 * 64;      // [slot][72] G, tau
-  static constexpr int doubles = GS + TM_G * 72;
+  static constexpr int STG = GS + TM_G * 72;         // [slot][16 x 8] next tile's block p
+  static constexpr int doubles = STG + TM_G * 128;
   static constexpr int NCNT = 3 * 16 + 2 * TM_G + 4;
   static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * NCNT;
 };
@@ -77,6 +81,12 @@ __device__ __forceinline__ void tm_ld(double (&x)[4], uint32_t taddr) {
   tm_ld_issue(r, taddr);
   tm_ld_wait();
   tm_unpack(x, r);
+}
+
+template <int I>
+__device__ __forceinline__ void dr_gen_nx(double (&x)[4], double rgi, double* Rrow, double* gs,
+                                          double* taus) {
+  dr_gen<I, false>(x, rgi, Rrow, gs, taus);
 }
 
 // Y_p of a slot in shared memory, natural 16 x 8 layout: the B operand of
@@ -138,6 +148,8 @@ k_leaf_tm(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
     double* gs = sm + TmSmem::GS + s * 72;
     double* taus = gs + 64;
     double2* tbs = reinterpret_cast<double2*>(sm + TmSmem::TB + s * 128);
+    double* stg = sm + TmSmem::STG + s * 128;
+    const bool v16 = ((lda & 1) == 0) && ((n & 1) == 0) && (((uintptr_t)A & 15) == 0);
     auto prefetch = [&](int t) {
       if (t >= T) return;
       const int64_t row = r0 + (int64_t)t * SP_H;
@@ -153,13 +165,16 @@ k_leaf_tm(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
     SP_TICK(k0_);
     for (int t = s; t < T; t += TM_G, ++lt) {
       SP_TICK(l0_);
-      // tile t: block 0 into registers, blocks 1.. into the slot's TMEM columns
-      // (from L2: prefetched one tile ahead).  Loading the next tile's blocks
-      // from the update warps as they die measured slower (52.8 vs 48.4 ms).
+      // tile t: block 0 into registers, blocks 1.. into the slot's TMEM columns.
+      // The slot's first tile is loaded here; every later tile was staged
+      // block by block during the previous tile (panel p moves block p, dead by
+      // then, through shared memory by cp.async), so only block 0 is read back.
+      // Loading the next tile from the update warps measured slower (52.8 ms).
       const int64_t row0 = r0 + (int64_t)t * SP_H;
       double x[4];
+      if (lt > 0) tm_ld(x, taddr(s, 0));
 #pragma unroll 1
-      for (int blk = 0; blk < 16; ++blk) {
+      for (int blk = 0; blk < (lt > 0 ? 0 : 16); ++blk) {
         double v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -179,26 +194,59 @@ k_leaf_tm(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
       prefetch(t + TM_G);
       SP_TICK(l1_);
       SP_ADD(6, l0_, l1_);
+      const bool more = t + TM_G < T;
+      const int64_t nrow0 = r0 + (int64_t)(t + TM_G) * SP_H;
+      const int nvalid = more ? (int)min64(SP_H, r0 + b - nrow0) : 0;
       for (int p = 0; p < npan; ++p) {
         const int job = lt * 16 + p;
         const int ldr = dr_ldr<128>(p);
         double* Rpan = Rp + dr_pbase<128>(p);
         double rg[8];
+        if (more) {  // next tile's block p -> shared stage (lands during this panel)
+          const unsigned sb = (unsigned)__cvta_generic_to_shared(stg);
+          if (v16) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int x2 = lane + 32 * i, r = x2 >> 2, c2 = x2 & 3;
+              const bool ok = r < nvalid && 8 * p + 2 * c2 < n;
+              cp_async<16>(sb + 8u * (unsigned)(r * 8 + 2 * c2),
+                           ok ? A + (nrow0 + r) * lda + 8 * p + 2 * c2 : A, ok ? 16u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int x1 = lane + 32 * i, r = x1 >> 3, c = x1 & 7;
+              const bool ok = r < nvalid && 8 * p + c < n;
+              cp_async<8>(sb + 8u * (unsigned)(r * 8 + c), ok ? A + (nrow0 + r) * lda + 8 * p + c : A,
+                          ok ? 8u : 0u);
+            }
+          }
+          cp_async_commit();
+        }
         SP_TICK(a0_);
         dr_wait(ver_pp + p, t, lane);
         SP_TICK(a1_);
         SP_ADD(0, a0_, a1_);
 #pragma unroll
         for (int i = 0; i < 8; ++i) rg[i] = Rpan[i * ldr + g];
-        dr_gen<0, false>(x, rg[0], Rpan, gs, taus);
-        dr_gen<1, false>(x, rg[1], Rpan + ldr, gs, taus);
-        dr_gen<2, false>(x, rg[2], Rpan + 2 * ldr, gs, taus);
-        dr_gen<3, false>(x, rg[3], Rpan + 3 * ldr, gs, taus);
-        dr_gen<4, false>(x, rg[4], Rpan + 4 * ldr, gs, taus);
-        dr_gen<5, false>(x, rg[5], Rpan + 5 * ldr, gs, taus);
-        dr_gen<6, false>(x, rg[6], Rpan + 6 * ldr, gs, taus);
-        dr_gen<7, false>(x, rg[7], Rpan + 7 * ldr, gs, taus);
+        TM_GEN<0>(x, rg[0], Rpan, gs, taus);
+        TM_GEN<1>(x, rg[1], Rpan + ldr, gs, taus);
+        TM_GEN<2>(x, rg[2], Rpan + 2 * ldr, gs, taus);
+        TM_GEN<3>(x, rg[3], Rpan + 3 * ldr, gs, taus);
+        TM_GEN<4>(x, rg[4], Rpan + 4 * ldr, gs, taus);
+        TM_GEN<5>(x, rg[5], Rpan + 5 * ldr, gs, taus);
+        TM_GEN<6>(x, rg[6], Rpan + 6 * ldr, gs, taus);
+        TM_GEN<7>(x, rg[7], Rpan + 7 * ldr, gs, taus);
         dr_signal(ver_pp + p, t + 1, lane);
+        if (more) {  // TMEM block p is dead (read by the hand-off of panel p-1): stage it
+          cp_async_wait<0>();
+          __syncwarp();
+          double v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] = stg[(8 * (k >> 1) + 2 * q + (k & 1)) * 8 + g];
+          __syncwarp();
+          tm_st(taddr(s, p), v);
+        }
         SP_TICK(a2_);
         SP_ADD(1, a1_, a2_);
         if (p + 1 >= npan) break;
