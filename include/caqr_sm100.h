@@ -199,8 +199,9 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * tensor cores; parity-tested but slower: one warp per panel serialises the tall tile);
  * 0 (default) = the CTA sweep k_leaf_dense. */
 #define CAQR_TUNE_DMMA_DENSE 14
-/* CAQR_TUNE_CC: R-only leaves with n in (64, 128]: 4 (default) = the split-role ring with
- * 16 tiles in flight held in tensor memory (k_leaf_tm<16>), 3 = the same with 12 tiles,
+/* CAQR_TUNE_CC: R-only leaves with n in (64, 128]: 5 (default) = the split-role ring with
+ * 4 tall tiles of 64 rows held in tensor memory (k_leaf_tt<64, 1>), 6 = 8 tiles of 32 rows,
+ * 4 = 16 tiles of 16 rows in tensor memory (k_leaf_tm<16>), 3 = the same with 12 tiles,
  * 2 = the split-role ring with 8 tiles in shared memory, 0 = the DMMA warp ring. */
 #define CAQR_TUNE_CC 15
 int caqr_tune(int key, int value);

@@ -148,7 +148,7 @@ TUNE_CC = 15
 TUNE_DEFAULTS = {TUNE_CHAIN_HT[32]: 16, TUNE_CHAIN_HT[64]: 16, TUNE_CHAIN_HT[128]: 16,
                  TUNE_NARROW: 3, TUNE_ZSTART: 1, TUNE_DMMA: 2,
                  TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1, TUNE_DMMA_TREE: 1,
-                 TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 4}
+                 TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 5}
 
 
 def tune(key: int, value: int) -> None:

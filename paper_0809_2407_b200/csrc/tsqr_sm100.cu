@@ -63,8 +63,9 @@ static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
-static int g_cc = 4;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 4 / 3 split-role ring with 16 / 12
-                              // tiles in TMEM, 2 split-role ring (smem tiles), 0 DMMA warp ring
+static int g_cc = 5;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 5 / 6 split-role ring with 4 / 8 tall
+                              // tiles (64 / 32 rows) in TMEM, 4 / 3 with 16 / 12 tiles of 16 rows in TMEM,
+                              // 2 split-role ring (smem tiles), 0 DMMA warp ring
 static int np_index(int p) { return p == 32 ? 0 : (p == 64 ? 1 : 2); }
 
 template <int NP>
@@ -1158,6 +1159,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 #include "dmma_apply.cuh"
 #include "split_leaf.cuh"
 #include "tm_leaf.cuh"
+#include "tm_tall.cuh"
 #include "dense_geqr2.cuh"
 
 // ===========================================================================
@@ -1303,7 +1305,17 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
       k_leaf_dense<NPV><<<grid, THREADS, DenseSmem<NPV>::bytes, st>>>(A, lda, m, (int)n,        \
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
-    if (NPV == 128 && zs && g_cc == 3) {                                                        \
+    if (NPV == 128 && zs && g_cc == 5) {                                                        \
+      rc = prep(k_leaf_tt<64, 1>, TtSmem<64>::bytes);                                           \
+      if (rc) return rc;                                                                        \
+      k_leaf_tt<64, 1><<<grid, TtCfg<64, 1>::THREADS, TtSmem<64>::bytes, st>>>(A, lda, m,       \
+          (int)n, (int)P, base, R, flag);                                                       \
+    } else if (NPV == 128 && zs && g_cc == 6) {                                                 \
+      rc = prep(k_leaf_tt<32, 1>, TtSmem<32>::bytes);                                           \
+      if (rc) return rc;                                                                        \
+      k_leaf_tt<32, 1><<<grid, TtCfg<32, 1>::THREADS, TtSmem<32>::bytes, st>>>(A, lda, m,       \
+          (int)n, (int)P, base, R, flag);                                                       \
+    } else if (NPV == 128 && zs && g_cc == 3) {                                                 \
       rc = prep(k_leaf_tm<12>, TmSmem<12>::bytes);                                              \
       if (rc) return rc;                                                                        \
       k_leaf_tm<12><<<grid, TmCfg<12>::THREADS, TmSmem<12>::bytes, st>>>(A, lda, m, (int)n,     \
@@ -1746,7 +1758,7 @@ int caqr_tune(int key, int value) {
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_CC) {
-    if (value != 0 && (value < 2 || value > 4)) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_CC takes 0, 2, 3 or 4");
+    if (value != 0 && (value < 2 || value > 6)) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_CC takes 0 or 2..6");
     g_cc = value;
     return CAQR_OK;
   }

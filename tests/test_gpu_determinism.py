@@ -40,7 +40,7 @@ def test_tsqr_r_only_rings_deterministic():
     A = _rand(1, (148 * 2048, 128))
     B = _rand(2, (3001 * 3, 100))
     try:
-        for cc in (4, 3, 2, 0):  # TMEM split-role rings / smem split-role ring / DMMA ring
+        for cc in (5, 6, 4, 3, 2, 0):  # tall-tile and 16-row TMEM split-role rings / smem split-role ring / DMMA ring
             _lib.tune(_lib.TUNE_CC, cc)
             _same(lambda: [factor_device(A, 148).R, factor_device(B, 3).R])
     finally:

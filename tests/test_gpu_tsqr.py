@@ -747,6 +747,45 @@ def test_split_role_leaves_bitwise_equal_to_ring(cc):
         _lib.reset_tuning()
 
 
+@pytest.mark.parametrize("cc", [5, 6])
+def test_tall_tile_leaves_match_ring_and_lapack(cc):
+    """CAQR_TUNE_CC = 5 (default) / 6: the split-role ring with 4 tiles of 64 rows /
+    8 tiles of 32 rows in tensor memory (k_leaf_tt).  Same Householder chain with
+    taller rectangles per step (qr_triangle_on_rect, householder.py:297-332), so R
+    agrees with the 16-row ring to rounding (not bitwise) and with LAPACK within the
+    R bar; run-to-run bitwise.  Shapes cover ragged leaves and last tiles, n < 128,
+    more and fewer tiles than slots, an ill-conditioned input and the NaN flag."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    try:
+        for (m, n, P) in [(4096, 128, 2), (20000, 100, 4), (3000, 72, 1), (9001, 128, 3),
+                          (148 * 512 + 77, 120, 148), (100, 65, 1), (129, 128, 1), (200, 128, 1)]:
+            A = torch.from_numpy(philox(m + 7 * n).standard_normal((m, n))).cuda()
+            _lib.tune(_lib.TUNE_CC, cc)
+            Rc = factor_device(A, P).R.cpu().numpy()
+            assert np.array_equal(Rc, factor_device(A, P).R.cpu().numpy())
+            _lib.tune(_lib.TUNE_CC, 0)
+            R0 = factor_device(A, P).R.cpu().numpy()
+            nrm = np.linalg.norm(A.cpu().numpy(), 2)
+            assert oracle.r_diff(Rc, R0, nrm) <= 50 * EPS
+            assert oracle.r_diff(Rc, np.linalg.qr(A.cpu().numpy(), mode="r"), nrm) <= 1000 * EPS
+        # kappa = 1e10: R^T R = A^T A to working accuracy (backward stability of the chain)
+        rng = philox(99)
+        U, _ = np.linalg.qr(rng.standard_normal((6000, 96)))
+        V, _ = np.linalg.qr(rng.standard_normal((96, 96)))
+        A = (U * np.logspace(0, -10, 96)) @ V.T
+        _lib.tune(_lib.TUNE_CC, cc)
+        R = factor_device(torch.from_numpy(A).cuda(), 3).R.cpu().numpy()
+        assert np.linalg.norm(R.T @ R - A.T @ A) <= 100 * 96 * EPS * np.linalg.norm(A, 2) ** 2
+        A = philox(7).standard_normal((5000, 96))
+        A[4321, 50] = np.nan
+        with pytest.raises(ValueError):
+            factor_device(torch.from_numpy(A).cuda(), 2)
+    finally:
+        _lib.reset_tuning()
+
+
 @pytest.mark.parametrize("m,P", [(16384 * 5, 5), (16384 * 3 + 333, 3), (300, 1), (256 * 7 + 1, 2)])
 def test_narrow8_parity_and_variants(m, P):
     """CAQR_TUNE_NARROW = 3 (default for contiguous aligned n = 8): 8 rows per
