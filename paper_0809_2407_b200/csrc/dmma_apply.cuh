@@ -322,7 +322,9 @@ __global__ void __launch_bounds__(THREADS, MB)
 k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
               int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
               int64_t ncols, const double* __restrict__ S, int64_t lds, int64_t s_slot_rows,
-              int zero_init) {
+              int zero_init, int dense_only) {
+  // dense_only: the leaf's chain tiles are not in this kernel's 16-row format (tall tiles:
+  // k_tall_apply runs them before / after this launch); only the dense first tile is applied
   using SMQ = DmmaQSmem<NP, KB>;
   constexpr int HD = Geo<NP>::HD, H0 = WARPS * HD, RG = HD / 16, CB = KB / 8, LDC = SMQ::LDC;
   extern __shared__ __align__(16) double sm[];
@@ -343,7 +345,7 @@ k_leaf_q_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restric
   double* Cl = C + r0 * ldc + col0;
   const double* Sl = S ? S + (int64_t)leaf * s_slot_rows * lds + col0 : nullptr;
   const int64_t rest = b - H0;
-  const int T = rest > 0 ? (int)((rest + DR_H - 1) / DR_H) : 0;
+  const int T = (rest > 0 && !dense_only) ? (int)((rest + DR_H - 1) / DR_H) : 0;
   const int npan = (n + 7) >> 3;
   for (int idx = threadIdx.x; idx < NP * KB; idx += THREADS) {
     const int r = idx / KB, c = idx - r * KB;

@@ -112,7 +112,7 @@ __device__ __forceinline__ void tt_st(uint32_t taddr, const double (&x)[K]) {
 // column x_I reaches the other column groups through xs (the caller alternates
 // two buffers: the warp barrier of generation I+1 separates the reads of
 // generation I from the writes of generation I+2).
-template <int I, int K>
+template <int I, int K, bool EXACT>
 __device__ __forceinline__ void tt_gen(double (&x)[K], double* Rrow, double* gs, double* taus,
                                        double* xs) {
   const int lane = threadIdx.x & 31;
@@ -146,9 +146,10 @@ __device__ __forceinline__ void tt_gen(double (&x)[K], double* Rrow, double* gs,
   const double tw = fma(scale, pd, rgi);  // R[I][g] + v^T x_g
   const double wv = tau * tw;
   const bool upd = g > I, own = (g == I);
-  const double f = upd ? tw * invb : (own ? scale - 1.0 : 0.0);
+  // kept factors (EXACT): the owner column becomes v = fma(scale, x_I, 0), one rounding (dr_gen)
+  const double f = upd ? tw * invb : (own ? (EXACT ? scale : scale - 1.0) : 0.0);
 #pragma unroll
-  for (int k = 0; k < K; ++k) x[k] = fma(f, xi[k], x[k]);
+  for (int k = 0; k < K; ++k) x[k] = fma(f, xi[k], (EXACT && own) ? 0.0 : x[k]);
   double* dst = upd ? Rrow + g : (own ? Rrow + I : gs + g * 8 + I);
   *dst = upd ? rgi - wv : (own ? beta : scale * pd);
   taus[I] = tau;
@@ -216,10 +217,15 @@ __device__ __forceinline__ void tt_upd(double (&c)[NBLK][K], const double (&y)[K
 }
 
 
-template <int H, int UWN>
+// Q = false: R only, the chain starts from R = 0 at the leaf's first row (h0 = 0).
+// Q = true: the chain continues from the leaf's R slot after a dense first tile of h0 rows
+// (k_leaf_dense) and keeps every tile's TRI_ON_RECT factor: Y rows h0 + H t.., tau at
+// (t + 1) * n, the layout of k_leaf_dmma with H-row tiles.  Y may alias A (a tile's rows
+// are on chip before its first panel is stored).
+template <int H, int UWN, bool Q>
 __global__ void __launch_bounds__(TtCfg<H, UWN>::THREADS, 1)
 k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
-          double* Rio, int* flag) {
+          double* Rio, int* flag, double* Y, int64_t ldy, double* tau, int64_t tau_stride, int h0) {
   using Cfg = TtCfg<H, UWN>;
   using Sm = TtSmem<H>;
   constexpr int G = Cfg::G, K = Cfg::K, UW = Cfg::UW, THREADS = Cfg::THREADS;
@@ -235,11 +241,24 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
-  const int64_t r0 = (int64_t)leaf * base;
-  const int64_t b = (leaf == P - 1) ? m - r0 : base;
+  const int64_t bl = (leaf == P - 1) ? m - (int64_t)leaf * base : base;
+  if (bl - h0 <= 0) return;  // the dense tile was the whole leaf: R is already in its slot
+  const int64_t r0 = (int64_t)leaf * base + h0, b = bl - h0;  // the chain's rows
   const int T = (int)((b + H - 1) / H);
   const int npan = (n + 7) >> 3;
-  for (int i = threadIdx.x; i < Sm::YN; i += THREADS) Rp[i] = 0.0;  // R only: R = 0
+  double* Rl0 = Rio + (int64_t)leaf * n * n;
+  for (int i = threadIdx.x; i < Sm::YN; i += THREADS) {
+    double v = 0.0;
+    if (Q) {  // panel-packed index -> (r, c)
+      int pp = 0;
+      while (pp + 1 < 16 && dr_pbase<128>(pp + 1) <= i) ++pp;
+      const int off = i - dr_pbase<128>(pp), ld = dr_ldr<128>(pp);
+      const int r = 8 * pp + off / ld, c = 8 * pp + off % ld;
+      if (r < n && c < n && c >= r) v = Rl0[r * n + c];
+    }
+    Rp[i] = v;
+  }
+  double* tl = Q ? tau + (int64_t)leaf * tau_stride : nullptr;
   for (int i = threadIdx.x; i < 4 * 16 + 2 * G; i += THREADS) cnt[i] = 0;
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
@@ -339,17 +358,26 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         dr_wait(ver_pp + p, t, lane);
         SP_TICK(a1_);
         SP_ADD(0, a0_, a1_);
-        tt_gen<0, K>(x, Rpan, gs, taus, xs);
-        tt_gen<1, K>(x, Rpan + ldr, gs, taus, xs + H);
-        tt_gen<2, K>(x, Rpan + 2 * ldr, gs, taus, xs);
-        tt_gen<3, K>(x, Rpan + 3 * ldr, gs, taus, xs + H);
-        tt_gen<4, K>(x, Rpan + 4 * ldr, gs, taus, xs);
-        tt_gen<5, K>(x, Rpan + 5 * ldr, gs, taus, xs + H);
-        tt_gen<6, K>(x, Rpan + 6 * ldr, gs, taus, xs);
-        tt_gen<7, K>(x, Rpan + 7 * ldr, gs, taus, xs + H);
+        tt_gen<0, K, Q>(x, Rpan, gs, taus, xs);
+        tt_gen<1, K, Q>(x, Rpan + ldr, gs, taus, xs + H);
+        tt_gen<2, K, Q>(x, Rpan + 2 * ldr, gs, taus, xs);
+        tt_gen<3, K, Q>(x, Rpan + 3 * ldr, gs, taus, xs + H);
+        tt_gen<4, K, Q>(x, Rpan + 4 * ldr, gs, taus, xs);
+        tt_gen<5, K, Q>(x, Rpan + 5 * ldr, gs, taus, xs + H);
+        tt_gen<6, K, Q>(x, Rpan + 6 * ldr, gs, taus, xs);
+        tt_gen<7, K, Q>(x, Rpan + 7 * ldr, gs, taus, xs + H);
         SP_TICK(g1_);
         SP_ADD(11, a1_, g1_);
         dr_signal(ver_pp + p, t + 1, lane);
+        if (Q) {  // the tile's factor for panel p: Y (= x) and tau
+          const int c = 8 * p + g;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int64_t row = row0 + erow(k);
+            if (row < r0 + b && c < n) Y[row * ldy + c] = x[k];
+          }
+          if (lane < 8 && 8 * p + lane < n) tl[(int64_t)(t + 1) * n + 8 * p + lane] = taus[lane];
+        }
         auto stage_move = [&]() {
           if (more) {  // TMEM block p is dead (read at the hand-off of panel p-1): stage the next tile's
             cp_async_wait<0>();

@@ -63,6 +63,7 @@ static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
+static int g_fuse = 148;      // CAQR_TUNE_FUSE: R-only n in (64,128]: CTAs (one per SM) that chain consecutive leaves; 0 off
 static int g_cc = 5;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 5 / 6 split-role ring with 4 / 8 tall
                               // tiles (64 / 32 rows) in TMEM, 4 / 3 with 16 / 12 tiles of 16 rows in TMEM,
                               // 2 split-role ring (smem tiles), 0 DMMA warp ring
@@ -1160,6 +1161,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 #include "split_leaf.cuh"
 #include "tm_leaf.cuh"
 #include "tm_tall.cuh"
+#include "tall_apply.cuh"
 #include "dense_geqr2.cuh"
 
 // ===========================================================================
@@ -1265,7 +1267,8 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
     return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor: bad arguments");
   if ((Y == nullptr) != (tau == nullptr)) return set_err(CAQR_ERR_ARG, "Y and tau go together");
   if (base < n) return set_err(CAQR_ERR_ARG, "leaf shorter than n");
-  if (m - (P - 1) * base < base) return set_err(CAQR_ERR_ARG, "last leaf shorter than base");
+  // (R only: the last leaf may be a shorter run of fused leaves, r_binary_impl)
+  if (m - (P - 1) * base < (Y ? base : n)) return set_err(CAQR_ERR_ARG, "last leaf shorter than base");
   if (tau && tau_stride < min_tau_stride(m, n, P, base))
     return set_err(CAQR_ERR_ARG, "tau_stride below the leaf's tiles * n");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1306,15 +1309,15 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
           (int)P, base, Y, ldy, tau, tau_stride, R, flag);                                      \
     }                                                                                           \
     if (NPV == 128 && zs && g_cc == 5) {                                                        \
-      rc = prep(k_leaf_tt<64, 1>, TtSmem<64>::bytes);                                           \
+      rc = prep(k_leaf_tt<64, 1, false>, TtSmem<64>::bytes);                                    \
       if (rc) return rc;                                                                        \
-      k_leaf_tt<64, 1><<<grid, TtCfg<64, 1>::THREADS, TtSmem<64>::bytes, st>>>(A, lda, m,       \
-          (int)n, (int)P, base, R, flag);                                                       \
+      k_leaf_tt<64, 1, false><<<grid, TtCfg<64, 1>::THREADS, TtSmem<64>::bytes, st>>>(A, lda,   \
+          m, (int)n, (int)P, base, R, flag, nullptr, 0, nullptr, 0, 0);                         \
     } else if (NPV == 128 && zs && g_cc == 6) {                                                 \
-      rc = prep(k_leaf_tt<32, 1>, TtSmem<32>::bytes);                                           \
+      rc = prep(k_leaf_tt<32, 1, false>, TtSmem<32>::bytes);                                    \
       if (rc) return rc;                                                                        \
-      k_leaf_tt<32, 1><<<grid, TtCfg<32, 1>::THREADS, TtSmem<32>::bytes, st>>>(A, lda, m,       \
-          (int)n, (int)P, base, R, flag);                                                       \
+      k_leaf_tt<32, 1, false><<<grid, TtCfg<32, 1>::THREADS, TtSmem<32>::bytes, st>>>(A, lda,   \
+          m, (int)n, (int)P, base, R, flag, nullptr, 0, nullptr, 0, 0);                         \
     } else if (NPV == 128 && zs && g_cc == 3) {                                                 \
       rc = prep(k_leaf_tm<12>, TmSmem<12>::bytes);                                              \
       if (rc) return rc;                                                                        \
@@ -1338,6 +1341,11 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
         k_leaf_split<false><<<grid, SP_THREADS, SpSmem::bytes, st>>>(A, lda, m, (int)n, (int)P, \
                                                                      base, R, flag);            \
       }                                                                                         \
+    } else if (NPV == 128 && !zs && Y && g_ht[2] == 64) {                                       \
+      rc = prep(k_leaf_tt<64, 1, true>, TtSmem<64>::bytes);                                     \
+      if (rc) return rc;                                                                        \
+      k_leaf_tt<64, 1, true><<<grid, TtCfg<64, 1>::THREADS, TtSmem<64>::bytes, st>>>(A, lda,    \
+          m, (int)n, (int)P, base, R, flag, Y, ldy, tau, tau_stride, WARPS * Geo<128>::HD);     \
     } else if ((NPV == 128 && g_dmma && (zs || g_ht[2] == 16)) ||                             \
         (NPV == 64 && g_dmma >= 2 && (zs || g_ht[1] == 16)) ||                                  \
         (NPV == 32 && g_dmma >= 3 && (zs || g_ht[0] == 16))) {                                  \
@@ -1382,6 +1390,17 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
     if (P > 1 && cudaMemsetAsync(tickets, 0, sizeof(int) * (size_t)levels * P, st) != cudaSuccess)
       return check_launch("cudaMemsetAsync");
     return launch_narrow(A, lda, m, n, P, base, Rslots, flag, P > 1 ? tickets : nullptr, st);
+  }
+  // R only, more leaves than SMs: every CTA keeps folding the next leaf into the same R (the
+  // flat tree of Alg. 2 across the g consecutive leaves of one CTA, the binary tree above it --
+  // the hybrid tree of PAPER.md Fig. 3), instead of writing 2048 R factors and combining them
+  // in tree levels that are several waves wide (C3: 2.1 -> 0.8 ms of tree).  Leaves stay whole.
+  if (g_fuse && p == 128 && g_zstart && P > 2 * g_fuse) {
+    const int64_t g = (P + g_fuse - 1) / g_fuse;
+    P = (P + g - 1) / g;
+    base *= g;
+    levels = 0;
+    while ((1LL << levels) < P) ++levels;
   }
   int rc = leaf_factor_impl(A, lda, m, n, P, base, nullptr, 0, nullptr, 0, Rslots, flag, stream);
   if (rc) return rc;
@@ -1573,6 +1592,43 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
     if (g_ht[np_index(NPV)] == HA) LA_LAUNCH(NPV, KB_, HA) else LA_LAUNCH(NPV, KB_, HB)           \
     break;                                                                                        \
   }
+  if (p == 128 && g_ht[2] == 64) {
+    // tall chain tiles (k_leaf_tt<64, 1, true>): the dense first tile through k_leaf_q_dmma
+    // (dense_only), the chain tiles through k_tall_apply; Q^T: dense then chain, Q: chain then
+    // dense, both through the leaf's top n rows of C
+    const int h0 = WARPS * Geo<128>::HD;
+    auto dense = [&](bool tr, int zi) -> int {
+      const size_t smq = DmmaQSmem<128, 64>::bytes;
+      dim3 gq((unsigned)P, (unsigned)((ncols + 63) / 64));
+      if (tr) {
+        int rc = prep(k_leaf_q_dmma<128, 64, 1, true>, smq); if (rc) return rc;
+        k_leaf_q_dmma<128, 64, 1, true><<<gq, THREADS, smq, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
+            (int)P, base, C, ldc, ncols, nullptr, 0, 0, zi, 1);
+      } else {
+        int rc = prep(k_leaf_q_dmma<128, 64, 1, false>, smq); if (rc) return rc;
+        k_leaf_q_dmma<128, 64, 1, false><<<gq, THREADS, smq, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
+            (int)P, base, C, ldc, ncols, nullptr, 0, 0, zi, 1);
+      }
+      return check_launch("k_leaf_q_dmma (dense tile)");
+    };
+#define TA_LAUNCH(TRV)                                                                            \
+    {                                                                                             \
+      const size_t sma = TallApplySmem::bytes;                                                    \
+      dim3 ga((unsigned)P, (unsigned)((ncols + TLA_KB - 1) / TLA_KB));                              \
+      int rc = prep(k_tall_apply<TRV>, sma); if (rc) return rc;                                   \
+      k_tall_apply<TRV><<<ga, TLA_W * 32, sma, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,   \
+          base, C, ldc, ncols, S, lds, s_slot_rows, zero_init, h0);                               \
+      rc = check_launch("k_tall_apply"); if (rc) return rc;                                       \
+    }
+    if (transpose) {
+      int rc = dense(true, 0); if (rc) return rc;
+      TA_LAUNCH(true)
+      return CAQR_OK;
+    }
+    TA_LAUNCH(false)
+    return dense(false, zero_init);
+#undef TA_LAUNCH
+  }
   const int var = transpose ? g_dmma_apply : g_dmma_q;
   const bool q16 = (p == 64 && g_ht[1] == 16) || (p == 128 && g_ht[2] == 16) ||
                    (p == 32 && g_ht[0] == 16);
@@ -1583,7 +1639,7 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
       dim3 gq((unsigned)P, (unsigned)((ncols + KBQ - 1) / KBQ));                                  \
       int rc = prep(k_leaf_q_dmma<NPV, KBQ, MB, TR>, sm); if (rc) return rc;                      \
       k_leaf_q_dmma<NPV, KBQ, MB, TR><<<gq, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m,         \
-          (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init);                   \
+          (int)n, (int)P, base, C, ldc, ncols, S, lds, s_slot_rows, zero_init, 0);                \
     }
     if (p == 32) {
       if (transpose) LQ_LAUNCH(32, 32, 2, true) else LQ_LAUNCH(32, 32, 2, false)
@@ -1719,7 +1775,7 @@ int caqr_tune(int key, int value) {
   if (key >= CAQR_TUNE_CHAIN_HT_32 && key <= CAQR_TUNE_CHAIN_HT_128) {
     const int i = key - CAQR_TUNE_CHAIN_HT_32;
     const int a = 16, b = i == 2 ? 24 : 32;
-    if (value != a && value != b && !(i == 1 && value == 24))
+    if (value != a && value != b && !(i == 1 && value == 24) && !(i == 2 && value == 64))
       return set_err(CAQR_ERR_ARG, "unsupported chain tile height");
     g_ht[i] = value;
     return CAQR_OK;
@@ -1755,6 +1811,11 @@ int caqr_tune(int key, int value) {
   if (key == CAQR_TUNE_DMMA) {
     if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0 .. 3");
     g_dmma = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_FUSE) {
+    if (value < 0) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_FUSE takes 0 (off) or a CTA count");
+    g_fuse = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_CC) {

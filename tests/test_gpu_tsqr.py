@@ -786,6 +786,29 @@ def test_tall_tile_leaves_match_ring_and_lapack(cc):
         _lib.reset_tuning()
 
 
+def test_fused_leaves_match_unfused_tree():
+    """CAQR_TUNE_FUSE (default 148): R-only TSQR with more than 2 x 148 leaves chains
+    ceil(P / 148) consecutive leaves per CTA (flat tree inside a CTA, binary tree above:
+    the hybrid tree of PAPER.md Fig. 3).  R agrees with the one-CTA-per-leaf binary tree
+    and with LAPACK within the R bar; a ragged last run of leaves is covered."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    try:
+        for (m, n, P) in [(600 * 256, 128, 600), (1000 * 130 + 77, 100, 1000), (297 * 128, 128, 297)]:
+            A = torch.from_numpy(philox(m).standard_normal((m, n))).cuda()
+            _lib.tune(_lib.TUNE_FUSE, 148)
+            Rf = factor_device(A, P).R.cpu().numpy()
+            assert np.array_equal(Rf, factor_device(A, P).R.cpu().numpy())
+            _lib.tune(_lib.TUNE_FUSE, 0)
+            R0 = factor_device(A, P).R.cpu().numpy()
+            nrm = np.linalg.norm(A.cpu().numpy(), 2)
+            assert oracle.r_diff(Rf, R0, nrm) <= 50 * EPS
+            assert oracle.r_diff(Rf, np.linalg.qr(A.cpu().numpy(), mode="r"), nrm) <= 1000 * EPS
+    finally:
+        _lib.reset_tuning()
+
+
 @pytest.mark.parametrize("m,P", [(16384 * 5, 5), (16384 * 3 + 333, 3), (300, 1), (256 * 7 + 1, 2)])
 def test_narrow8_parity_and_variants(m, P):
     """CAQR_TUNE_NARROW = 3 (default for contiguous aligned n = 8): 8 rows per

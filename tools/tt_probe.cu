@@ -16,8 +16,8 @@ using namespace tsqr;
 
 static std::vector<double> g_ref;
 
-template <typename KERN>
-void run(const char* name, KERN kern, int threads, size_t smem, double* A, double* R, int* flag, int P,
+template <typename KERN, typename LAUNCH>
+void run(const char* name, KERN kern, LAUNCH launch, size_t smem, double* A, double* R, int* flag, int P,
          int64_t b, int64_t n, int64_t m, double tiles_rows) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   float best = 1e30f;
@@ -32,7 +32,7 @@ void run(const char* name, KERN kern, int threads, size_t smem, double* A, doubl
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    kern<<<P, threads, smem>>>(A, n, m, (int)n, P, b, R, flag);
+    launch();
     cudaEventRecord(e1);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) break;
@@ -84,9 +84,18 @@ int main(int argc, char** argv) {
   cudaMalloc(&flag, 4);
   cudaMemcpy(A, h.data(), (size_t)m * n * 8, cudaMemcpyHostToDevice);
   printf("P=%d b=%lld n=%lld\n", P, (long long)b, (long long)n);
-  run("tm16 (H=16)", k_leaf_tm<16>, TmCfg<16>::THREADS, TmSmem<16>::bytes, A, R, flag, P, b, n, m, 16.0);
-  run("tt H=32 UW=1", k_leaf_tt<32, 1>, TtCfg<32, 1>::THREADS, TtSmem<32>::bytes, A, R, flag, P, b, n, m, 32.0);
-  run("tt H=64 UW=2", k_leaf_tt<64, 2>, TtCfg<64, 2>::THREADS, TtSmem<64>::bytes, A, R, flag, P, b, n, m, 64.0);
-  run("tt H=64 UW=1", k_leaf_tt<64, 1>, TtCfg<64, 1>::THREADS, TtSmem<64>::bytes, A, R, flag, P, b, n, m, 64.0);
+  run("tm16 (H=16)", k_leaf_tm<16>,
+      [&] { k_leaf_tm<16><<<P, TmCfg<16>::THREADS, TmSmem<16>::bytes>>>(A, n, m, (int)n, P, b, R, flag); },
+      TmSmem<16>::bytes, A, R, flag, P, b, n, m, 16.0);
+#define TT_RUN(NAME, H, UW)                                                                          \
+  run(NAME, k_leaf_tt<H, UW, false>,                                                                 \
+      [&] {                                                                                          \
+        k_leaf_tt<H, UW, false><<<P, TtCfg<H, UW>::THREADS, TtSmem<H>::bytes>>>(                     \
+            A, n, m, (int)n, P, b, R, flag, nullptr, 0, nullptr, 0, 0);                              \
+      },                                                                                             \
+      TtSmem<H>::bytes, A, R, flag, P, b, n, m, (double)H)
+  TT_RUN("tt H=32 UW=1", 32, 1);
+  TT_RUN("tt H=64 UW=2", 64, 2);
+  TT_RUN("tt H=64 UW=1", 64, 1);
   return 0;
 }
