@@ -34,7 +34,8 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22 (BASELINE.md section 2
 # DRAM bytes (read + write) over the 8mn algorithmic bytes, from this round's
 # ncu --set full captures (profiles/r02/*_ncu_summary.txt)
 NARROW8_TRAFFIC = (8.596103e9 + 10.115584e6) / (8.0 * 134217728 * 8)
-DMMA_TRAFFIC = 1.0047  # k_leaf_dmma, profiles/r01/dmma_kernel_ncu_summary.txt (kernel unchanged)
+# k_leaf_tt<64, 1, false> at C3 full size, profiles/r02/leaf_tt_kernel_ncu_summary.txt
+DMMA_TRAFFIC = (17.367186e9 + 6.626816e6) / (8.0 * 16777216 * 128)
 METRIC = "TSQR fp64 GFLOP/s & % of roofline"
 
 CONFIGS = {
@@ -613,11 +614,13 @@ def run_ours(args, cfg):
         else:
             ach = F_leaf / t_leaf / 1e12
             # DRAM traffic of the leaf kernel from the committed ncu capture
-            # (profiles/r01/dmma_kernel_ncu_summary.txt: 1.2432e9 B read + 4.1e6 B
-            # written for 148 leaves of 8192 x 128 = 1.0047x the 8mn algorithmic
-            # bytes), scaled to this launch's rows; None for other widths.
+            # (profiles/r02/leaf_tt_kernel_ncu_summary.txt: 17.367 GB read + 6.6 MB
+            # written at C3 full size = 1.0113x the 8mn algorithmic bytes), scaled
+            # to this launch's rows; None for other widths.
             traffic = 8.0 * (hi - lo) * n * DMMA_TRAFFIC if (n == 128 and cfg["q"] == "none") else None
-            kern = ("k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)"
+            kern = (("k_leaf_tt<64,1> (tall tiles in tensor memory, CTAs chaining consecutive leaves) + "
+                     "k_tree_ring (one factor_device call)" if n > 64 else
+                     "k_leaf_dmma (DMMA warp ring) + k_tree_ring (one factor_device call)")
                     if cfg["q"] == "none" else
                     ("k_leaf_dense + k_leaf_dmma<64> + k_tree_factor_dmma, then Q: k_tree_apply_dmma + "
                      "k_leaf_q_dmma<64> " if 32 < n <= 64 else
@@ -626,7 +629,7 @@ def run_ours(args, cfg):
                     "(graph replay of the step; credited with the factor and Q-formation flops)")
             roof = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
-                    "traffic_source": "ncu --set full, profiles/r01 (scaled per launch)",
+                    "traffic_source": "ncu --set full of k_leaf_tt at C3 full size, profiles/r02/leaf_tt_kernel_ncu_summary.txt (scaled per launch)",
                     "kernel": kern,
                     "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (BASELINE.md; no FP64 "
                                    "entry in MEASURED_PEAKS.json)",
