@@ -154,6 +154,15 @@ __device__ __forceinline__ void house_fast(double x0, double sigma, double& beta
   invb = z ? 0.0 : (pos ? neg_alu(y) : y);
 }
 
+// Sum over the four lanes (g, 0..3) of a column group, result in all four: one DMMA,
+// D[g][.] = sum_q A[g][q] * 1 (26 cycles), instead of two shuffle + add rounds (~72 cycles
+// on the reflector chain: tools/ttg_probe.cu, 596 -> 519 cycles per generation at 64 rows).
+__device__ __forceinline__ double dr_quad_sum(double v) {
+  double d0 = 0.0, d1 = 0.0;
+  dmma(d0, d1, v, 1.0);
+  return d0;
+}
+
 // One generation (reflector I of the panel) of the register Level-2, with
 // branch-free stores: every lane stores (the four lanes of a column group
 // write the same value to the same address), so the look-ahead block stays
@@ -176,8 +185,7 @@ __device__ __forceinline__ void dr_gen(double (&x)[4], double rgi, double* Rrow,
   pd = fma(xi[1], x[1], pd);
   pd2 = fma(xi[3], x[3], pd2);
   pd += pd2;
-  pd += __shfl_xor_sync(FULL, pd, 1);
-  pd += __shfl_xor_sync(FULL, pd, 2);
+  pd = dr_quad_sum(pd);
   const double s = __shfl_sync(FULL, pd, 4 * I);
   double beta, tau, scale, invb;
   house_fast(x0, s, beta, tau, scale, invb);

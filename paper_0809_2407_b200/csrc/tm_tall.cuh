@@ -138,8 +138,7 @@ __device__ __forceinline__ void tt_gen(double (&x)[K], double* Rrow, double* gs,
 #pragma unroll
   for (int k = 4; k < K; ++k) a[k & 3] = fma(xi[k], x[k], a[k & 3]);
   double pd = (a[0] + a[1]) + (a[2] + a[3]);
-  pd += __shfl_xor_sync(FULL, pd, 1);
-  pd += __shfl_xor_sync(FULL, pd, 2);
+  pd = dr_quad_sum(pd);
   const double s = __shfl_sync(FULL, pd, 4 * I);
   double beta, tau, scale, invb;
   house_fast(x0, s, beta, tau, scale, invb);

@@ -24,14 +24,14 @@ __global__ void __launch_bounds__(512, 1) k_g(long long* out, double* sink, int 
     long long t0 = clock64();
     for (int p = 0; p < panels; ++p) {
       double* gs = gsa[w];
-      tt_gen<0, K>(x, Rs[w], gs, gs + 64, xsa[w]);
-      tt_gen<1, K>(x, Rs[w] + 10, gs, gs + 64, xsa[w] + 4 * K);
-      tt_gen<2, K>(x, Rs[w] + 20, gs, gs + 64, xsa[w]);
-      tt_gen<3, K>(x, Rs[w] + 30, gs, gs + 64, xsa[w] + 4 * K);
-      tt_gen<4, K>(x, Rs[w] + 40, gs, gs + 64, xsa[w]);
-      tt_gen<5, K>(x, Rs[w] + 50, gs, gs + 64, xsa[w] + 4 * K);
-      tt_gen<6, K>(x, Rs[w] + 60, gs, gs + 64, xsa[w]);
-      tt_gen<7, K>(x, Rs[w] + 70, gs, gs + 64, xsa[w] + 4 * K);
+      tt_gen<0, K, false>(x, Rs[w], gs, gs + 64, xsa[w]);
+      tt_gen<1, K, false>(x, Rs[w] + 10, gs, gs + 64, xsa[w] + 4 * K);
+      tt_gen<2, K, false>(x, Rs[w] + 20, gs, gs + 64, xsa[w]);
+      tt_gen<3, K, false>(x, Rs[w] + 30, gs, gs + 64, xsa[w] + 4 * K);
+      tt_gen<4, K, false>(x, Rs[w] + 40, gs, gs + 64, xsa[w]);
+      tt_gen<5, K, false>(x, Rs[w] + 50, gs, gs + 64, xsa[w] + 4 * K);
+      tt_gen<6, K, false>(x, Rs[w] + 60, gs, gs + 64, xsa[w]);
+      tt_gen<7, K, false>(x, Rs[w] + 70, gs, gs + 64, xsa[w] + 4 * K);
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < K; ++k) x[k] = (((((lane + 7 * p) * 2654435761u) ^ (k * 40503u + 12345u + p)) * 2246822519u >> 8) & 0xffff) / 32768.0 - 1.0;
