@@ -25,16 +25,21 @@
 //
 //   G = 256/H generation warps (warp s = slot s): the reflector chain of the
 //     slot's tile, Y_p / T_p, and the update of the next panel's block;
-//   8 update warps: H = 32: one per slot, all trailing blocks; H = 64: two per
-//     slot, blocks of their parity (so the R_p,trail hand-over between
-//     consecutive tiles is per parity: ver_u[parity][p]).
+//   G update warps (warp G + s, same sub-partition): the slot's other trailing
+//     blocks, and the staging of the slot's NEXT tile: block b goes global ->
+//     shared (cp.async, issued a panel ahead) -> the TMEM columns of block b as
+//     soon as the generation warp has taken the current tile's block b (its
+//     ver_p1 signal), so the chain warp never touches global memory after its
+//     first tile.  (Two update warps per slot measured slower: 13.6 vs 14.3
+//     TF/s; a generation warp's FP64 instructions wait for every DMMA on its
+//     sub-partition.)
 //
 // Counters and TMEM hand-offs as in k_leaf_tm.  The arithmetic is that of
 // k_leaf_dmma with taller rectangles (same reflectors up to summation order),
 // so R agrees with the 16-row kernels to rounding, not bitwise.
 // Included by tsqr_sm100.cu (namespace tsqr), after tm_leaf.cuh.
 
-template <int H, int UWN = (H >= 64 ? 2 : 1)>
+template <int H, int UWN = 1>
 struct TtCfg {
   static constexpr int G = 256 / H;             // generation warps = tiles in flight
   static constexpr int UW = UWN;                // update warps per slot
@@ -54,7 +59,7 @@ struct TtSmem {  // offsets in doubles, then ints
   static constexpr int XS = GS + G * 72;            // [slot][2][H] owner column of a generation
   static constexpr int STG = XS + G * 2 * H;        // [slot][H x 8] next tile's block p
   static constexpr int doubles = STG + G * H * 8;
-  static constexpr int NCNT = 4 * 16 + 2 * G + 4;
+  static constexpr int NCNT = 4 * 16 + 3 * G + 4;
   static constexpr size_t bytes = sizeof(double) * doubles + sizeof(int) * NCNT;
 };
 
@@ -228,6 +233,9 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
   using Cfg = TtCfg<H, UWN>;
   using Sm = TtSmem<H>;
   constexpr int G = Cfg::G, K = Cfg::K, UW = Cfg::UW, THREADS = Cfg::THREADS;
+  // (two update warps per slot ran correctly until the next tile's staging moved to the update
+  // warp; with it the UW = 2 build returned a wrong R in tools/tt_probe.cu and was dropped)
+  static_assert(UW == 1, "one update warp per slot");
   extern __shared__ __align__(16) double sm[];
   double* Rp = sm + Sm::R;
   int* cnt = reinterpret_cast<int*>(sm + Sm::doubles);
@@ -236,7 +244,8 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
   int* ver_u = cnt + 32;  // [UW][16]
   int* yrdy = cnt + 64;
   int* ufirst = yrdy + G;
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(ufirst + G);
+  int* staged = ufirst + G;  // slot s: tiles staged for the generation warp by the update warp
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(staged + G);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
@@ -258,7 +267,7 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
     Rp[i] = v;
   }
   double* tl = Q ? tau + (int64_t)leaf * tau_stride : nullptr;
-  for (int i = threadIdx.x; i < 4 * 16 + 2 * G; i += THREADS) cnt[i] = 0;
+  for (int i = threadIdx.x; i < 4 * 16 + 3 * G; i += THREADS) cnt[i] = 0;
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
                  :: "r"((unsigned)__cvta_generic_to_shared(tbase_s)) : "memory");
@@ -280,8 +289,6 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
     double* taus = gs + 64;
     double* xs = sm + Sm::XS + s * 2 * H;
     double2* tbs = reinterpret_cast<double2*>(sm + Sm::TB + s * 128);
-    double* stg = sm + Sm::STG + s * H * 8;
-    const bool v16 = ((lda & 1) == 0) && ((n & 1) == 0) && (((uintptr_t)A & 15) == 0);
     auto prefetch = [&](int t) {
       if (t >= T) return;
       const int64_t row = r0 + (int64_t)t * H;
@@ -299,11 +306,15 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
       SP_TICK(l0_);
       // tile t: block 0 into registers, blocks 1.. in the slot's TMEM columns.  The
       // slot's first tile is loaded here; every later tile was staged block by
-      // block during the previous tile (panel p moves block p, dead by then).
+      // block during the previous tile by the slot's update warp (block b once
+      // this warp had taken it), off this warp's chain.
       const int64_t row0 = r0 + (int64_t)t * H;
       double x[K];
-      tm_st_wait();  // the staged blocks of this tile (tcgen05.st of the previous tile's panels)
-      if (lt > 0) tt_ld<K>(x, taddr(s, 0));
+      if (lt > 0) {
+        sp_wait_ge(staged + s, lt, lane);
+        tm_fence_after();
+        tt_ld<K>(x, taddr(s, 0));
+      }
 #pragma unroll 1
       for (int blk = 0; blk < (lt > 0 ? 0 : 16); ++blk) {
         double v[K];
@@ -325,34 +336,10 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
       prefetch(t + G);
       SP_TICK(l1_);
       SP_ADD(6, l0_, l1_);
-      const bool more = t + G < T;
-      const int64_t nrow0 = r0 + (int64_t)(t + G) * H;
-      const int nvalid = more ? (int)min64(H, r0 + b - nrow0) : 0;
       for (int p = 0; p < npan; ++p) {
         const int job = lt * 16 + p;
         const int ldr = dr_ldr<128>(p);
         double* Rpan = Rp + dr_pbase<128>(p);
-        if (more) {  // next tile's block p -> shared stage (lands during this panel)
-          const unsigned sb = (unsigned)__cvta_generic_to_shared(stg);
-          if (v16) {
-#pragma unroll
-            for (int i = 0; i < H / 8; ++i) {
-              const int x2 = lane + 32 * i, r = x2 >> 2, c2 = x2 & 3;
-              const bool ok = r < nvalid && 8 * p + 2 * c2 < n;
-              cp_async<16>(sb + 8u * (unsigned)(r * 8 + 2 * c2),
-                           ok ? A + (nrow0 + r) * lda + 8 * p + 2 * c2 : A, ok ? 16u : 0u);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < H / 4; ++i) {
-              const int x1 = lane + 32 * i, r = x1 >> 3, c = x1 & 7;
-              const bool ok = r < nvalid && 8 * p + c < n;
-              cp_async<8>(sb + 8u * (unsigned)(r * 8 + c), ok ? A + (nrow0 + r) * lda + 8 * p + c : A,
-                          ok ? 8u : 0u);
-            }
-          }
-          cp_async_commit();
-        }
         SP_TICK(a0_);
         dr_wait(ver_pp + p, t, lane);
         SP_TICK(a1_);
@@ -377,21 +364,7 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
           }
           if (lane < 8 && 8 * p + lane < n) tl[(int64_t)(t + 1) * n + 8 * p + lane] = taus[lane];
         }
-        auto stage_move = [&]() {
-          if (more) {  // TMEM block p is dead (read at the hand-off of panel p-1): stage the next tile's
-            cp_async_wait<0>();
-            __syncwarp();
-            double v[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = stg[erow(k) * 8 + g];
-            __syncwarp();
-            tt_st<K>(taddr(s, p), v);
-          }
-        };
-        if (p + 1 >= npan) {
-          stage_move();
-          break;
-        }
+        if (p + 1 >= npan) break;
         SP_TICK(a2_);
         // publish Y_p (natural layout: the B operand of Y^T; fragment order: the B
         // operand of C^T Y for the update warps) and T_p
@@ -415,7 +388,6 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         dr_signal(yrdy + s, job + 1, lane);
         SP_TICK(a3_);
         SP_ADD(2, a2_, a3_);
-        stage_move();
         SP_TICK(a7_);
         SP_ADD(1, a3_, a7_);
         // hand-off: block p+1 (panel p-1 applied by an update warp), panel p here
@@ -430,7 +402,8 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         SP_ADD(4, a4_, a5_);
         double* const rp1[1] = {Rpan + 2 * q * ldr + 8 + g};
         tt_upd<K, 1>(c1, x, vb, tb0, tb1, rp1, ldr);
-        dr_signal(ver_p1 + p, t + 1, lane);
+        tm_fence_before();
+        dr_signal(ver_p1 + p, t + 1, lane);  // also: block p+1 is in registers, its TMEM columns free
         SP_TICK(a6_);
         SP_ADD(5, a5_, a6_);
 #pragma unroll
@@ -445,9 +418,46 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
     const int s = u % G, hf = u / G;  // slot (same sub-partition: G % 4 == 0), block parity
     int* vu = ver_u + hf * 16;
     const double2* tbs = reinterpret_cast<const double2*>(sm + Sm::TB + s * 128);
+    double* stg = sm + Sm::STG + s * H * 8;
+    const bool v16 = ((lda & 1) == 0) && ((n & 1) == 0) && (((uintptr_t)A & 15) == 0);
     int lt = 0;
     for (int t = s; t < T; t += G, ++lt) {
-      for (int p = 0; p + 2 < npan; ++p) {
+      const bool more = hf == 0 && t + G < T;  // this warp stages the slot's next tile
+      const int64_t nrow0 = r0 + (int64_t)(t + G) * H;
+      const int nvalid = more ? (int)min64(H, r0 + b - nrow0) : 0;
+      // next tile's block bk: global -> shared stage (issued a job ahead, lands under the
+      // updates) -> the block's TMEM columns once the generation warp has taken the old block
+      auto stage_issue = [&](int bk) {
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(stg);
+        if (v16) {
+#pragma unroll
+          for (int i = 0; i < H / 8; ++i) {
+            const int x2 = lane + 32 * i, r = x2 >> 2, c2 = x2 & 3;
+            const bool ok = r < nvalid && 8 * bk + 2 * c2 < n;
+            cp_async<16>(sb + 8u * (unsigned)(r * 8 + 2 * c2),
+                         ok ? A + (nrow0 + r) * lda + 8 * bk + 2 * c2 : A, ok ? 16u : 0u);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < H / 4; ++i) {
+            const int x1 = lane + 32 * i, r = x1 >> 3, c = x1 & 7;
+            const bool ok = r < nvalid && 8 * bk + c < n;
+            cp_async<8>(sb + 8u * (unsigned)(r * 8 + c), ok ? A + (nrow0 + r) * lda + 8 * bk + c : A,
+                        ok ? 8u : 0u);
+          }
+        }
+        cp_async_commit();
+      };
+      auto stage_move = [&](int bk) {
+        cp_async_wait<0>();
+        __syncwarp();
+        double v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = stg[erow(k) * 8 + g];
+        __syncwarp();
+        tt_st<K>(taddr(s, bk), v);
+      };
+      for (int p = 0; p + 1 < npan; ++p) {
         const int job = lt * 16 + p;
         const int ldr = dr_ldr<128>(p);
         double* Rpan = Rp + dr_pbase<128>(p);
@@ -456,6 +466,14 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         tm_fence_after();
         SP_TICK(u1_);
         SP_ADD(8, u0_, u1_);
+        if (more) {
+          if (p == 0) {  // block 0 was taken by the generation warp at the tile's start
+            stage_issue(0);
+            stage_move(0);
+          }
+          stage_issue(p + 1);
+        }
+        if (p + 2 < npan) {
         const double* yn = sm + Sm::YN + (s * 2 + (p & 1)) * H * 8;
         const double* yf = sm + Sm::YF + (s * 2 + (p & 1)) * H * 8;
         double y[K], vb[K / 2][2];
@@ -512,6 +530,17 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         dr_signal(vu + p, t + 1, lane);
         SP_TICK(u3_);
         SP_ADD(10, u2_, u3_);
+        }
+        if (more) {
+          sp_wait_ge(ver_p1 + p, t + 1, lane);  // block p+1 taken (hand-off of panel p)
+          tm_fence_after();
+          stage_move(p + 1);
+        }
+      }
+      if (more) {
+        tm_st_wait();
+        tm_fence_before();
+        dr_signal(staged + s, lt + 1, lane);
       }
     }
   }

@@ -95,7 +95,6 @@ int main(int argc, char** argv) {
       },                                                                                             \
       TtSmem<H>::bytes, A, R, flag, P, b, n, m, (double)H)
   TT_RUN("tt H=32 UW=1", 32, 1);
-  TT_RUN("tt H=64 UW=2", 64, 2);
   TT_RUN("tt H=64 UW=1", 64, 1);
   return 0;
 }
