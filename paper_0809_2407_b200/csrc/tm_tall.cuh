@@ -457,6 +457,7 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         __syncwarp();
         tt_st<K>(taddr(s, bk), v);
       };
+      double keep[1][K];  // block p+2 between jobs p-1 and p
       for (int p = 0; p + 1 < npan; ++p) {
         const int job = lt * 16 + p;
         const int ldr = dr_ldr<128>(p);
@@ -466,17 +467,10 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
         tm_fence_after();
         SP_TICK(u1_);
         SP_ADD(8, u0_, u1_);
-        if (more) {
-          if (p == 0) {  // block 0 was taken by the generation warp at the tile's start
-            stage_issue(0);
-            stage_move(0);
-          }
-          stage_issue(p + 1);
-        }
+        double y[K], vb[K / 2][2], tb0 = 0.0, tb1 = 0.0;
         if (p + 2 < npan) {
         const double* yn = sm + Sm::YN + (s * 2 + (p & 1)) * H * 8;
         const double* yf = sm + Sm::YF + (s * 2 + (p & 1)) * H * 8;
-        double y[K], vb[K / 2][2];
 #pragma unroll
         for (int k = 0; k < K; ++k) y[k] = yf[k * 32 + lane];
 #pragma unroll
@@ -486,38 +480,56 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
           vb[i][1] = t2.y;
         }
         const double2 tb = tbs[(p & 1) * 32 + lane];
-        const double tb0 = tb.x, tb1 = tb.y;
+        tb0 = tb.x;
+        tb1 = tb.y;
         dr_wait(vu + p, t, lane);
         SP_TICK(u2_);
         SP_ADD(9, u1_, u2_);
         double* rrow = Rpan + 2 * q * ldr + g - 8 * p;  // + 8 * bb: block bb's pivot rows
-        int bb = p + 2;
-        if (UW > 1 && ((bb ^ hf) & 1)) ++bb;  // first block of this warp's parity
-        if (bb == p + 2) {  // the generation warp's next look-ahead block first, alone
-          double c[1][K];
-          tt_ld<K>(c[0], taddr(s, bb));
-          double* const rp[1] = {rrow + 8 * bb};
-          tt_upd<K, 1>(c, y, vb, tb0, tb1, rp, ldr);
-          tt_st<K>(taddr(s, bb), c[0]);
+        {  // the generation warp's next look-ahead block first: block p+2, still in this
+           // warp's registers from job p-1 (it was updated last there and not stored)
+          if (p == 0) tt_ld<K>(keep[0], taddr(s, 2));
+          double* const rp[1] = {rrow + 8 * (p + 2)};
+          tt_upd<K, 1>(keep, y, vb, tb0, tb1, rp, ldr);
+          tt_st<K>(taddr(s, p + 2), keep[0]);
           tm_st_wait();
           tm_fence_before();
           dr_signal(ufirst + s, job + 1, lane);
-          bb += UW;
         }
-        for (; bb + UW < npan; bb += 2 * UW) {
+        SP_TICK(u2e_);
+        SP_ADD(10, u2_, u2e_);
+        }
+        // staging of the slot's next tile, after the hand-off block (which the generation
+        // warp is waiting for): block p (in flight since job p-1) into its TMEM columns, then
+        // block p+1 into the stage
+        if (more) {
+          if (p == 0) {
+            stage_issue(0);  // taken by the generation warp at the tile's start
+          } else {
+            sp_wait_ge(ver_p1 + p - 1, t + 1, lane);  // block p taken (hand-off of panel p-1)
+            tm_fence_after();
+          }
+          stage_move(p);
+          stage_issue(p + 1);
+        }
+        if (p + 2 < npan) {
+        SP_TICK(u2b_);
+        double* rrow = Rpan + 2 * q * ldr + g - 8 * p;
+        int bb = p + 4;
+        for (; bb + 1 < npan; bb += 2) {
           double c[2][K];
           {
             uint32_t ra[2 * K], rb[2 * K];
             tt_ld_issue<K>(ra, taddr(s, bb));
-            tt_ld_issue<K>(rb, taddr(s, bb + UW));
+            tt_ld_issue<K>(rb, taddr(s, bb + 1));
             tm_ld_wait();
             tt_unpack<K>(c[0], ra);
             tt_unpack<K>(c[1], rb);
           }
-          double* const rp[2] = {rrow + 8 * bb, rrow + 8 * (bb + UW)};
+          double* const rp[2] = {rrow + 8 * bb, rrow + 8 * (bb + 1)};
           tt_upd<K, 2>(c, y, vb, tb0, tb1, rp, ldr);
           tt_st<K>(taddr(s, bb), c[0]);
-          tt_st<K>(taddr(s, bb + UW), c[1]);
+          tt_st<K>(taddr(s, bb + 1), c[1]);
         }
         if (bb < npan) {
           double c[1][K];
@@ -526,18 +538,21 @@ k_leaf_tt(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, in
           tt_upd<K, 1>(c, y, vb, tb0, tb1, rp, ldr);
           tt_st<K>(taddr(s, bb), c[0]);
         }
+        if (p + 3 < npan) {  // block p+3 last, kept in registers: the next job's first block
+          tt_ld<K>(keep[0], taddr(s, p + 3));
+          double* const rp[1] = {rrow + 8 * (p + 3)};
+          tt_upd<K, 1>(keep, y, vb, tb0, tb1, rp, ldr);
+        }
         tm_st_wait();
         dr_signal(vu + p, t + 1, lane);
         SP_TICK(u3_);
-        SP_ADD(10, u2_, u3_);
-        }
-        if (more) {
-          sp_wait_ge(ver_p1 + p, t + 1, lane);  // block p+1 taken (hand-off of panel p)
-          tm_fence_after();
-          stage_move(p + 1);
+        SP_ADD(10, u2b_, u3_);
         }
       }
       if (more) {
+        sp_wait_ge(ver_p1 + npan - 2, t + 1, lane);  // the last block taken
+        tm_fence_after();
+        stage_move(npan - 1);
         tm_st_wait();
         tm_fence_before();
         dr_signal(staged + s, lt + 1, lane);
