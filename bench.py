@@ -35,7 +35,7 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22 (BASELINE.md section 2
 # ncu --set full captures (profiles/r02/*_ncu_summary.txt)
 NARROW8_TRAFFIC = (8.596103e9 + 10.115584e6) / (8.0 * 134217728 * 8)
 # k_leaf_tt<64, 1, false> at C3 full size, profiles/r02/leaf_tt_kernel_ncu_summary.txt
-DMMA_TRAFFIC = (17.367186e9 + 6.626816e6) / (8.0 * 16777216 * 128)
+DMMA_TRAFFIC = (17.376649e9 + 7.044608e6) / (8.0 * 16777216 * 128)
 METRIC = "TSQR fp64 GFLOP/s & % of roofline"
 
 CONFIGS = {
@@ -614,8 +614,8 @@ def run_ours(args, cfg):
         else:
             ach = F_leaf / t_leaf / 1e12
             # DRAM traffic of the leaf kernel from the committed ncu capture
-            # (profiles/r02/leaf_tt_kernel_ncu_summary.txt: 17.367 GB read + 6.6 MB
-            # written at C3 full size = 1.0113x the 8mn algorithmic bytes), scaled
+            # (profiles/r02/leaf_tt_kernel_ncu_summary.txt: 17.377 GB read + 7.0 MB
+            # written at C3 full size = 1.0119x the 8mn algorithmic bytes), scaled
             # to this launch's rows; None for other widths.
             traffic = 8.0 * (hi - lo) * n * DMMA_TRAFFIC if (n == 128 and cfg["q"] == "none") else None
             kern = (("k_leaf_tt<64,1> (tall tiles in tensor memory, CTAs chaining consecutive leaves) + "
