@@ -60,7 +60,7 @@ static int g_zstart = 1;  // CAQR_TUNE_ZSTART: R-only leaves skip the dense firs
 static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA warp ring
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
 static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles on DMMA (opt-in, slower)
-static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: n <= 64 node factors on DMMA
+static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: node factors on DMMA (n <= 64: 8 warps, n <= 128: 16)
 static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int g_fuse = 148;      // CAQR_TUNE_FUSE: R-only n in (64,128]: CTAs (one per SM) that chain consecutive leaves; 0 off
@@ -1162,6 +1162,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 #include "tm_leaf.cuh"
 #include "tm_tall.cuh"
 #include "tall_apply.cuh"
+#include "tree_factor128.cuh"
 #include "dense_geqr2.cuh"
 
 // ===========================================================================
@@ -1481,6 +1482,13 @@ int tsqr_f64_tree_factor_level(double* Rslots, int64_t n, const int32_t* events,
     k_tree_factor<NPV><<<(int)nev, THREADS, TreeSmem<NPV>::bytes, st>>>(Rslots, (int)n,  \
         events, Ynode, taunode, 0);                                                      \
     break;                                                                               \
+  }
+  if (p == 128 && g_dmma_tree_factor) {
+    int rc = prep(k_tree_factor_dmma128, TreeFactor128Smem::bytes);
+    if (rc) return rc;
+    k_tree_factor_dmma128<<<(int)nev, TF_W * 32, TreeFactor128Smem::bytes, st>>>(Rslots, (int)n, events,
+                                                                                 Ynode, taunode);
+    return check_launch("k_tree_factor_dmma128");
   }
   if (p <= 64 && g_dmma_tree_factor) {
 #define TFD_LAUNCH(NPV)                                                                  \
