@@ -186,9 +186,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * order); for n in (32, 64]: 2 = 32-column CTAs, 3 = one CTA per SM; 0 = the
  * reflector-by-reflector warp ring. */
 #define CAQR_TUNE_DMMA_Q 11
-/* CAQR_TUNE_DMMA_TREE: 1 (default) = Q C / Q^T C of the tree nodes (STACKED factors) runs
- * k_tree_apply_dmma (compact WY per 8 reflectors, two CTA barriers per panel); 0 = the
- * reflector-by-reflector k_tree_apply / k_tree_apply_w32. */
+/* CAQR_TUNE_DMMA_TREE: Q C / Q^T C of the tree nodes (STACKED factors): 2 (default) =
+ * k_tree_apply_cp for n in (64, 128] (column-parallel warps, no barrier in the panel loop) and
+ * k_tree_apply_dmma below; 1 = k_tree_apply_dmma for every n (compact WY per 8 reflectors, two
+ * CTA barriers per panel); 0 = the reflector-by-reflector k_tree_apply / k_tree_apply_w32. */
 #define CAQR_TUNE_DMMA_TREE 12
 /* CAQR_TUNE_DMMA_TREE_FACTOR: 1 (default) = the q = 2 node factors (Q kept) for n <= 64 run
  * k_tree_factor_dmma (column-block warps, panels factored Level-2 by the owning warp and

@@ -148,7 +148,7 @@ TUNE_FUSE = 16
 # the library's defaults (csrc/tsqr_sm100.cu, g_ht / g_narrow / ... initialisers)
 TUNE_DEFAULTS = {TUNE_CHAIN_HT[32]: 16, TUNE_CHAIN_HT[64]: 16, TUNE_CHAIN_HT[128]: 16,
                  TUNE_NARROW: 3, TUNE_ZSTART: 1, TUNE_DMMA: 2,
-                 TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1, TUNE_DMMA_TREE: 1,
+                 TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1, TUNE_DMMA_TREE: 2,
                  TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 5, TUNE_FUSE: 148}
 
 

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "tsqr_sm100.cu")]
-HEADERS = [os.path.join(HERE, "csrc", "tsqr_device.cuh"), os.path.join(HERE, "csrc", "dmma_ring.cuh"), os.path.join(HERE, "csrc", "dmma_apply.cuh"), os.path.join(HERE, "csrc", "split_leaf.cuh"), os.path.join(HERE, "csrc", "tm_leaf.cuh"), os.path.join(HERE, "csrc", "tm_tall.cuh"), os.path.join(HERE, "csrc", "tall_apply.cuh"), os.path.join(HERE, "csrc", "tree_factor128.cuh"), os.path.join(HERE, "csrc", "dense_geqr2.cuh"), os.path.join(ROOT, "include", "caqr_sm100.h")]
+HEADERS = [os.path.join(HERE, "csrc", "tsqr_device.cuh"), os.path.join(HERE, "csrc", "dmma_ring.cuh"), os.path.join(HERE, "csrc", "dmma_apply.cuh"), os.path.join(HERE, "csrc", "split_leaf.cuh"), os.path.join(HERE, "csrc", "tm_leaf.cuh"), os.path.join(HERE, "csrc", "tm_tall.cuh"), os.path.join(HERE, "csrc", "tall_apply.cuh"), os.path.join(HERE, "csrc", "tree_factor128.cuh"), os.path.join(HERE, "csrc", "tree_apply_cp.cuh"), os.path.join(HERE, "csrc", "dense_geqr2.cuh"), os.path.join(ROOT, "include", "caqr_sm100.h")]
 OUT = os.path.join(HERE, "lib", "libcaqr_sm100.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

@@ -61,7 +61,7 @@ static int g_dmma = 2;     // CAQR_TUNE_DMMA: n in (32,128] leaves on the DMMA w
 static int g_dmma_q = 1;      // CAQR_TUNE_DMMA_Q: Q C of 16-row-tile chain leaves (n <= 128) on the DMMA ring
 static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles on DMMA (opt-in, slower)
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: node factors on DMMA (n <= 64: 8 warps, n <= 128: 16)
-static int g_dmma_tree = 1;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA
+static int g_dmma_tree = 2;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA (2: column-parallel for n > 64)
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
 static int g_fuse = 148;      // CAQR_TUNE_FUSE: R-only n in (64,128]: CTAs (one per SM) that chain consecutive leaves; 0 off
 static int g_cc = 5;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 5 / 6 split-role ring with 4 / 8 tall
@@ -1163,6 +1163,7 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
 #include "tm_tall.cuh"
 #include "tall_apply.cuh"
 #include "tree_factor128.cuh"
+#include "tree_apply_cp.cuh"
 #include "dense_geqr2.cuh"
 
 // ===========================================================================
@@ -1537,6 +1538,20 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
           C, ldc, slot_rows, ncols, zero_partner);                                              \
     }                                                                                           \
     break;                                                                                      \
+  }
+  if (g_dmma_tree >= 2 && p == 128) {  // column-parallel warps, no barriers in the panel loop
+    const size_t smc = TreeApplyCpSmem::bytes;
+    dim3 gc((unsigned)nev, (unsigned)((ncols + TAC_KB - 1) / TAC_KB));
+    if (transpose) {
+      int rc = prep(k_tree_apply_cp<true>, smc); if (rc) return rc;
+      k_tree_apply_cp<true><<<gc, THREADS, smc, st>>>(Ynode, taunode, (int)n, events, C, ldc, slot_rows,
+                                                      ncols, zero_partner);
+    } else {
+      int rc = prep(k_tree_apply_cp<false>, smc); if (rc) return rc;
+      k_tree_apply_cp<false><<<gc, THREADS, smc, st>>>(Ynode, taunode, (int)n, events, C, ldc, slot_rows,
+                                                       ncols, zero_partner);
+    }
+    return check_launch("k_tree_apply_cp");
   }
   if (g_dmma_tree) {
     const size_t sm = TreeApplyDmmaSmem::bytes;
