@@ -289,7 +289,7 @@ def caqr_roofline(A, cfg, args):
 
     m, n = A.shape
     b = 128
-    full = caqr_factor(A, b=b, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+    full = caqr_factor(A, b=b, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains, apply_waves=args.apply_waves)
     launches = full.launches
     del full
     P = _panel_leaves(m, b, cfg["leaf"])
@@ -468,7 +468,7 @@ def run_ours(args, cfg):
         if is_caqr:
             from paper_0809_2407_b200.caqr import caqr_factor
 
-            last["f"] = caqr_factor(A, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+            last["f"] = caqr_factor(A, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains, apply_waves=args.apply_waves)
             return last["f"]
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -651,7 +651,7 @@ def run_ours(args, cfg):
             from paper_0809_2407_b200.caqr import caqr_factor
 
             def e2e_step():
-                res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains)
+                res = caqr_factor(Ah, b=128, leaf_rows=cfg["leaf"], panel_chains=args.panel_chains, apply_waves=args.apply_waves)
                 return res.R
         elif ws == 1:
             def e2e_step():
@@ -741,6 +741,7 @@ def main():
     ap.add_argument("--data", default="reference", choices=["reference", "torch"],
                     help="inputs: the reference's generators bit for bit (default) or torch Philox")
     ap.add_argument("--grid-lookahead", action="store_true", help="c5 grid: two-stream lookahead")
+    ap.add_argument("--apply-waves", type=float, default=4.0, help="c5: waves of trailing-update CTAs per panel")
     ap.add_argument("--panel-chains", type=int, default=4,
                     help="CAQR: split each panel's leaves into GPU chains up to this count")
     args = ap.parse_args()

@@ -104,3 +104,37 @@ def test_tall_run_to_run_bitwise():
     A = philox(11).standard_normal((148 * 700, 128))
     f1, f2 = factor(A, 148), factor(A, 148)
     assert torch.equal(f1.R, f2.R) and torch.equal(f1.Y, f2.Y) and torch.equal(f1.tau, f2.tau)
+
+
+# ---- the n in (64, 128] tree kernels (k_tree_factor_dmma128, k_tree_apply_cp), default format ----
+
+@pytest.mark.parametrize("m,n,P", [(3000, 72, 5), (2600, 100, 2), (4000, 127, 3), (5000, 128, 7),
+                                   (1300, 65, 4)])
+def test_wide_tree_nodes_match_oracle(m, n, P):
+    """Node factors (qr_stacked_triangles, householder.py:263-294) element-wise against the
+    oracle, explicit Q, and Q^T C / Q C with a column count that is not a multiple of 8
+    (partial warps of the column-parallel tree apply), both directions, zero partner included."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import apply_q_device, explicit_q_device, factor_device
+
+    _lib.reset_tuning()  # default 16-row leaf format; the tree kernels are the same for both
+    A = philox(m * 3 + n).standard_normal((m, n))
+    _, h0, ht = _lib.geometry(n)
+    f = factor_device(torch.from_numpy(A).cuda(), P, want_q=True)
+    ref = oracle.tsqr_hybrid(A, P, h0, ht)
+    nY, nt = f.node_Y.cpu().numpy(), f.node_tau.cpu().numpy()
+    for e, (lvl, a, b, Yb, tn) in enumerate(ref["nodes"]):
+        assert np.max(np.abs(nY[e] - Yb)) <= 1e-9, e
+        assert np.max(np.abs(nt[e] - tn)) <= 1e-12, e
+    Q = explicit_q_device(f).cpu().numpy()
+    assert np.max(np.abs(Q - oracle.tsqr_hybrid_q(ref))) <= 1e-11
+    R = f.R.cpu().numpy()
+    assert oracle.residual(A, Q, R) <= 10 * n * EPS
+    assert oracle.orthogonality(Q) <= 10 * n * EPS
+    for k in (37, 131):
+        C = philox(k).standard_normal((m, k))
+        Ct = torch.from_numpy(C).cuda()
+        QtC = apply_q_device(f, Ct, transpose=True)
+        assert np.max(np.abs(QtC.cpu().numpy()[:n] - Q.T @ C)) <= 200 * n * EPS * np.max(np.abs(C))
+        back = apply_q_device(f, QtC, transpose=False).cpu().numpy()
+        assert np.max(np.abs(back - C)) <= 100 * n * EPS * np.max(np.abs(C))
