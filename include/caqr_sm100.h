@@ -118,6 +118,22 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
                         const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
                         int zero_init, int tri_skip, void* stream);
 
+/* The CAQR trailing update with the chain tiles' panel T kept (householder.py:175-186, :209:
+ * _apply_yt(transpose=True) with T from form_t, :148-164, instead of rebuilt per call).
+ * tsqr_f64_leaf_factor_t is tsqr_f64_leaf_factor (Y, tau required) and also writes, for
+ * every chain tile t and 8-column panel p of a leaf, T_p as 32 x 2 doubles at
+ * T[((leaf * (tau_stride / n) + t + 1) * 16 + p) * 64 ..]: T needs P * (tau_stride / n) * 1024
+ * doubles.  tsqr_f64_leaf_apply_t is tsqr_f64_leaf_apply(transpose = 1) reading that buffer.
+ * The buffer is used when tsqr_f64_panel_t_used(n) returns 1 (n in (64, 128] with the default
+ * 16-row DMMA ring kernels); otherwise both calls behave like the plain ones and T is ignored. */
+int tsqr_f64_panel_t_used(int64_t n);
+int tsqr_f64_leaf_factor_t(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Y,
+                           int64_t ldy, double* tau, int64_t tau_stride, double* R, int* flag,
+                           double* T, void* stream);
+int tsqr_f64_leaf_apply_t(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
+                          int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
+                          const double* T, void* stream);
+
 /* Single-CTA factorization of a block of rows <= 128: mode 0 = DENSE
  * (qr_unblocked: R out, Y m x n LAPACK layout), mode 2 = TRIRECT
  * (qr_triangle_on_rect: R in/out, Y = rectangle), mode 3 = STACKED with q-1

@@ -27,6 +27,9 @@ SYMBOLS = (
     "tsqr_f64_tree_factor_level",
     "tsqr_f64_tree_apply_level",
     "tsqr_f64_leaf_apply",
+    "tsqr_f64_leaf_factor_t",
+    "tsqr_f64_leaf_apply_t",
+    "tsqr_f64_panel_t_used",
     "tsqr_f64_block_factor",
     "tsqr_f64_block_apply",
     "tsqr_f64_geqr2",
@@ -56,6 +59,12 @@ def _sig(lib):
     lib.tsqr_f64_geometry.restype = i32
     lib.tsqr_f64_geometry.argtypes = [i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                       ctypes.POINTER(i64)]
+    lib.tsqr_f64_panel_t_used.restype = i32
+    lib.tsqr_f64_panel_t_used.argtypes = [i64]
+    lib.tsqr_f64_leaf_factor_t.restype = i32
+    lib.tsqr_f64_leaf_factor_t.argtypes = [dp, i64, i64, i64, i64, dp, i64, dp, i64, dp, ip, dp, vp]
+    lib.tsqr_f64_leaf_apply_t.restype = i32
+    lib.tsqr_f64_leaf_apply_t.argtypes = [dp, i64, dp, i64, i64, i64, i64, dp, i64, i64, dp, vp]
     lib.tsqr_f64_leaf_factor.restype = i32
     lib.tsqr_f64_leaf_factor.argtypes = [dp, i64, i64, i64, i64, dp, i64, dp, i64, dp, ip, vp]
     lib.tsqr_f64_r_binary.restype = i32

@@ -141,6 +141,12 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         n_rs += P * w * w
         n_ny += (P - 1) * w * w
         n_nt += (P - 1) * w
+    # panel T of the chain tiles (tsqr_f64_leaf_factor_t / _apply_t): two slots, panel jp uses
+    # slot jp & 1 -- factor(jp + 1) is enqueued behind the far update of panel jp - 1 (evB), the
+    # last reader of that slot
+    use_t = bool(lib.tsqr_f64_panel_t_used(b)) if nb > 1 else False
+    t_len = max((pl[4] * pl[7] for pl in plan), default=0) * 1024 if use_t else 0
+    t_all = torch.empty((2, max(1, t_len)), dtype=torch.float64, device=dev)
     tau_all = torch.zeros(max(1, n_tau), dtype=torch.float64, device=dev)
     rs_all = torch.empty(max(1, n_rs), dtype=torch.float64, device=dev)
     ny_all = torch.zeros(max(1, n_ny), dtype=torch.float64, device=dev)
@@ -154,9 +160,15 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         base_ptr = _ptr(W) + 8 * (c0 * n + c0)
         sh = int(st.cuda_stream)
         nlaunch[0] += 1 + (mj - lay.base * (P - 1) > h0) + (len(levels) if P > 1 else 0)
-        _lib.check(lib.tsqr_f64_leaf_factor(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
-                                            tiles * w, _ptr(Rs), _ptr(flag), sh),
-                   "tsqr_f64_leaf_factor")
+        if use_t and w == b:
+            _lib.check(lib.tsqr_f64_leaf_factor_t(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
+                                                  tiles * w, _ptr(Rs), _ptr(flag),
+                                                  _ptr(t_all[jp & 1]), sh),
+                       "tsqr_f64_leaf_factor_t")
+        else:
+            _lib.check(lib.tsqr_f64_leaf_factor(base_ptr, n, mj, w, P, base_ptr, n, _ptr(tau),
+                                                tiles * w, _ptr(Rs), _ptr(flag), sh),
+                       "tsqr_f64_leaf_factor")
         node_Y = node_tau = None
         if P > 1:
             node_Y = ny_all[o_y:o_y + (P - 1) * w * w].view(P - 1, w, w)
@@ -181,9 +193,15 @@ def caqr_factor(A, layout: BlockCyclicLayout | None = None, b: int = 128, leaf_r
         cptr = _ptr(W) + 8 * (c0 * n + lo)
         sh = int(st.cuda_stream)
         nlaunch[0] += 1 + len(pnl.levels)
-        _lib.check(lib.tsqr_f64_leaf_apply(base_ptr, n, _ptr(pnl.tau), pnl.tau.shape[1] * w, mj, w,
-                                           P, cptr, n, hi - lo, 0, 0, 0, 1, 0, 0, sh),
-                   "tsqr_f64_leaf_apply")
+        if use_t and w == b:
+            _lib.check(lib.tsqr_f64_leaf_apply_t(base_ptr, n, _ptr(pnl.tau), pnl.tau.shape[1] * w,
+                                                 mj, w, P, cptr, n, hi - lo, _ptr(t_all[jp & 1]),
+                                                 sh),
+                       "tsqr_f64_leaf_apply_t")
+        else:
+            _lib.check(lib.tsqr_f64_leaf_apply(base_ptr, n, _ptr(pnl.tau), pnl.tau.shape[1] * w, mj,
+                                               w, P, cptr, n, hi - lo, 0, 0, 0, 1, 0, 0, sh),
+                       "tsqr_f64_leaf_apply")
         for ev in pnl.levels:
             _lib.check(lib.tsqr_f64_tree_apply_level(_ptr(pnl.node_Y), _ptr(pnl.node_tau), w,
                                                      _ptr(ev), ev.shape[0], cptr, n,

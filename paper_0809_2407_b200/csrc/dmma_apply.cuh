@@ -112,7 +112,8 @@ template <int KB>
 __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
                   int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
-                  int64_t ncols) {
+                  int64_t ncols, const double* __restrict__ Tin = nullptr) {
+  // Tin (nullable): the chain tiles' panel T stored by k_leaf_dmma (Tout), read instead of formed
   constexpr int H0 = WARPS * Geo<128>::HD, CB = KB / 8;  // dense first tile: 128 rows
   constexpr int DA_KB = KB, DA_LDC = DmmaApplySmem<KB>::LDC;
   extern __shared__ __align__(16) double sm[];
@@ -257,13 +258,28 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
     // stale data and is discarded
     nxt = cur;
     double tb0, tb1;
-    da_form_t(cur, tb0, tb1);
+    const double2* Tt = Tin ? reinterpret_cast<const double2*>(Tin) +
+                                  ((int64_t)(leaf * (tau_stride / n) + t + 1) * 16) * 32 + lane
+                            : nullptr;
+    if (Tt) {
+      const double2 t2 = __ldg(Tt);
+      tb0 = t2.x;
+      tb1 = t2.y;
+    } else {
+      da_form_t(cur, tb0, tb1);
+    }
     for (int p = 0; p < npan; ++p) {
       if (p + 1 < npan) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p + 1));
       dr_wait(ver + p, t, lane);
       double* rrow = Cs + (8 * p + 2 * q) * DA_LDC + g;
       double tn0, tn1;
-      da_form_t(nxt, tn0, tn1);
+      if (Tt) {
+        const double2 t2 = __ldg(Tt + (p + 1 < npan ? p + 1 : p) * 32);
+        tn0 = t2.x;
+        tn1 = t2.y;
+      } else {
+        da_form_t(nxt, tn0, tn1);
+      }
       // all blocks, unguarded (columns >= ncb are zero in Ct and Cs and never
       // stored): one basic block, so ptxas interleaves the blocks' DMMA chains
 #pragma unroll

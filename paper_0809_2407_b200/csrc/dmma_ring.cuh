@@ -275,7 +275,11 @@ template <int NP, bool V16, bool Q>
 __global__ void __launch_bounds__(DR_WARPS * 32, DmmaRingSmem<NP>::MINB)
 k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, int64_t base,
             double* Y, int64_t ldy, double* tau, int64_t tau_stride, double* Rio, int* flag,
-            int h0) {
+            int h0, double* Tout = nullptr) {
+  // Tout (nullable, with Y): every chain tile's panel T, as the apply kernels want it
+  // (tb[s] = T[2q+s][g] per lane), at ((leaf * tau_stride / n + t + 1) * 16 + p) * 64 + 2 * lane:
+  // the CAQR trailing update then reads 512 bytes per tile panel instead of rebuilding T
+  // (14 of its 174 DMMAs) in every 128-column CTA.
   // h0 = 0: R only, the chain starts from R = 0 at the leaf's first row.
   // h0 > 0: the chain continues from the leaf's R slot after a dense first tile of h0 rows
   // (k_leaf_dense); Y / tau (nullable) receive each chain tile's TRI_ON_RECT factor in the
@@ -387,6 +391,9 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         for (int k = 0; k < 4; ++k) vs[(8 * (k >> 1) + 2 * q + (k & 1)) * 12 + g] = x[k];
         __syncwarp();
         dr_form_t(gs, taus, tb0, tb1);
+        if (Q && Tout)
+          reinterpret_cast<double2*>(Tout)[((int64_t)(leaf * (tau_stride / n) + t + 1) * 16 + p) * 32 + lane] =
+              make_double2(tb0, tb1);
 #pragma unroll
         for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
@@ -433,6 +440,14 @@ k_leaf_dmma(const double* __restrict__ A, int64_t lda, int64_t m, int n, int P, 
         for (int k = 0; k < 4; ++k) x[k] = xn[k];
         DR_TICK(c5_);
         DR_ADD(3, c4_, c5_);
+      }
+      if (Q && Tout && nl <= 1) {  // the last panel has no trailing block here; the update needs its T
+        double tb0, tb1;
+        __syncwarp();
+        dr_form_t(gs, taus, tb0, tb1);
+        reinterpret_cast<double2*>(Tout)[((int64_t)(leaf * (tau_stride / n) + t + 1) * 16 + p) * 32 + lane] =
+            make_double2(tb0, tb1);
+        __syncwarp();
       }
       // shift the register blocks: the next panel becomes block 0
 #pragma unroll

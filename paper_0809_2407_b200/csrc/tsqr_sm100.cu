@@ -1263,7 +1263,7 @@ static int64_t min_tau_stride(int64_t m, int64_t n, int64_t P, int64_t base) {
 // Leaves of `base` rows, the last one taking the remainder (m - (P-1) base >= base).
 static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
                             int64_t base, double* Y, int64_t ldy, double* tau, int64_t tau_stride,
-                            double* R, int* flag, void* stream) {
+                            double* R, int* flag, void* stream, double* Tout = nullptr) {
   const int p = padded(n);
   if (!p || !A || !R || P < 1 || m < n * P || lda < n || (Y && ldy < n))
     return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor: bad arguments");
@@ -1292,7 +1292,7 @@ static int leaf_factor_impl(const double* A, int64_t lda, int64_t m, int64_t n, 
     rc = prep(k_leaf_dmma<NPD, V16, Q>, DmmaRingSmem<NPD>::bytes);                              \
     if (rc) return rc;                                                                          \
     k_leaf_dmma<NPD, V16, Q><<<grid, DR_WARPS * 32, DmmaRingSmem<NPD>::bytes, st>>>(A, lda, m,  \
-        (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag, h0d);                           \
+        (int)n, (int)P, base, Y, ldy, tau, tau_stride, R, flag, h0d, Tout);                     \
   }
 #define LEAF_CASE(NPV, HA, HB)                                                                  \
   case NPV: {                                                                                   \
@@ -1376,6 +1376,20 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
                          void* stream) {
   if (P < 1) return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor: bad arguments");
   return leaf_factor_impl(A, lda, m, n, P, m / P, Y, ldy, tau, tau_stride, R, flag, stream);
+}
+
+// 1 when tsqr_f64_leaf_factor_t / _apply_t use the panel-T buffer for this width under the
+// current tuning (n in (64, 128], 16-row chain tiles on the DMMA ring kernels), else 0.
+int tsqr_f64_panel_t_used(int64_t n) {
+  return padded(n) == 128 && g_ht[2] == 16 && g_dmma && g_dmma_apply ? 1 : 0;
+}
+
+int tsqr_f64_leaf_factor_t(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Y,
+                           int64_t ldy, double* tau, int64_t tau_stride, double* R, int* flag,
+                           double* T, void* stream) {
+  if (P < 1 || !Y || !tau) return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_factor_t: bad arguments");
+  return leaf_factor_impl(A, lda, m, n, P, m / P, Y, ldy, tau, tau_stride, R, flag, stream,
+                          tsqr_f64_panel_t_used(n) ? T : nullptr);
 }
 
 static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P,
@@ -1582,10 +1596,10 @@ int tsqr_f64_tree_apply_level(const double* Ynode, const double* taunode, int64_
   return check_launch("k_tree_apply");
 }
 
-int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
-                        int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
-                        const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
-                        int zero_init, int tri_skip, void* stream) {
+static int leaf_apply_impl(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
+                           int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
+                           const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
+                           int zero_init, int tri_skip, void* stream, const double* Tin) {
   const int p = padded(n);
   if (!p || !Y || !tau || !C || P < 1 || m < n * P || ncols < 1 || ldc < ncols || ldy < n)
     return set_err(CAQR_ERR_ARG, "tsqr_f64_leaf_apply: bad arguments");
@@ -1698,14 +1712,14 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
           if (rc) return rc;
           dim3 gd((unsigned)P, (unsigned)((ncols + 31) / 32));
           k_leaf_apply_dmma<32><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
-                                                         base, C, ldc, ncols);
+                                                         base, C, ldc, ncols, Tin);
         } else {
           const size_t sm = DmmaApplySmem<128>::bytes;
           int rc = prep(k_leaf_apply_dmma<128>, sm);
           if (rc) return rc;
           dim3 gd((unsigned)P, (unsigned)((ncols + 127) / 128));
           k_leaf_apply_dmma<128><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
-                                                          base, C, ldc, ncols);
+                                                          base, C, ldc, ncols, Tin);
         }
       } else LA_LAUNCH(128, 4, 16)
       break;
@@ -1714,6 +1728,21 @@ int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t
 #undef LA_CASE
 #undef LA_LAUNCH
   return check_launch("k_leaf_apply");
+}
+
+int tsqr_f64_leaf_apply(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
+                        int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
+                        const double* S, int64_t lds, int64_t s_slot_rows, int transpose,
+                        int zero_init, int tri_skip, void* stream) {
+  return leaf_apply_impl(Y, ldy, tau, tau_stride, m, n, P, C, ldc, ncols, S, lds, s_slot_rows,
+                         transpose, zero_init, tri_skip, stream, nullptr);
+}
+
+int tsqr_f64_leaf_apply_t(const double* Y, int64_t ldy, const double* tau, int64_t tau_stride,
+                          int64_t m, int64_t n, int64_t P, double* C, int64_t ldc, int64_t ncols,
+                          const double* T, void* stream) {
+  return leaf_apply_impl(Y, ldy, tau, tau_stride, m, n, P, C, ldc, ncols, nullptr, 0, 0, 1, 0, 0,
+                         stream, tsqr_f64_panel_t_used(n) ? T : nullptr);
 }
 
 int tsqr_f64_block_factor(const double* A, int64_t lda, int64_t rows, int64_t n, double* R,
