@@ -1715,11 +1715,18 @@ static int leaf_apply_impl(const double* Y, int64_t ldy, const double* tau, int6
                                                          base, C, ldc, ncols, Tin);
         } else {
           const size_t sm = DmmaApplySmem<128>::bytes;
-          int rc = prep(k_leaf_apply_dmma<128>, sm);
-          if (rc) return rc;
           dim3 gd((unsigned)P, (unsigned)((ncols + 127) / 128));
-          k_leaf_apply_dmma<128><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
-                                                          base, C, ldc, ncols, Tin);
+          if (base <= 1024) {  // short leaves: column-parallel dense first tile
+            int rc = prep(k_leaf_apply_dmma<128, true>, sm);
+            if (rc) return rc;
+            k_leaf_apply_dmma<128, true><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
+                                                                  (int)P, base, C, ldc, ncols, Tin);
+          } else {
+            int rc = prep(k_leaf_apply_dmma<128, false>, sm);
+            if (rc) return rc;
+            k_leaf_apply_dmma<128, false><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
+                                                                   (int)P, base, C, ldc, ncols, Tin);
+          }
         }
       } else LA_LAUNCH(128, 4, 16)
       break;
