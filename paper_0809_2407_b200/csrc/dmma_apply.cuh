@@ -39,6 +39,7 @@ struct DmmaApplySmem {
 struct DaPanel {
   double x[4], vb[2][2], tg, tq0, tq1;
 };
+template <bool TAUS = true>
 __device__ __forceinline__ void da_load_panel(DaPanel& P, const double* __restrict__ Yt,
                                               int64_t ldy, const double* __restrict__ tt, int valid,
                                               int n, int pc) {
@@ -56,9 +57,11 @@ __device__ __forceinline__ void da_load_panel(DaPanel& P, const double* __restri
       const int r = 8 * bb + g, c = pc + 2 * q + s;
       P.vb[bb][s] = (r < valid && c < n) ? __ldg(Yt + (int64_t)r * ldy + c) : 0.0;
     }
-  P.tg = (pc + g < n) ? __ldg(tt + pc + g) : 0.0;
-  P.tq0 = (pc + 2 * q < n) ? __ldg(tt + pc + 2 * q) : 0.0;
-  P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tt + pc + 2 * q + 1) : 0.0;
+  if constexpr (TAUS) {
+    P.tg = (pc + g < n) ? __ldg(tt + pc + g) : 0.0;
+    P.tq0 = (pc + 2 * q < n) ? __ldg(tt + pc + 2 * q) : 0.0;
+    P.tq1 = (pc + 2 * q + 1 < n) ? __ldg(tt + pc + 2 * q + 1) : 0.0;
+  }
 }
 
 // TR: tb[s] = T[2q+s][g] of the panel (the B operand of W'^T = W^T T, for Q^T)
@@ -146,12 +149,12 @@ __device__ __forceinline__ void da_dense_panel(double (&c)[2][32], const double*
 // DCP (KB = 128 only): the dense first tile column-parallel (below); chosen by the launcher for
 // short leaves, where a quarter to a half of the rows are dense first tiles (leaves of 512 rows:
 // 7.47 -> 6.92 ms on 16256 columns; leaves of 2048 rows measured 3% slower with it)
-template <int KB, bool DCP = false>
+template <int KB, bool DCP = false, bool HAST = false>
 __global__ void __launch_bounds__(THREADS, 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
                   int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
                   int64_t ncols, const double* __restrict__ Tin = nullptr) {
-  // Tin (nullable): the chain tiles' panel T stored by k_leaf_dmma (Tout), read instead of formed
+  // HAST: Tin holds the chain tiles' panel T stored by k_leaf_dmma (Tout), read instead of formed
   constexpr int H0 = WARPS * Geo<128>::HD, CB = KB / 8;  // dense first tile: 128 rows
   constexpr int DA_KB = KB, DA_LDC = DmmaApplySmem<KB>::LDC;
   extern __shared__ __align__(16) double sm[];
@@ -353,16 +356,16 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
     const double* Yt = Yl + row * ldy;
     const double* tt = tl + (int64_t)(t + 1) * n;
     DaPanel cur, nxt;
-    da_load_panel(cur, Yt, ldy, tt, valid, n, 0);
+    da_load_panel<!HAST>(cur, Yt, ldy, tt, valid, n, 0);
     // T of panel p+1 is formed in the same basic block as panel p's block
     // updates (its DMMA chain runs under them); for the last panel it works on
     // stale data and is discarded
     nxt = cur;
     double tb0, tb1;
-    const double2* Tt = Tin ? reinterpret_cast<const double2*>(Tin) +
-                                  ((int64_t)(leaf * (tau_stride / n) + t + 1) * 16) * 32 + lane
-                            : nullptr;
-    if (Tt) {
+    const double2* Tt = HAST ? reinterpret_cast<const double2*>(Tin) +
+                                   ((int64_t)(leaf * (tau_stride / n) + t + 1) * 16) * 32 + lane
+                             : nullptr;
+    if constexpr (HAST) {
       const double2 t2 = __ldg(Tt);
       tb0 = t2.x;
       tb1 = t2.y;
@@ -370,11 +373,11 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
       da_form_t(cur, tb0, tb1);
     }
     for (int p = 0; p < npan; ++p) {
-      if (p + 1 < npan) da_load_panel(nxt, Yt, ldy, tt, valid, n, 8 * (p + 1));
+      if (p + 1 < npan) da_load_panel<!HAST>(nxt, Yt, ldy, tt, valid, n, 8 * (p + 1));
       dr_wait(ver + p, t, lane);
       double* rrow = Cs + (8 * p + 2 * q) * DA_LDC + g;
       double tn0, tn1;
-      if (Tt) {
+      if constexpr (HAST) {
         const double2 t2 = __ldg(Tt + (p + 1 < npan ? p + 1 : p) * 32);
         tn0 = t2.x;
         tn1 = t2.y;

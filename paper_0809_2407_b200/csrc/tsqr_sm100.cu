@@ -1706,28 +1706,23 @@ static int leaf_apply_impl(const double* Y, int64_t ldy, const double* tau, int6
         // panel): 32-column blocks, 4x the CTAs at ~3x the T overhead per column
         // (C5: threshold 148 -> 466.6 ms, 296 -> 469.6, 592 -> 504.5)
         const bool narrow = P * ((ncols + 127) / 128) < 148;
-        if (narrow) {
-          const size_t sm = DmmaApplySmem<32>::bytes;
-          int rc = prep(k_leaf_apply_dmma<32>, sm);
-          if (rc) return rc;
-          dim3 gd((unsigned)P, (unsigned)((ncols + 31) / 32));
-          k_leaf_apply_dmma<32><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n, (int)P,
-                                                         base, C, ldc, ncols, Tin);
-        } else {
-          const size_t sm = DmmaApplySmem<128>::bytes;
-          dim3 gd((unsigned)P, (unsigned)((ncols + 127) / 128));
-          if (base <= 1024) {  // short leaves: column-parallel dense first tile
-            int rc = prep(k_leaf_apply_dmma<128, true>, sm);
-            if (rc) return rc;
-            k_leaf_apply_dmma<128, true><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
-                                                                  (int)P, base, C, ldc, ncols, Tin);
-          } else {
-            int rc = prep(k_leaf_apply_dmma<128, false>, sm);
-            if (rc) return rc;
-            k_leaf_apply_dmma<128, false><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, (int)n,
-                                                                   (int)P, base, C, ldc, ncols, Tin);
-          }
+#define AD_LAUNCH(KBV, DCPV, HASTV, GY)                                                            \
+        {                                                                                          \
+          const size_t sm = DmmaApplySmem<KBV>::bytes;                                             \
+          int rc = prep(k_leaf_apply_dmma<KBV, DCPV, HASTV>, sm);                                  \
+          if (rc) return rc;                                                                       \
+          dim3 gd((unsigned)P, (unsigned)(GY));                                                    \
+          k_leaf_apply_dmma<KBV, DCPV, HASTV><<<gd, THREADS, sm, st>>>(Y, ldy, tau, tau_stride, m, \
+              (int)n, (int)P, base, C, ldc, ncols, Tin);                                           \
         }
+        if (narrow) {
+          if (Tin) AD_LAUNCH(32, false, true, (ncols + 31) / 32) else AD_LAUNCH(32, false, false, (ncols + 31) / 32)
+        } else if (base <= 1024) {  // short leaves: column-parallel dense first tile
+          if (Tin) AD_LAUNCH(128, true, true, (ncols + 127) / 128) else AD_LAUNCH(128, true, false, (ncols + 127) / 128)
+        } else {
+          if (Tin) AD_LAUNCH(128, false, true, (ncols + 127) / 128) else AD_LAUNCH(128, false, false, (ncols + 127) / 128)
+        }
+#undef AD_LAUNCH
       } else LA_LAUNCH(128, 4, 16)
       break;
     }
