@@ -150,7 +150,7 @@ __device__ __forceinline__ void da_dense_panel(double (&c)[2][32], const double*
 // short leaves, where a quarter to a half of the rows are dense first tiles (leaves of 512 rows:
 // 7.47 -> 6.92 ms on 16256 columns; leaves of 2048 rows measured 3% slower with it)
 template <int KB, bool DCP = false, bool HAST = false>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, KB == 64 ? 2 : 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
                   int64_t tau_stride, int64_t m, int n, int P, int64_t base, double* C, int64_t ldc,
                   int64_t ncols, const double* __restrict__ Tin = nullptr) {
