@@ -3,21 +3,30 @@
 // Kernels (all FP64, see tsqr_device.cuh for the register layout).  Defaults
 // for n > 32 run on the FP64 tensor cores (mma.m8n8k4.f64, DMMA):
 //   k_leaf_dense    : dense first tile of a leaf that keeps Q (CTA sweep).    [a3]
+//   k_leaf_tt       : (tm_tall.cuh) R-only leaves of 64 < n <= 128: split-role ring
+//                     with 4 tiles of 64 rows in tensor memory, generation warps +
+//                     update warps, CTAs chaining consecutive leaves.  The C3 hot
+//                     kernel; <64,1,true> keeps the factors (opt-in format).    [a10]
+//   k_leaf_tm / k_leaf_split : (tm_leaf.cuh, split_leaf.cuh) the same ring with 16-row
+//                     tiles in tensor memory / shared memory (tuning fallbacks). [a10]
 //   k_leaf_dmma     : (dmma_ring.cuh) the leaf's flat chain of
 //                     triangle-on-rectangle tiles as a DMMA warp ring, 8-column
-//                     Level-2 panels + compact-WY updates; NP = 128 / 64 (/ 32).
-//                     The C3 hot kernel.                                       [a10]
+//                     Level-2 panels + compact-WY updates; NP = 128 / 64 (/ 32):
+//                     the leaves that keep Q (with the panel T for CAQR).       [a10]
 //   k_leaf_chain    : the rank-1 warp ring (n <= 32, tuning fallback).        [a10]
 //   k_leaf_narrow   : n <= 8, R only: lane-private rows + fused ticket tree.  [C4]
 //   k_tree_ring     : R-only stacked combine as a warp ring.                  [a9]
-//   k_tree_factor_dmma / k_tree_factor / k_tree_factor_w32 : stacked combine
-//                     with node factors (dmma: n <= 64, column-block warps).  [a9]
-//   k_tree_apply_dmma / k_tree_apply / k_tree_apply_w32 : Q or Q^T of a stacked
-//                     node on the two n-row blocks of C it acts on.       [a11,a12]
-//   k_leaf_apply_dmma (Q^T, 64 < n <= 128), k_leaf_q_dmma (Q, n <= 128; Q^T,
-//                     n <= 64), k_leaf_apply (reflector ring): a leaf chain's
-//                     Q / Q^T on the leaf's rows of C (explicit Q, apply_q, the
-//                     CAQR trailing update).                                [a6,a12]
+//   k_tree_factor_dmma128 / k_tree_factor_dmma / k_tree_factor / k_tree_factor_w32 :
+//                     stacked combine with node factors (dmma: column-block warps,
+//                     16 for 64 < n <= 128 in tree_factor128.cuh, 8 for n <= 64).  [a9]
+//   k_tree_apply_cp / k_tree_apply_dmma / k_tree_apply / k_tree_apply_w32 : Q or Q^T
+//                     of a stacked node on the two n-row blocks of C it acts on
+//                     (cp: column-parallel warps, 64 < n <= 128).           [a11,a12]
+//   k_leaf_apply_dmma (Q^T, 64 < n <= 128; with the kept panel T: 64-column CTAs,
+//                     two per SM), k_leaf_q_dmma (Q, n <= 128; Q^T, n <= 64),
+//                     k_tall_apply (both, 64-row chain tiles), k_leaf_apply
+//                     (reflector ring): a leaf chain's Q / Q^T on the leaf's rows
+//                     of C (explicit Q, apply_q, the CAQR trailing update).   [a6,a12]
 //   k_block_factor / k_block_apply : single-CTA DENSE / TRIRECT factorization
 //                     and apply of a small block (kernel-level API mirrors).
 //   k_peak_probe    : DFMA / DMMA throughput microbenchmark.
