@@ -84,10 +84,21 @@ k_tree_apply_cp(const double* __restrict__ Ynode, const double* __restrict__ tau
       Ca[j][k] = in ? Cag[(int64_t)r * ldc + g] : 0.0;
       Cb[j][k] = (in && !zero_partner) ? Cbg[(int64_t)r * ldc + g] : 0.0;
     }
-  // node Y -> shared memory, triangular (column c of panel p = c >> 3 has rows 0 .. 8p+7)
-  for (int idx = threadIdx.x; idx < 128 * 128; idx += THREADS) {
-    const int r = idx >> 7, c = idx & 127, p = c >> 3;
-    if (r < 8 * p + 8) sm[Sm::YS + Sm::ys_off(p) + r * LDY + (c & 7)] = (r < n && c < n) ? __ldg(Yn + (int64_t)r * n + c) : 0.0;
+  // node Y -> shared memory, triangular (column c of panel p = c >> 3 has rows 0 .. 8p+7):
+  // 8-byte cp.async, all in flight at once (a load-then-store loop spent ~15 us of the
+  // kernel's 31 here on L2 latency)
+  {
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(sm + Sm::YS);
+    for (int idx = threadIdx.x; idx < 128 * 128; idx += THREADS) {
+      const int r = idx >> 7, c = idx & 127, p = c >> 3;
+      if (r < 8 * p + 8) {
+        const bool ok = r < n && c < n;
+        cp_async<8>(sb + 8u * (unsigned)(Sm::ys_off(p) + r * LDY + (c & 7)), ok ? Yn + (int64_t)r * n + c : Yn,
+                    ok ? 8u : 0u);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
   }
   __syncthreads();
   for (int p = w; p < 16; p += WARPS) {  // T of panels w, w + 8
