@@ -105,12 +105,17 @@ k_tree_factor_dmma128(double* Rslots, int n, const int* __restrict__ ev, double*
   const int a = ev[3 * blockIdx.x], b = ev[3 * blockIdx.x + 1], id = ev[3 * blockIdx.x + 2];
   const double* Rag = Rslots + (int64_t)a * n * n;
   const double* Rbg = Rslots + (int64_t)b * n * n;
-  for (int i = threadIdx.x; i < Sm::YS; i += TF_W * 32) {  // panel-packed index -> (r, c)
-    int pp = 0;
-    while (pp + 1 < 16 && dr_pbase<128>(pp + 1) <= i) ++pp;
-    const int off = i - dr_pbase<128>(pp), ld = dr_ldr<128>(pp);
-    const int r = 8 * pp + off / ld, c = 8 * pp + off % ld;
-    Ra[i] = (r < n && c < n && c >= r) ? Rag[r * n + c] : 0.0;
+  {  // R_a -> the panel-packed pivot rows (row r of panel r >> 3: columns 8 (r >> 3) .. 127), cp.async
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(Ra);
+    for (int idx = threadIdx.x; idx < 128 * 128; idx += TF_W * 32) {
+      const int r = idx >> 7, c = idx & 127, pn = r >> 3;
+      if (c >= 8 * pn) {
+        const bool ok = r < n && c < n && c >= r;
+        cp_async<8>(sb + 8u * (unsigned)(dr_pbase<128>(pn) + (r & 7) * dr_ldr<128>(pn) + (c - 8 * pn)),
+                    ok ? Rag + r * n + c : Rag, ok ? 8u : 0u);
+      }
+    }
+    cp_async_commit();
   }
   if (threadIdx.x < 16) ver[threadIdx.x] = 0;
   // block w of R_b: rows 0 .. 8w+7 (groups 0 .. w/2), column 8w + g
@@ -123,6 +128,7 @@ k_tree_factor_dmma128(double* Rslots, int n, const int* __restrict__ ev, double*
       const int r = 16 * j + 8 * (k >> 1) + 2 * q + (k & 1), c = 8 * w + g;
       C[j][k] = (j < ngw && r < n && c < n && c >= r) ? Rbg[r * n + c] : 0.0;
     }
+  cp_async_wait<0>();
   __syncthreads();
   TF_TICK(k0_);
   const int npan = (n + 7) >> 3;
