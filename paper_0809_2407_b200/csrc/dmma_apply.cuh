@@ -183,11 +183,18 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
     constexpr int LDV = DA_LDC;
     double* Vs = Cs;
     double* tdn = Cs + DR_NP * DA_LDC;  // [16][64], before ver
-    for (int idx = threadIdx.x; idx < 128 * 128; idx += THREADS) {
-      const int r = idx >> 7, c = idx & 127;
-      double v = 0.0;
-      if (r < b && c < n) v = r > c ? __ldg(Yl + (int64_t)r * ldy + c) : (r == c ? 1.0 : 0.0);
-      Vs[r * LDV + c] = v;
+    {  // cp.async for the strict lower part (zero fill above it and past b / n), 1 on the diagonal
+      const unsigned sbv = (unsigned)__cvta_generic_to_shared(Vs);
+      for (int idx = threadIdx.x; idx < 128 * 128; idx += THREADS) {
+        const int r = idx >> 7, c = idx & 127;
+        if (r == c) {
+          Vs[r * LDV + c] = (r < b && c < n) ? 1.0 : 0.0;
+        } else {
+          const bool ok = r > c && r < b && c < n;
+          cp_async<8>(sbv + 8u * (unsigned)(r * LDV + c), ok ? Yl + (int64_t)r * ldy + c : Yl, ok ? 8u : 0u);
+        }
+      }
+      cp_async_commit();
     }
     double c[2][32];
 #pragma unroll
@@ -197,6 +204,7 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
         const int r = 8 * (k >> 1) + 2 * q + (k & 1), cc = 16 * w + 8 * j + g;
         c[j][k] = (r < b && cc < ncb) ? Cl[(int64_t)r * ldc + cc] : 0.0;
       }
+    cp_async_wait<0>();
     __syncthreads();
     for (int p = w; p < 16; p += WARPS) {
       const int pc = 8 * p;
