@@ -197,7 +197,7 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * 64-column CTAs, two per SM; 2 = 32-column CTAs, 3 = one CTA per SM); 0 = the
  * reflector-by-reflector warp ring.  n in (64, 128]: 128-column CTAs (the dense first tile
  * column-parallel for leaves of <= 1024 rows); with the kept panel T (tsqr_f64_leaf_apply_t)
- * 64-column CTAs, two per SM, for leaves over 1024 rows (3 = for every leaf). */
+ * 64-column CTAs, two per SM, dense first tile column-parallel. */
 #define CAQR_TUNE_DMMA_APPLY 10
 /* CAQR_TUNE_DMMA_Q: 1 (default) = Q C (explicit Q, apply_q) for leaves with 16-row chain tiles
  * and n <= 128 runs the DMMA ring backward (compact WY per 8-reflector panel, panels in reverse

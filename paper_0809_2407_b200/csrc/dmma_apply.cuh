@@ -28,8 +28,9 @@
 template <int KB>
 struct DmmaApplySmem {
   static constexpr int LDC = KB + 2;  // pivot-row stride (doubles)
-  static constexpr size_t doubles = (size_t)DR_NP * LDC;  // pivot rows (also the dense phase's W / G / V)
-  static constexpr size_t tdense = KB == 128 ? 16 * 64 : 0;  // the dense tile's 16 panel T (column-parallel phase)
+  // pivot rows (also the dense phase's W / G, or its staged V: 9 x 8 x 136 doubles, trapezoidal)
+  static constexpr size_t doubles = (size_t)DR_NP * LDC > 9792 ? (size_t)DR_NP * LDC : 9792;
+  static constexpr size_t tdense = KB >= 64 ? 16 * 64 : 0;  // the dense tile's 16 panel T (column-parallel phase)
   static constexpr size_t bytes = sizeof(double) * (doubles + tdense) + sizeof(int) * DR_NCB;
   static_assert(WARPS * 8 * KB + WARPS * 64 + 8 * KB <= DR_NP * LDC, "dense-phase scratch fits in Cs");
 };
@@ -112,43 +113,45 @@ __device__ __forceinline__ void da_form_t(const DaPanel& P, double& tb0, double&
   da_form_t_g<TR>(P, G, tb0, tb1);
 }
 
-// Panel P of the dense first tile on a warp's 16 columns (column-parallel dense phase of
-// k_leaf_apply_dmma<128>): c[j][2 rb + e] = C[8 rb + 2q + e][8j + g]; V (unit lower trapezoidal,
+// Panel P of the dense first tile on a warp's 8 NJ columns (column-parallel dense phase of
+// k_leaf_apply_dmma<64 NJ>): c[j][2 rb + e] = C[8 rb + 2q + e][8j + g]; V (unit lower trapezoidal,
 // zero above row 8P) staged in shared memory with row stride LDV; tb = T_P^T as the B operand.
-template <int P, int LDV>
-__device__ __forceinline__ void da_dense_panel(double (&c)[2][32], const double* Vs, const double* tdn,
+// offset of panel p in the staged V: rows 8p .. 127 of its 8 columns, row stride 9
+__host__ __device__ constexpr int da_voff(int p) { return 9 * (128 * p - 4 * p * (p - 1)); }
+template <int P, int NJ>
+__device__ __forceinline__ void da_dense_panel(double (&c)[NJ][32], const double* Vall, const double* tdn,
                                                int lane, int g, int q) {
+  constexpr int LDV = 9;
+  const double* Vs = Vall + da_voff(P) - 8 * P * LDV;  // row r of the panel at Vs[r * LDV + .]
   const double tb0 = tdn[P * 64 + 2 * lane], tb1 = tdn[P * 64 + 2 * lane + 1];
-  double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0}, v0[2] = {0.0, 0.0}, v1[2] = {0.0, 0.0};
+  double w0[NJ] = {}, w1[NJ] = {}, v0[NJ] = {}, v1[NJ] = {};
 #pragma unroll
   for (int rb = P; rb < 16; ++rb) {
-    const double y0 = Vs[(8 * rb + 2 * q) * LDV + 8 * P + g], y1 = Vs[(8 * rb + 2 * q + 1) * LDV + 8 * P + g];
+    const double y0 = Vs[(8 * rb + 2 * q) * LDV + g], y1 = Vs[(8 * rb + 2 * q + 1) * LDV + g];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       dmma(w0[j], w1[j], c[j][2 * rb], y0);
       dmma(v0[j], v1[j], c[j][2 * rb + 1], y1);
     }
   }
-  double u0[2] = {0.0, 0.0}, u1[2] = {0.0, 0.0};
+  double u0[NJ] = {}, u1[NJ] = {};
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < NJ; ++j) {
     dmma(u0[j], u1[j], w0[j] + v0[j], tb0);
     dmma(u0[j], u1[j], w1[j] + v1[j], tb1);
   }
 #pragma unroll
   for (int rb = P; rb < 16; ++rb) {
-    const double vb0 = Vs[(8 * rb + g) * LDV + 8 * P + 2 * q], vb1 = Vs[(8 * rb + g) * LDV + 8 * P + 2 * q + 1];
+    const double vb0 = Vs[(8 * rb + g) * LDV + 2 * q], vb1 = Vs[(8 * rb + g) * LDV + 2 * q + 1];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       dmma(c[j][2 * rb], c[j][2 * rb + 1], -u0[j], vb0);
       dmma(c[j][2 * rb], c[j][2 * rb + 1], -u1[j], vb1);
     }
   }
 }
 
-// DCP (KB = 128 only): the dense first tile column-parallel (below); chosen by the launcher for
-// short leaves, where a quarter to a half of the rows are dense first tiles (leaves of 512 rows:
-// 7.47 -> 6.92 ms on 16256 columns; leaves of 2048 rows measured 3% slower with it)
+// DCP (KB = 64 or 128): the dense first tile column-parallel (below)
 template <int KB, bool DCP = false, bool HAST = false>
 __global__ void __launch_bounds__(THREADS, KB == 64 ? 2 : 1)
 k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ tau,
@@ -159,7 +162,7 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
   constexpr int DA_KB = KB, DA_LDC = DmmaApplySmem<KB>::LDC;
   extern __shared__ __align__(16) double sm[];
   double* Cs = sm;
-  int* ver = reinterpret_cast<int*>(Cs + DR_NP * DA_LDC + DmmaApplySmem<KB>::tdense);
+  int* ver = reinterpret_cast<int*>(Cs + DmmaApplySmem<KB>::doubles + DmmaApplySmem<KB>::tdense);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int leaf = blockIdx.x;
@@ -173,35 +176,38 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
   const int64_t rest = b - H0;
   const int T = rest > 0 ? (int)((rest + DR_H - 1) / DR_H) : 0;
   const int npan = (n + 7) >> 3;
-  if constexpr (KB == 128 && DCP) {
+  if constexpr (KB >= 64 && DCP) {
+    constexpr int NJ = KB / 64;  // 8-column blocks per warp
     // Dense first tile, COLUMN-parallel (as k_tree_apply_cp): V (128 x 128, unit lower
     // trapezoidal, LAPACK layout) staged in the pivot-row area, the 16 panel T formed once per
     // CTA (warp w: panels w, w + 8), then warp w applies all 16 panels to its 16 columns x 128
     // rows in registers -- two barriers for the tile instead of two per panel (the row-split
     // phase below, kept for the 32-column CTAs), and rows above 8p are skipped.  A quarter to a
     // half of the rows of CAQR's late panels are dense first tiles.
-    constexpr int LDV = DA_LDC;
     double* Vs = Cs;
-    double* tdn = Cs + DR_NP * DA_LDC;  // [16][64], before ver
-    {  // cp.async for the strict lower part (zero fill above it and past b / n), 1 on the diagonal
+    double* tdn = Cs + DmmaApplySmem<KB>::doubles;  // [16][64], before ver
+    {  // V trapezoid (panel p: rows 8p .. 127): cp.async for the strict lower part (zero fill
+       // above it and past b / n), 1 on the diagonal
       const unsigned sbv = (unsigned)__cvta_generic_to_shared(Vs);
       for (int idx = threadIdx.x; idx < 128 * 128; idx += THREADS) {
-        const int r = idx >> 7, c = idx & 127;
+        const int r = idx >> 7, c = idx & 127, p = c >> 3;
+        if (r < 8 * p) continue;
+        const int o = da_voff(p) + (r - 8 * p) * 9 + (c & 7);
         if (r == c) {
-          Vs[r * LDV + c] = (r < b && c < n) ? 1.0 : 0.0;
+          Vs[o] = (r < b && c < n) ? 1.0 : 0.0;
         } else {
           const bool ok = r > c && r < b && c < n;
-          cp_async<8>(sbv + 8u * (unsigned)(r * LDV + c), ok ? Yl + (int64_t)r * ldy + c : Yl, ok ? 8u : 0u);
+          cp_async<8>(sbv + 8u * (unsigned)o, ok ? Yl + (int64_t)r * ldy + c : Yl, ok ? 8u : 0u);
         }
       }
       cp_async_commit();
     }
-    double c[2][32];
+    double c[NJ][32];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const int r = 8 * (k >> 1) + 2 * q + (k & 1), cc = 16 * w + 8 * j + g;
+        const int r = 8 * (k >> 1) + 2 * q + (k & 1), cc = 8 * NJ * w + 8 * j + g;
         c[j][k] = (r < b && cc < ncb) ? Cl[(int64_t)r * ldc + cc] : 0.0;
       }
     cp_async_wait<0>();
@@ -210,7 +216,8 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
       const int pc = 8 * p;
       double G[2] = {0.0, 0.0}, G2[2] = {0.0, 0.0};
       for (int rb = p; rb < 16; ++rb) {
-        const double y0 = Vs[(8 * rb + 2 * q) * LDV + pc + g], y1 = Vs[(8 * rb + 2 * q + 1) * LDV + pc + g];
+        const double* vp = Vs + da_voff(p) - pc * 9;
+        const double y0 = vp[(8 * rb + 2 * q) * 9 + g], y1 = vp[(8 * rb + 2 * q + 1) * 9 + g];
         dmma(G[0], G[1], y0, y0);
         dmma(G2[0], G2[1], y1, y1);
       }
@@ -227,16 +234,16 @@ k_leaf_apply_dmma(const double* __restrict__ Y, int64_t ldy, const double* __res
       tdn[p * 64 + 2 * lane + 1] = tb1;
     }
     __syncthreads();
-#define DA_DP(PV) if (PV < npan) da_dense_panel<PV, LDV>(c, Vs, tdn, lane, g, q);
+#define DA_DP(PV) if (PV < npan) da_dense_panel<PV, NJ>(c, Vs, tdn, lane, g, q);
     DA_DP(0) DA_DP(1) DA_DP(2) DA_DP(3) DA_DP(4) DA_DP(5) DA_DP(6) DA_DP(7)
     DA_DP(8) DA_DP(9) DA_DP(10) DA_DP(11) DA_DP(12) DA_DP(13) DA_DP(14) DA_DP(15)
 #undef DA_DP
     __syncthreads();  // every warp is done with V before the pivot rows take its place
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const int r = 8 * (k >> 1) + 2 * q + (k & 1), cc = 16 * w + 8 * j + g;
+        const int r = 8 * (k >> 1) + 2 * q + (k & 1), cc = 8 * NJ * w + 8 * j + g;
         if (r < n) Cs[r * DA_LDC + cc] = c[j][k];
         else if (r < b && cc < ncb) Cl[(int64_t)r * ldc + cc] = c[j][k];  // final rows
       }

@@ -1726,11 +1726,11 @@ static int leaf_apply_impl(const double* Y, int64_t ldy, const double* tau, int6
         }
         if (narrow) {
           if (Tin) AD_LAUNCH(32, false, true, (ncols + 31) / 32) else AD_LAUNCH(32, false, false, (ncols + 31) / 32)
-        } else if (Tin && (base > 1024 || g_dmma_apply == 3)) {
+        } else if (Tin) {
           // kept T: 64-column CTAs, two per SM (16 warps instead of 8 hide the fragment loads
-          // and the ring waits: 6.09 -> 5.85 ms on panel 0 of C5; without the kept T the
-          // doubled T formation costs more than that)
-          AD_LAUNCH(64, false, true, (ncols + 63) / 64)
+          // and the ring waits; without the kept T the doubled T formation costs more than
+          // that), dense first tile column-parallel (C5: 379.9 -> 341.9 ms)
+          AD_LAUNCH(64, true, true, (ncols + 63) / 64)
         } else if (base <= 1024) {  // short leaves: column-parallel dense first tile
           if (Tin) AD_LAUNCH(128, true, true, (ncols + 127) / 128) else AD_LAUNCH(128, true, false, (ncols + 127) / 128)
         } else {
