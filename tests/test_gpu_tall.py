@@ -138,3 +138,37 @@ def test_wide_tree_nodes_match_oracle(m, n, P):
         assert np.max(np.abs(QtC.cpu().numpy()[:n] - Q.T @ C)) <= 200 * n * EPS * np.max(np.abs(C))
         back = apply_q_device(f, QtC, transpose=False).cpu().numpy()
         assert np.max(np.abs(back - C)) <= 100 * n * EPS * np.max(np.abs(C))
+
+
+@pytest.mark.parametrize("kind", ["kappa1e12", "zero_columns", "duplicate_columns", "zero_matrix"])
+def test_wide_tsqr_degenerate_inputs(kind):
+    """n = 128 with kept factors on degenerate inputs (tau = 0 reflectors, sigma = 0 columns,
+    kappa = 1e12): the column-block tree factor, the column-parallel tree apply and the leaf
+    kernels keep the reference's bars (residual, orthogonality <= 10 n eps; pkg/tests/
+    test_householder.py:340-350)."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import explicit_q_device, factor_device
+
+    _lib.reset_tuning()
+    m, n, P = 6000, 128, 6
+    rng = philox(17)
+    if kind == "kappa1e12":
+        U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        A = (U * np.logspace(0, -12, n)) @ V.T
+    elif kind == "zero_columns":
+        A = rng.standard_normal((m, n))
+        A[:, [0, 5, 64, 127]] = 0.0
+    elif kind == "duplicate_columns":
+        A = rng.standard_normal((m, n))
+        A[:, 70:80] = A[:, 10:20]
+    else:
+        A = np.zeros((m, n))
+    f = factor_device(torch.from_numpy(A).cuda(), P, want_q=True)
+    Q = explicit_q_device(f).cpu().numpy()
+    R = f.R.cpu().numpy()
+    assert np.all(np.isfinite(Q)) and np.all(np.isfinite(R))
+    assert oracle.orthogonality(Q) <= 10 * n * EPS
+    scale = max(np.linalg.norm(A), 1e-300)
+    assert np.linalg.norm(A - Q @ R) <= 10 * n * EPS * scale + 0.0
+    assert np.allclose(np.tril(R, -1), 0.0)
