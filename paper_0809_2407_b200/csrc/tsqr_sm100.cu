@@ -1693,7 +1693,7 @@ static int leaf_apply_impl(const double* Y, int64_t ldy, const double* tau, int6
       if (var == 2) LQ_LAUNCH(64, 32, 2, true)
       else if (var == 3) LQ_LAUNCH(64, 64, 1, true)
       else LQ_LAUNCH(64, 64, 2, true)
-    } else if (p == 128) LQ_LAUNCH(128, 64, 1, false)
+    } else if (p == 128) LQ_LAUNCH(128, 64, 2, false)  // two CTAs per SM: 3.6% on factor + explicit Q
     else if (var == 2) LQ_LAUNCH(64, 32, 2, false)
     else if (var == 3) LQ_LAUNCH(64, 64, 1, false)
     else LQ_LAUNCH(64, 64, 2, false)
