@@ -158,6 +158,16 @@ def host_sample(cfg, rows):
     return out
 
 
+def _tree_note(P, n, q):
+    """How the leaves of one GPU are combined (CAQR_TUNE_FUSE, csrc/tsqr_sm100.cu r_binary_impl)."""
+    fuse = 148
+    if q == "none" and 64 < n <= 128 and P > 2 * fuse:
+        g = -(-P // fuse)
+        return (f"flat tree inside a CTA over {g} consecutive leaves ({-(-P // g)} CTAs), binary tree "
+                "above (hybrid tree, PAPER.md Fig. 3); CAQR_TUNE=16=0 gives the binary tree over all leaves")
+    return "binary tree over the leaves"
+
+
 def parity_vs_reference(cfg, R):
     """The timed run's R against the reference's R on the same input
     (tests/golden/fullsize_<cfg>.npz, made by oracle/make_fullsize.py from the
@@ -713,7 +723,8 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["name"], "m": m, "n": n, "leaf_rows": cfg["leaf"],
                        "leaves_per_gpu": P // chains, "gpu_chains_per_leaf": chains, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
                        "l2": "inputs larger than L2 (no flush needed)" if 8 * m * n > 256e6
-                       else "inputs smaller than L2"},
+                       else "inputs smaller than L2",
+                       "tree": _tree_note(P, n, cfg["q"])},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "clocks": clk.summary(), "gpu_launches": launches,
             "cuda_graph": graph is not None,
