@@ -158,13 +158,27 @@ def host_sample(cfg, rows):
     return out
 
 
-def _tree_note(P, n, q):
-    """How the leaves of one GPU are combined (CAQR_TUNE_FUSE, csrc/tsqr_sm100.cu r_binary_impl)."""
-    fuse = 148
-    if q == "none" and 64 < n <= 128 and P > 2 * fuse:
-        g = -(-P // fuse)
-        return (f"flat tree inside a CTA over {g} consecutive leaves ({-(-P // g)} CTAs), binary tree "
-                "above (hybrid tree, PAPER.md Fig. 3); CAQR_TUNE=16=0 gives the binary tree over all leaves")
+def _runs(m, P, n, q):
+    """(CTAs, rows per CTA) of the R-only wide leaf kernel on one GPU: csrc/tsqr_sm100.cu
+    r_binary_impl deals the rows to at most CAQR_TUNE_FUSE = 148 CTAs in whole 64-row tiles."""
+    fuse, base = 148, m // P
+    if q == "none" and 64 < n <= 128 and P > fuse:
+        b2 = max(128, -(-(-(-m // fuse)) // 64) * 64)
+        if b2 > base:
+            P2 = -(-m // b2)
+            if P2 > 1 and m - (P2 - 1) * b2 < n:
+                P2 -= 1
+            return P2, b2
+    return P, base
+
+
+def _tree_note(m, P, n, q):
+    """How the rows of one GPU are combined (CAQR_TUNE_FUSE, csrc/tsqr_sm100.cu r_binary_impl)."""
+    P2, b2 = _runs(m, P, n, q)
+    if P2 != P:
+        return (f"flat tree inside a CTA over runs of {b2} rows ({P2} CTAs, whole 64-row tiles), "
+                "binary tree above (hybrid tree, PAPER.md Fig. 3); CAQR_TUNE=16=0 gives the binary tree "
+                "over all leaves")
     return "binary tree over the leaves"
 
 
@@ -708,7 +722,8 @@ def run_ours(args, cfg):
         cb = cpu_baseline(cfg, budget_s=args.cpu_budget, threads=1)
         cpu = {"value": cb["value"], "unit": "GFLOP/s", "cores": 1, "kind": "port",
                "sample": cb["sample"]}
-    levels = max(0, int(np.ceil(np.log2(P)))) if P > 1 else 0
+    P_run = _runs(hi - lo, P, n, cfg["q"])[0]
+    levels = max(0, int(np.ceil(np.log2(P_run)))) if P_run > 1 else 0
     launches = (1 + levels) * args.steps
     if cfg["q"] == "explicit":
         launches += (levels + 1) * args.steps
@@ -724,7 +739,7 @@ def run_ours(args, cfg):
                        "leaves_per_gpu": P // chains, "gpu_chains_per_leaf": chains, "outputs": cfg["q"], "parallelism": f"1-D rows x{ws}",
                        "l2": "inputs larger than L2 (no flush needed)" if 8 * m * n > 256e6
                        else "inputs smaller than L2",
-                       "tree": _tree_note(P, n, cfg["q"])},
+                       "tree": _tree_note(hi - lo, P, n, cfg["q"])},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "clocks": clk.summary(), "gpu_launches": launches,
             "cuda_graph": graph is not None,

@@ -223,9 +223,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * 4 = 16 tiles of 16 rows in tensor memory (k_leaf_tm<16>), 3 = the same with 12 tiles,
  * 2 = the split-role ring with 8 tiles in shared memory, 0 = the DMMA warp ring. */
 #define CAQR_TUNE_CC 15
-/* CAQR_TUNE_FUSE: R-only binary-tree TSQR with n in (64, 128] and more than 2 x value leaves:
- * `value` CTAs (default 148, one per SM) each chain ceil(P / value) consecutive leaves into one
- * R (flat tree inside a CTA, binary tree across CTAs); 0 = one CTA and one tree leaf per leaf. */
+/* CAQR_TUNE_FUSE: R-only binary-tree TSQR with n in (64, 128] and more than `value` leaves:
+ * the rows are dealt to at most `value` CTAs (default 148, one per SM) in runs of whole 64-row
+ * tiles, each CTA chaining its run into one R (flat tree inside a CTA, binary tree across
+ * CTAs); 0 = one CTA and one tree leaf per leaf. */
 #define CAQR_TUNE_FUSE 16
 int caqr_tune(int key, int value);
 

@@ -1416,16 +1416,24 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
       return check_launch("cudaMemsetAsync");
     return launch_narrow(A, lda, m, n, P, base, Rslots, flag, P > 1 ? tickets : nullptr, st);
   }
-  // R only, more leaves than SMs: every CTA keeps folding the next leaf into the same R (the
-  // flat tree of Alg. 2 across the g consecutive leaves of one CTA, the binary tree above it --
-  // the hybrid tree of PAPER.md Fig. 3), instead of writing 2048 R factors and combining them
-  // in tree levels that are several waves wide (C3: 2.1 -> 0.8 ms of tree).  Leaves stay whole.
-  if (g_fuse && p == 128 && g_zstart && P > 2 * g_fuse) {
-    const int64_t g = (P + g_fuse - 1) / g_fuse;
-    P = (P + g - 1) / g;
-    base *= g;
-    levels = 0;
-    while ((1LL << levels) < P) ++levels;
+  // R only, more leaves than SMs: every CTA keeps folding the next rows into the same R (the
+  // flat tree of Alg. 2 inside a CTA, the binary tree above it -- the hybrid tree of PAPER.md
+  // Fig. 3), instead of writing 2048 R factors and combining them in tree levels that are
+  // several waves wide (C3: 2.1 -> 0.8 ms of tree).  The rows are dealt to g_fuse CTAs in runs
+  // of whole 64-row tiles, so one wave carries them evenly whatever P is (256 leaves on 148
+  // SMs would otherwise take two waves for 1.73 waves of work); any row partition gives the
+  // same R up to rounding and signs (section 5).
+  if (g_fuse && p == 128 && g_zstart && P > g_fuse) {
+    int64_t b2 = ((m + g_fuse - 1) / g_fuse + 63) / 64 * 64;
+    if (b2 < 128) b2 = 128;
+    if (b2 > base) {
+      int64_t P2 = (m + b2 - 1) / b2;
+      if (P2 > 1 && m - (P2 - 1) * b2 < n) --P2;  // a short tail rides with the last run
+      P = P2;
+      base = b2;
+      levels = 0;
+      while ((1LL << levels) < P) ++levels;
+    }
   }
   int rc = leaf_factor_impl(A, lda, m, n, P, base, nullptr, 0, nullptr, 0, Rslots, flag, stream);
   if (rc) return rc;

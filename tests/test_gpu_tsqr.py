@@ -787,15 +787,17 @@ def test_tall_tile_leaves_match_ring_and_lapack(cc):
 
 
 def test_fused_leaves_match_unfused_tree():
-    """CAQR_TUNE_FUSE (default 148): R-only TSQR with more than 2 x 148 leaves chains
-    ceil(P / 148) consecutive leaves per CTA (flat tree inside a CTA, binary tree above:
-    the hybrid tree of PAPER.md Fig. 3).  R agrees with the one-CTA-per-leaf binary tree
-    and with LAPACK within the R bar; a ragged last run of leaves is covered."""
+    """CAQR_TUNE_FUSE (default 148): R-only TSQR with more than 148 leaves deals the rows
+    to at most 148 CTAs in runs of whole 64-row tiles (flat tree inside a CTA, binary tree
+    above: the hybrid tree of PAPER.md Fig. 3).  R agrees with the one-CTA-per-leaf binary
+    tree and with LAPACK within the R bar; ragged last runs, a tail shorter than n that
+    rides with the last run, and 148 < P <= 296 are covered."""
     from paper_0809_2407_b200 import _lib
     from paper_0809_2407_b200.tsqr import factor_device
 
     try:
-        for (m, n, P) in [(600 * 256, 128, 600), (1000 * 130 + 77, 100, 1000), (297 * 128, 128, 297)]:
+        for (m, n, P) in [(600 * 256, 128, 600), (1000 * 130 + 77, 100, 1000), (297 * 128, 128, 297),
+                          (200 * 512, 128, 200), (19205, 100, 150)]:
             A = torch.from_numpy(philox(m).standard_normal((m, n))).cuda()
             _lib.tune(_lib.TUNE_FUSE, 148)
             Rf = factor_device(A, P).R.cpu().numpy()
