@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
 # DRAM bytes (read + write) over the 8mn algorithmic bytes, from this round's
 # ncu --set full captures (profiles/r02/*_ncu_summary.txt)
-NARROW8_TRAFFIC = (8.596103e9 + 10.115584e6) / (8.0 * 134217728 * 8)
+NARROW8_TRAFFIC = (8.592664e9 + 3.943936e6) / (8 * 134217728 * 8)  # ncu dram read + write / 8mn, profiles/r02/narrow8_kernel_ncu_summary.txt
 # k_leaf_tt<64, 1, false> at C3 full size, profiles/r02/leaf_tt_kernel_ncu_summary.txt
 DMMA_TRAFFIC = (17.376649e9 + 7.044608e6) / (8.0 * 16777216 * 128)
 METRIC = "TSQR fp64 GFLOP/s & % of roofline"
@@ -159,12 +159,14 @@ def host_sample(cfg, rows):
 
 
 def _runs(m, P, n, q):
-    """(CTAs, rows per CTA) of the R-only wide leaf kernel on one GPU: csrc/tsqr_sm100.cu
-    r_binary_impl deals the rows to at most CAQR_TUNE_FUSE = 148 CTAs in whole 64-row tiles."""
+    """(chains, rows per chain) of the R-only leaf kernels on one GPU: csrc/tsqr_sm100.cu
+    r_binary_impl deals the rows to at most CAQR_TUNE_FUSE = 148 CTAs in whole 64-row tiles
+    (64 < n <= 128), or to 148 x 8 warps in whole 256-row steps (n <= 8)."""
     fuse, base = 148, m // P
-    if q == "none" and 64 < n <= 128 and P > fuse:
-        b2 = max(128, -(-(-(-m // fuse)) // 64) * 64)
-        if b2 > base:
+    if q == "none" and (64 < n <= 128 or n <= 8):
+        W, g = (fuse, 64) if n > 8 else (8 * fuse, 256)
+        b2 = max(128, -(-(-(-m // W)) // g) * g)
+        if P > W and b2 > base:
             P2 = -(-m // b2)
             if P2 > 1 and m - (P2 - 1) * b2 < n:
                 P2 -= 1
@@ -176,7 +178,9 @@ def _tree_note(m, P, n, q):
     """How the rows of one GPU are combined (CAQR_TUNE_FUSE, csrc/tsqr_sm100.cu r_binary_impl)."""
     P2, b2 = _runs(m, P, n, q)
     if P2 != P:
-        return (f"flat tree inside a CTA over runs of {b2} rows ({P2} CTAs, whole 64-row tiles), "
+        who = "a CTA" if n > 8 else "a warp"
+        unit = "64-row tiles" if n > 8 else "256-row steps"
+        return (f"flat tree inside {who} over runs of {b2} rows ({P2} runs, whole {unit}), "
                 "binary tree above (hybrid tree, PAPER.md Fig. 3); CAQR_TUNE=16=0 gives the binary tree "
                 "over all leaves")
     return "binary tree over the leaves"
@@ -725,6 +729,8 @@ def run_ours(args, cfg):
     P_run = _runs(hi - lo, P, n, cfg["q"])[0]
     levels = max(0, int(np.ceil(np.log2(P_run)))) if P_run > 1 else 0
     launches = (1 + levels) * args.steps
+    if n <= 8 and cfg["q"] == "none":
+        launches = args.steps  # leaf kernel with the ticket tree fused (one kernel per step)
     if cfg["q"] == "explicit":
         launches += (levels + 1) * args.steps
     if is_caqr:

@@ -228,6 +228,10 @@ int tsqr_f64_block_apply(const double* Y, int64_t ldy, int64_t rows, int64_t n, 
  * tiles, each CTA chaining its run into one R (flat tree inside a CTA, binary tree across
  * CTAs); 0 = one CTA and one tree leaf per leaf. */
 #define CAQR_TUNE_FUSE 16
+/* CAQR_TUNE_NARROW_PF: how many 256-row steps ahead k_leaf_narrow8 prefetches into L2
+ * (default 1: measured 1.46 ms at C4 against 1.62 / 1.99 ms for 2 / 3 steps, whose lines are
+ * evicted again before they are read; 0 = no prefetch, 1.56 ms). */
+#define CAQR_TUNE_NARROW_PF 17
 int caqr_tune(int key, int value);
 
 /* FP64 pipe microbenchmark (mode 0 DFMA, 1 DMMA m8n8k4). */

@@ -152,13 +152,14 @@ TUNE_DMMA_TREE_FACTOR = 13
 TUNE_DMMA_DENSE = 14
 TUNE_CC = 15
 TUNE_FUSE = 16
+TUNE_NARROW_PF = 17
 
 
 # the library's defaults (csrc/tsqr_sm100.cu, g_ht / g_narrow / ... initialisers)
 TUNE_DEFAULTS = {TUNE_CHAIN_HT[32]: 16, TUNE_CHAIN_HT[64]: 16, TUNE_CHAIN_HT[128]: 16,
                  TUNE_NARROW: 3, TUNE_ZSTART: 1, TUNE_DMMA: 2,
                  TUNE_DMMA_APPLY: 1, TUNE_DMMA_Q: 1, TUNE_DMMA_TREE: 2,
-                 TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 5, TUNE_FUSE: 148}
+                 TUNE_DMMA_TREE_FACTOR: 1, TUNE_DMMA_DENSE: 0, TUNE_CC: 5, TUNE_FUSE: 148, TUNE_NARROW_PF: 1}
 
 
 def tune(key: int, value: int) -> None:

@@ -72,6 +72,7 @@ static int g_dmma_dense = 0;  // CAQR_TUNE_DMMA_DENSE: n <= 64 dense first tiles
 static int g_dmma_tree_factor = 1;  // CAQR_TUNE_DMMA_TREE_FACTOR: node factors on DMMA (n <= 64: 8 warps, n <= 128: 16)
 static int g_dmma_tree = 2;   // CAQR_TUNE_DMMA_TREE: Q / Q^T of the tree nodes on DMMA (2: column-parallel for n > 64)
 static int g_dmma_apply = 1;  // CAQR_TUNE_DMMA_APPLY: Q^T of n in (32,128] chain leaves on the DMMA ring
+static int g_narrow_pf = 1;   // CAQR_TUNE_NARROW_PF: k_leaf_narrow8 L2 prefetch distance in 256-row steps
 static int g_fuse = 148;      // CAQR_TUNE_FUSE: R-only n in (64,128]: CTAs (one per SM) that chain consecutive leaves; 0 off
 static int g_cc = 5;          // CAQR_TUNE_CC: R-only n in (64,128] leaves: 5 / 6 split-role ring with 4 / 8 tall
                               // tiles (64 / 32 rows) in TMEM, 4 / 3 with 16 / 12 tiles of 16 rows in TMEM,
@@ -410,12 +411,12 @@ __device__ __forceinline__ void narrow8_col(double (&R)[36], double (&B)[8][8],
 // scalars are amortised over 8 rows: ~30% fewer instructions per row).  No
 // staging buffer: the next step's column pair (2c, 2c+1) is loaded into the
 // registers of columns 2c, 2c+1 once reflector 2c+1 has consumed them, from
-// L2 (prefetched three steps ahead).  A shared-memory stage (cp.async one
+// L2 (prefetched one step ahead, CAQR_TUNE_NARROW_PF).  A shared-memory stage (cp.async one
 // step ahead, LDS at the step boundary) measured slower: 2.14 vs 1.78 ms.
 template <int W>
 __global__ void __launch_bounds__(W * 32, 1)
 k_leaf_narrow8(const double* __restrict__ A, int64_t m, int P, int64_t base, double* Rout, int* flag,
-               int* tickets) {
+               int* tickets, int pf) {
   constexpr int K = 8;
   const int lane = threadIdx.x & 31;
   const int leaf = blockIdx.x * W + (threadIdx.x >> 5);
@@ -447,11 +448,10 @@ k_leaf_narrow8(const double* __restrict__ A, int64_t m, int P, int64_t base, dou
       B[k][2 * c2 + 1] = t.y;
     }
   }
-  prefetch(1);
-  prefetch(2);
+  for (int i = 1; i < pf; ++i) prefetch(i);
   for (int64_t st = 0; st < steps; ++st) {
     const bool more = st + 1 < steps;
-    prefetch(st + 3);
+    if (pf) prefetch(st + pf);
     narrow8_col<0>(R, B, A2, st, more, b, lane);
     narrow8_col<1>(R, B, A2, st, more, b, lane);
     narrow8_col<2>(R, B, A2, st, more, b, lane);
@@ -1247,7 +1247,7 @@ static int launch_narrow(const double* A, int64_t lda, int64_t m, int64_t n, int
   if (g_narrow == 3 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // 16-byte rows, K = 8
     constexpr int W8 = 8;
     k_leaf_narrow8<W8><<<(int)((P + W8 - 1) / W8), W8 * 32, 0, st>>>(A, m, (int)P, base, R, flag,
-                                                                     tickets);
+                                                                     tickets, g_narrow_pf);
   } else if (g_narrow >= 2 && n == 8 && lda == 8 && (((uintptr_t)A & 15) == 0)) {  // cp.async 16 B granules
     NARROW_PIPE(4)
   } else {
@@ -1412,6 +1412,23 @@ static int r_binary_impl(const double* A, int64_t lda, int64_t m, int64_t n, int
   int levels = 0;
   while ((1LL << levels) < P) ++levels;
   if (n <= 8 && g_narrow) {
+    // More leaves than resident warps (8 per SM): deal the rows to g_fuse x 8 warps in runs of
+    // whole 256-row steps, one wave of CTAs, so the start-up loads and the lane / ticket
+    // combine of a leaf are paid once per warp instead of once per leaf (C4: 8192 leaves of
+    // 16384 rows were 7 waves of CTAs whose 8 warps start and finish together).
+    // (never more runs than leaves: Rslots and tickets are sized by the caller's P)
+    if (g_fuse && P > 8 * (int64_t)g_fuse) {
+      const int64_t W = 8 * (int64_t)g_fuse;
+      const int64_t b2 = ((m + W - 1) / W + 255) / 256 * 256;
+      if (b2 > base) {
+        int64_t P2 = (m + b2 - 1) / b2;
+        if (P2 > 1 && m - (P2 - 1) * b2 < n) --P2;
+        P = P2;
+        base = b2;
+        levels = 0;
+        while ((1LL << levels) < P) ++levels;
+      }
+    }
     if (P > 1 && cudaMemsetAsync(tickets, 0, sizeof(int) * (size_t)levels * P, st) != cudaSuccess)
       return check_launch("cudaMemsetAsync");
     return launch_narrow(A, lda, m, n, P, base, Rslots, flag, P > 1 ? tickets : nullptr, st);
@@ -1887,6 +1904,11 @@ int caqr_tune(int key, int value) {
   if (key == CAQR_TUNE_DMMA) {
     if (value < 0 || value > 3) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_DMMA takes 0 .. 3");
     g_dmma = value;
+    return CAQR_OK;
+  }
+  if (key == CAQR_TUNE_NARROW_PF) {
+    if (value < 0 || value > 64) return set_err(CAQR_ERR_ARG, "CAQR_TUNE_NARROW_PF takes 0 .. 64");
+    g_narrow_pf = value;
     return CAQR_OK;
   }
   if (key == CAQR_TUNE_FUSE) {

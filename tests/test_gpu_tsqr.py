@@ -811,6 +811,31 @@ def test_fused_leaves_match_unfused_tree():
         _lib.reset_tuning()
 
 
+@pytest.mark.parametrize("m,n,P", [(1500 * 2100, 8, 1500), (4000 * 300 + 123, 8, 4000),
+                                   (1300 * 2500 + 3, 5, 1300), (2048 * 1183 + 7, 8, 1200)])
+def test_narrow_runs_match_one_warp_per_leaf(m, n, P):
+    """CAQR_TUNE_FUSE for n <= 8: with more leaves than 148 x 8 the rows are dealt to
+    148 x 8 warps in runs of whole 256-row steps (one wave, flat tree inside a warp, ticket
+    tree above).  R agrees with the one-warp-per-leaf tree and with LAPACK; a tail shorter
+    than n rides with the last run (last case: 1183 runs of 2048 rows + 7 rows)."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = philox(m % 1000 + n).uniform(-1, 1, (m, n))
+    At = torch.from_numpy(A).cuda()
+    nrm = np.linalg.norm(A, 2)
+    try:
+        _lib.tune(_lib.TUNE_FUSE, 148)
+        Rf = factor_device(At, P).R.cpu().numpy()
+        assert np.array_equal(Rf, factor_device(At, P).R.cpu().numpy())
+        _lib.tune(_lib.TUNE_FUSE, 0)
+        R0 = factor_device(At, P).R.cpu().numpy()
+        assert oracle.r_diff(Rf, R0, nrm) <= 50 * EPS
+        assert oracle.r_diff(Rf, np.linalg.qr(A, mode="r"), nrm) <= 1000 * EPS
+    finally:
+        _lib.reset_tuning()
+
+
 @pytest.mark.parametrize("m,P", [(16384 * 5, 5), (16384 * 3 + 333, 3), (300, 1), (256 * 7 + 1, 2)])
 def test_narrow8_parity_and_variants(m, P):
     """CAQR_TUNE_NARROW = 3 (default for contiguous aligned n = 8): 8 rows per
