@@ -73,7 +73,9 @@ int tsqr_f64_leaf_factor(const double* A, int64_t lda, int64_t m, int64_t n, int
 
 /* R-only TSQR with the binary reduce tree (trees.py:52-66), everything on
  * device: the leaves of BlockRowLayout(m, n, P), then every tree level.  The
- * root R ends in Rslots[0] (P x n x n workspace).  tickets: device workspace
+ * root R ends in Rslots[0] (P x n x n workspace; with more leaves than the GPU has CTA or
+ * warp slots the rows are dealt to fewer, longer runs, CAQR_TUNE_FUSE below: the same R up to
+ * rounding, the other slots are scratch).  tickets: device workspace
  * of P * ceil(log2 P) ints (zeroed by the call; used by the fused-tree narrow
  * path for n <= 8, may be null otherwise). */
 int tsqr_f64_r_binary(const double* A, int64_t lda, int64_t m, int64_t n, int64_t P, double* Rslots,
