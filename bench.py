@@ -484,7 +484,8 @@ def run_ours(args, cfg):
     P = _leaves_for(hi - lo, n, cfg["leaf"])
     from paper_0809_2407_b200.tsqr import split_leaves
 
-    chains = 1 if is_caqr else split_leaves(hi - lo, n, P, fill=(n > 8 and cfg["q"] == "none"))
+    chains = 1 if is_caqr else split_leaves(hi - lo, n, P, fill=(n > 8 and cfg["q"] == "none"),
+                                                  narrow=(n <= 8 and cfg["q"] == "none"))
     P *= chains
     want_q = cfg["q"] != "none"
     stream = torch.cuda.current_stream(dev)

@@ -332,7 +332,7 @@ def _leaves_for(m: int, n: int, leaf_rows: int) -> int:
 
 
 def split_leaves(m: int, n: int, P: int, min_chains: int | None = None,
-                 min_rows: int = 512, fill: bool = False) -> int:
+                 min_rows: int = 512, fill: bool = False, narrow: bool = False) -> int:
     """GPU chains per leaf (a power of two) for a leaf count P.
 
     A leaf processed as 2^k equal chains whose R factors are combined by a
@@ -344,13 +344,23 @@ def split_leaves(m: int, n: int, P: int, min_chains: int | None = None,
     chains / (waves x SMs) instead; a further split must gain > 2% fill
     (measured: C3's per-GPU shard at 4 GPUs runs 10% faster as 2 chains per
     leaf; splitting R + Q or the narrow kernel's leaves only adds tree and
-    per-chain overhead, tools/prof_split.py).
+    per-chain overhead, tools/prof_split.py).  With ``narrow`` (R only, n <= 8:
+    one warp per chain, 8 warps per SM) the split goes on until there are more
+    chains than warp slots: the library then deals the rows to exactly one
+    wave of warps (CAQR_TUNE_FUSE; C4's per-GPU shard at 8 GPUs, 1024 leaves of
+    16384 rows, would otherwise run on 128 of the 148 SMs).
     """
     if min_chains is None:
         min_chains = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
     def ok(k):
         return m // (P * 2 * k) >= max(min_rows, 4 * n)
+
+    if narrow:
+        k = 1
+        while P * k <= 8 * min_chains and ok(k):
+            k *= 2
+        return k if P * k > 8 * min_chains else 1
 
     if not fill:
         k = 1
@@ -382,7 +392,10 @@ def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None =
     sign convention (beta = -sign(x0)||x||: mixed-sign diagonal).  A host
     matrix with q = "none" on the binary tree is streamed through the GPU in
     row chunks with the copies overlapped (``stream.tsqr_stream``; same
-    leaves and tree, bitwise-identical R); ``stream=False`` copies it whole.
+    leaves and tree, bitwise-identical R as long as no call has more leaves
+    than the GPU has CTA / warp slots -- beyond that the library deals the rows
+    of a call to longer runs, CAQR_TUNE_FUSE, and the two paths agree to
+    rounding); ``stream=False`` copies it whole.
     """
     if q not in ("none", "implicit", "explicit"):
         raise ValueError(f"q must be none / implicit / explicit, got {q!r}")
@@ -419,7 +432,7 @@ def tsqr(A, leaf_rows: int = 8192, q: str = "none", tree: ReductionTree | None =
     else:
         P = _leaves_for(m, n, leaf_rows)
         if split:
-            P *= split_leaves(m, n, P, fill=(n > 8 and q == "none"))
+            P *= split_leaves(m, n, P, fill=(n > 8 and q == "none"), narrow=(n <= 8 and q == "none"))
     f = factor_device(At, P, want_q=(q != "none"), tree=tree, counter=counter, host=host)
     if q == "none":
         return f.R_out()

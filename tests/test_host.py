@@ -220,6 +220,11 @@ def test_split_leaves_wave_fill():
     assert split_leaves(1 << 21, 128, 256, S, fill=True) == 4         # C3 per GPU at 8 GPUs
     assert split_leaves(1 << 24, 8, 1024, S) == 1                     # C4 per GPU at 8 GPUs
     assert split_leaves(4096, 64, 1, S) == 8                          # chains stay >= 512 rows
+    # n <= 8, R only: more chains than the 148 x 8 warp slots, which the library deals evenly
+    assert split_leaves(1 << 24, 8, 1024, S, narrow=True) == 2        # C4 per GPU at 8 GPUs
+    assert split_leaves(1 << 27, 8, 8192, S, narrow=True) == 1        # C4, 1 GPU
+    assert split_leaves(1 << 20, 8, 64, S, narrow=True) == 32         # 2048 chains of 512 rows
+    assert split_leaves(1 << 16, 8, 4, S, narrow=True) == 1           # too short to fill a wave
 
 
 def test_caqr_grid_layout_needs_a_distributed_job():
