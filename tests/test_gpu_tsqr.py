@@ -861,3 +861,42 @@ def test_narrow8_parity_and_variants(m, P):
         assert oracle.r_diff(factor_device(view, P).R.cpu().numpy(), Rl, nrm) <= 1000 * EPS
     finally:
         _lib.reset_tuning()
+
+
+def _dealing_cases():
+    rng = np.random.default_rng(20240809)
+    cases = []
+    for i in range(36):
+        wide = i % 2 == 0
+        n = int(rng.integers(65, 129)) if wide else int(rng.integers(1, 9))
+        P = int(rng.integers(149, 700)) if wide else int(rng.integers(1185, 5000))
+        leaf = int(rng.integers(n, 4 * n + 40)) if wide else int(rng.integers(max(n, 16), 700))
+        tail = int(rng.integers(0, leaf))
+        pad = int(rng.integers(0, 3)) * (1 if i % 3 else 0)  # lda > n for two cases in three
+        cases.append((P * leaf + tail, n, P, pad))
+    return cases
+
+
+@pytest.mark.parametrize("m,n,P,pad", _dealing_cases())
+def test_row_dealing_random_shapes(m, n, P, pad):
+    """R-only TSQR with more leaves than CTA (64 < n <= 128) or warp (n <= 8) slots, seeded
+    random shapes: ragged last leaves, leaves barely taller than n, strided views (lda > n).
+    The dealt runs give LAPACK's R within the R bar and the one-slot-per-leaf tree's R to a
+    few eps, and the same bits on a second call."""
+    from paper_0809_2407_b200 import _lib
+    from paper_0809_2407_b200.tsqr import factor_device
+
+    A = philox(m + 31 * n + P).standard_normal((m, n + pad))
+    At = torch.from_numpy(A).cuda()[:, :n]
+    A = A[:, :n]
+    nrm = np.linalg.norm(A, 2)
+    try:
+        Rf = factor_device(At, P).R.cpu().numpy()
+        assert np.array_equal(Rf, factor_device(At, P).R.cpu().numpy())
+        _lib.tune(_lib.TUNE_FUSE, 0)
+        R0 = factor_device(At, P).R.cpu().numpy()
+    finally:
+        _lib.reset_tuning()
+    assert np.array_equal(np.tril(Rf, -1), np.zeros_like(Rf))
+    assert oracle.r_diff(Rf, R0, nrm) <= 50 * EPS
+    assert oracle.r_diff(Rf, np.linalg.qr(A, mode="r"), nrm) <= 1000 * EPS
