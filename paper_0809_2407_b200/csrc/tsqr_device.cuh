@@ -309,13 +309,16 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
         for (int s2 = s; s2 < S; ++s2) {
           const int c = 32 * s2 + lane;
           if (s2 > s || lane > jj) {
+            // the partials of warps q0 .. q1, all loads in flight at once; two running sums by
+            // the parity of q: the same two sums as pairing from q0 (swapped when q0 is odd)
             double t0 = 0.0, t1 = 0.0;
-            int q = q0;
-            for (; q + 1 <= q1; q += 2) {
-              t0 += part[q * NP + c];
-              t1 += part[(q + 1) * NP + c];
+#pragma unroll
+            for (int q = 0; q < WARPS; ++q) {
+              const double pv = part[q * NP + c];
+              const double pz = (q >= q0 && q <= q1) ? pv : 0.0;
+              if (q & 1) t1 += pz;
+              else t0 += pz;
             }
-            if (q <= q1) t0 += part[q * NP + c];
             const double wv = tau * (t0 + t1);
 #pragma unroll
             for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
