@@ -221,17 +221,19 @@ __device__ __forceinline__ void house_lean(double x0, double sigma, double& beta
 // Block row r = w*RW + k.  tau_out[j] written by thread 0 (nullable).
 // smem: red[WARPS], sx0[1], part[WARPS*NP], vbuf[WARPS*RW].
 // ---------------------------------------------------------------------------
-template <int NP, int RW, int MODE>
-__device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps, int n,
-                                           double* tau_out, double* red, double* sx0,
-                                           double* part, double* vbuf) {
+// Columns 32 s .. 32 s + 31 (s a template parameter: with s a loop variable nvcc kept the
+// outer loop rolled -- the inner loop returns early -- and the tile X[.][s] went to local
+// memory, 587 LDL / STL in k_leaf_dense<128>).  Returns true when column n was reached.
+template <int NP, int RW, int MODE, int s>
+__device__ __forceinline__ bool cta_factor_seg(double (&X)[RW][NP / 32], double* Ps, int n,
+                                               double* tau_out, double* red, double* sx0,
+                                               double* part, double* vbuf) {
   constexpr int S = NP / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
+  {
     for (int jj = 0; jj < 32; ++jj) {
       const int j = 32 * s + jj;
-      if (j >= n) return;
+      if (j >= n) return true;
       const int pw = j / RW;
       // -- 1. partial sigma of column j over this warp's support rows
       double sga[4] = {0.0, 0.0, 0.0, 0.0};
@@ -246,10 +248,14 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
       const double sg = (sga[0] + sga[1]) + (sga[2] + sga[3]);
       if (lane == jj) red[w] = sg;
       if (MODE == DENSE && w == pw && lane == jj) {
+        // (selp in inline asm: written as `if (k == kk) x0 = X[k][s]` nvcc turns the chain into
+        // X[kk][s], a dynamic index that moves the whole tile X to local memory)
         double x0 = 0.0;
+        const int kk = j - pw * RW;
 #pragma unroll
         for (int k = 0; k < RW; ++k)
-          if (k == j - pw * RW) x0 = X[k][s];
+          asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\tselp.f64 %0, %1, %0, p;\n\t}"
+              : "+d"(x0) : "d"(X[k][s]), "r"(k), "r"(kk));
         *sx0 = x0;
       }
       __syncthreads();
@@ -284,14 +290,19 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
           }
         }
         __syncwarp();
+        // NP = 128: v stays in shared memory (warp-private segment, rewritten only after the
+        // next CTA barrier): 32 registers less where the tile alone takes 128
+#define VV(k) (NP == 128 ? vbuf[w * RW + (k)] : v[k])
+        if (NP != 128) {
 #pragma unroll
-        for (int k = 0; k < RW; ++k) v[k] = vbuf[w * RW + k];
+          for (int k = 0; k < RW; ++k) v[k] = vbuf[w * RW + k];
+        }
         // -- 3. partial dots with the trailing columns
 #pragma unroll
         for (int s2 = s; s2 < S; ++s2) {
           double pa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int k = 0; k < RW; ++k) pa[k & 3] = fma(v[k], X[k][s2], pa[k & 3]);
+          for (int k = 0; k < RW; ++k) pa[k & 3] = fma(VV(k), X[k][s2], pa[k & 3]);
           double p = (pa[0] + pa[1]) + (pa[2] + pa[3]);
           if (MODE != DENSE && w == 0) {
             pold[s2] = Ps[j * NP + 32 * s2 + lane];
@@ -321,7 +332,7 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
             }
             const double wv = tau * (t0 + t1);
 #pragma unroll
-            for (int k = 0; k < RW; ++k) X[k][s2] = fma(-v[k], wv, X[k][s2]);
+            for (int k = 0; k < RW; ++k) X[k][s2] = fma(-VV(k), wv, X[k][s2]);
             if (MODE != DENSE && w == 0) Ps[j * NP + c] = pold[s2] - wv;
           }
         }
@@ -329,6 +340,24 @@ __device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps,
       }
       if (threadIdx.x == 0 && tau_out) tau_out[j] = tau;
     }
+  }
+  return false;
+}
+
+#undef VV
+
+template <int NP, int RW, int MODE>
+__device__ __forceinline__ void cta_factor(double (&X)[RW][NP / 32], double* Ps, int n,
+                                           double* tau_out, double* red, double* sx0,
+                                           double* part, double* vbuf) {
+  constexpr int S = NP / 32;
+  if (cta_factor_seg<NP, RW, MODE, 0>(X, Ps, n, tau_out, red, sx0, part, vbuf)) return;
+  if constexpr (S > 1) {
+    if (cta_factor_seg<NP, RW, MODE, 1>(X, Ps, n, tau_out, red, sx0, part, vbuf)) return;
+  }
+  if constexpr (S > 2) {
+    if (cta_factor_seg<NP, RW, MODE, 2>(X, Ps, n, tau_out, red, sx0, part, vbuf)) return;
+    cta_factor_seg<NP, RW, MODE, 3>(X, Ps, n, tau_out, red, sx0, part, vbuf);
   }
 }
 
